@@ -1,0 +1,180 @@
+/*
+ * cmtf_b200.h -- C ABI of the B200-native S^3CMTF training path.
+ *
+ * This is the drop-in boundary for the reference's in-process C++ library
+ * API (CMake package cmtf::core, /root/reference/proj/core).  The reference
+ * has no FFI of its own; each entry point below names the reference
+ * function it replaces (file:line, relative to /root/reference/proj/core).
+ * Plain pointers and sizes only; no torch or CUDA types.  The C++ wrapper
+ * in include/cmtf_b200.hpp rebuilds the reference's signatures and
+ * exception types on top of it.
+ *
+ * Conventions (as the reference, include/cmtf/sparse_data.hpp:13-40):
+ *  - indices are 0-based u32, tensor entries AoS (order indices per entry),
+ *    matrix entries AoS pairs (row, col); values are f64 on the boundary and
+ *    f32 on the device;
+ *  - the core is row-major with the last mode fastest (src/tucker.cpp:49-54),
+ *    factors are row-major I_n x J_n, coupled factors cols x J_mode.
+ *
+ * Return codes: 0 ok, 1 validation (ValidationError), 2 divergence
+ * (DivergenceError), 3 CUDA error, 4 NCCL error, 5 unsupported.
+ * The message of the last failure is available from cmtf_gpu_last_error()
+ * (per calling thread) and cmtf_gpu_ctx_error(ctx).  A context is not
+ * thread-safe, as TrainState is not (include/cmtf/trainer.hpp:49-56).
+ */
+#ifndef CMTF_B200_H_
+#define CMTF_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMTF_OK 0
+#define CMTF_EVALIDATION 1
+#define CMTF_EDIVERGENCE 2
+#define CMTF_ECUDA 3
+#define CMTF_ENCCL 4
+#define CMTF_EUNSUPPORTED 5
+
+/* GradientKernel (include/cmtf/trainer.hpp:14) */
+#define CMTF_KERNEL_NAIVE 0
+#define CMTF_KERNEL_OPT 1
+
+/* Execution mode of an epoch on the device. */
+#define CMTF_EXEC_HOGWILD 0 /* lock-free parallel sweep (the product path) */
+#define CMTF_EXEC_SERIAL 1  /* exact reference order, P=1 semantics      */
+
+/* TrainConfig (include/cmtf/trainer.hpp:18-36) plus device fields. */
+typedef struct cmtf_gpu_config {
+  int32_t order;
+  const uint32_t *ranks; /* [order] */
+  double eta0;           /* default 1e-3 */
+  double mu;             /* default 0.1  */
+  double lambda_reg;     /* default 0.1  */
+  int32_t workers;       /* reference worker count; informs the core-step
+                            scale only in CMTF_EXEC_SERIAL (P=1 there)   */
+  int32_t max_epochs;    /* default 100  */
+  double rel_tol;        /* default 1e-4 */
+  uint64_t seed;
+  int32_t kernel;         /* CMTF_KERNEL_* */
+  int32_t core_structure; /* 0 dense Tucker; 1 CP (not yet on device)   */
+  int32_t nonnegative;    /* per-step clamp at 0 (src/trainer.cpp:185) */
+  double init_scale;      /* default 1.0 */
+  /* ---- device fields ---- */
+  int32_t device;        /* CUDA ordinal */
+  int32_t exec_mode;     /* CMTF_EXEC_* */
+  int32_t hog_threads;   /* concurrent Hogwild workers; 0 = auto        */
+  int32_t sort_mode;     /* mode the COO is sorted by; -1 = auto        */
+  int32_t force_generic; /* 1: use the generic-N kernels even when a
+                            specialised one exists (testing)            */
+} cmtf_gpu_config;
+
+typedef struct cmtf_gpu_ctx cmtf_gpu_ctx;
+
+/* Fills defaults exactly as TrainConfig's member initialisers. */
+void cmtf_gpu_config_default(cmtf_gpu_config *cfg);
+
+const char *cmtf_gpu_last_error(void);
+const char *cmtf_gpu_ctx_error(const cmtf_gpu_ctx *ctx);
+/* ABI version, bumped on any signature change. */
+int32_t cmtf_gpu_abi_version(void);
+
+int cmtf_gpu_create(const cmtf_gpu_config *cfg, cmtf_gpu_ctx **out);
+int cmtf_gpu_destroy(cmtf_gpu_ctx *ctx);
+
+/* DataBundle (include/cmtf/sparse_data.hpp:80-84) built from the training
+ * SparseTensor (:17-40) and CoupledMatrix list (:44-70); counts as
+ * count_mode_occurrences (src/sparse_data.cpp:344-362) are derived on the
+ * device.  Range and finiteness are validated as check_entries
+ * (src/sparse_data.cpp:19-64); duplicate detection is the caller's
+ * (the reference rejects duplicates when the SparseTensor is constructed). */
+int cmtf_gpu_set_tensor(cmtf_gpu_ctx *ctx, const uint32_t *dims,
+                        const uint32_t *idx, const double *vals, uint64_t nnz);
+int cmtf_gpu_add_matrix(cmtf_gpu_ctx *ctx, int32_t mode0, uint32_t rows,
+                        uint32_t cols, const uint32_t *idx, const double *vals,
+                        uint64_t nnz, double weight);
+/* Drops the matrices (for re-uploading a bundle into the same context). */
+int cmtf_gpu_clear_matrices(cmtf_gpu_ctx *ctx);
+
+/* initialize / make_state (src/trainer.cpp:94-103,130-137): the seeded
+ * random model (draw law of random_model, src/trainer.cpp:30-58), epoch 0,
+ * eta = eta0, schedule = build_schedule. */
+int cmtf_gpu_make_state(cmtf_gpu_ctx *ctx);
+
+/* Model transfer (host f64 <-> device f32).  couplings may be NULL when
+ * there are no matrices. */
+int cmtf_gpu_set_model(cmtf_gpu_ctx *ctx, const double *core,
+                       const double *const *factors,
+                       const double *const *couplings);
+int cmtf_gpu_get_model(cmtf_gpu_ctx *ctx, double *core, double *const *factors,
+                       double *const *couplings);
+int cmtf_gpu_get_state(cmtf_gpu_ctx *ctx, int32_t *epoch, double *eta);
+int cmtf_gpu_set_state(cmtf_gpu_ctx *ctx, int32_t epoch, double eta);
+
+/* run_epoch (src/trainer.cpp:267-316): one sweep over every training entry
+ * and matrix entry, then epoch += 1, eta = eta0 / (1 + mu * epoch), and the
+ * non-finite scan (returns CMTF_EDIVERGENCE with the reference's message).
+ * Serial mode replays the reference schedule (build_schedule +
+ * shuffle_schedule, src/trainer.cpp:114-128) on the device. */
+int cmtf_gpu_run_epoch(cmtf_gpu_ctx *ctx);
+
+/* epoch_stats (src/eval.cpp:120-144). */
+int cmtf_gpu_epoch_stats(cmtf_gpu_ctx *ctx, double lambda_reg,
+                         double *train_rmse, double *objective);
+
+/* test_rmse (src/eval.cpp:101-107) for a held-out tensor. */
+int cmtf_gpu_test_rmse(cmtf_gpu_ctx *ctx, const uint32_t *idx,
+                       const double *vals, uint64_t nnz, double *rmse);
+
+/* matrix_rmse (src/eval.cpp:109-118) for coupled matrix m of the bundle. */
+int cmtf_gpu_matrix_rmse(cmtf_gpu_ctx *ctx, int32_t m, double *rmse);
+
+/* train (src/trainer.cpp:318-346) without the QR finalisation: epochs until
+ * |delta rmse| / rmse < rel_tol or max_epochs.  log receives 4 doubles per
+ * epoch (epoch, train_rmse, objective, seconds); capacity in entries. */
+int cmtf_gpu_train(cmtf_gpu_ctx *ctx, double *log, int32_t log_capacity,
+                   int32_t *n_log);
+
+/* Per-entry probe at the frozen model: compute_gradient(_opt)
+ * (src/gradients.cpp:83-223) for training entries ids[0..n).  grow holds
+ * n * (J_1 + ... + J_N) row gradients, gcore n * prod(J) core gradients
+ * (may be NULL), xhat / residual n values each (may be NULL). */
+int cmtf_gpu_entry_grads(cmtf_gpu_ctx *ctx, const uint64_t *ids, uint64_t n,
+                         double *xhat, double *residual, double *grow,
+                         double *gcore);
+
+/* Stateless batched form of compute_gradient / compute_gradient_opt
+ * (include/cmtf/gradients.hpp:59-74): n independent entries, each with its
+ * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core. */
+int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order,
+                              const uint32_t *ranks, const double *core,
+                              uint64_t n, const double *x, const double *rows,
+                              const uint32_t *counts, double lambda_reg,
+                              uint64_t nnz_total, int32_t with_core,
+                              double *grow, double *gcore, double *residual,
+                              int32_t device);
+
+/* Batched matrix_entry_gradients (include/cmtf/gradients.hpp:83-86). */
+int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double *y,
+                                    const double *u, const double *v,
+                                    double lambda_m, double lambda_reg,
+                                    const uint32_t *col_count, double *du,
+                                    double *dv, double *residual,
+                                    int32_t device);
+
+/* Timing and introspection for the harness.  Events bracket the last
+ * run_epoch on the launching stream.  kernel_ms[0..3] = tensor sweep,
+ * matrix sweep(s), non-finite scan, total; launches = kernels launched. */
+int cmtf_gpu_last_epoch_timing(cmtf_gpu_ctx *ctx, double *kernel_ms,
+                               int32_t *launches);
+/* Which tensor kernel the context selected: 0 generic, 1 specialised N=3,
+ * 2 specialised N=4; hog_threads actually used. */
+int cmtf_gpu_kernel_info(cmtf_gpu_ctx *ctx, int32_t *which,
+                         int32_t *hog_threads, int32_t *sort_mode);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMTF_B200_H_ */

@@ -1,0 +1,1451 @@
+// context.cu -- C ABI (include/cmtf_b200.h) of the B200 S^3CMTF path:
+// device-resident DataBundle and model, the epoch driver (run_epoch /
+// train), evaluation, per-entry probes.  Host logic mirrors the reference
+// trainer (/root/reference/proj/core/src/trainer.cpp) and is native C++;
+// every O(nnz) step runs on the device.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/cmtf_b200.h"
+#include "common.cuh"
+#include "generic.cuh"
+#include "hog3.cuh"
+
+using namespace cmtfb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DevMatrix {
+  int mode = 0;
+  uint32_t rows = 0, cols = 0;
+  uint64_t nnz = 0;
+  double weight = 1.0;
+  uint32_t* rec = nullptr;   // sorted by row, 3 words
+  uint32_t* pos = nullptr;   // entry id -> sorted position
+  uint32_t* count = nullptr; // per col
+  float* vreg = nullptr;     // lambda_m * lambda / count
+  float* V = nullptr;        // cols x JP
+};
+
+}  // namespace
+
+struct cmtf_gpu_ctx {
+  cmtf_gpu_config cfg{};
+  std::vector<uint32_t> ranks;
+  int order = 0;
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // bundle
+  std::vector<uint32_t> dims;
+  uint64_t nnz = 0;
+  int sort_mode = 0;
+  uint32_t* rec = nullptr;  // sorted tensor records, (order+1) words
+  uint32_t* pos = nullptr;  // training id -> sorted position
+  uint32_t* count[kMaxOrder] = {};
+  float* reg[kMaxOrder] = {};
+  std::vector<DevMatrix> mats;
+  std::vector<DevMatrix> spare;  // parked by clear_matrices
+
+  // model
+  float* U[kMaxOrder] = {};
+  float* G = nullptr;
+  bool have_model = false;
+
+  // state (TrainState, include/cmtf/trainer.hpp:49-56)
+  int32_t epoch = 0;
+  double eta = 0.0;
+  std::vector<uint64_t> schedule;  // serial mode only
+  uint64_t* d_sched = nullptr;
+  uint64_t d_sched_cap = 0;
+
+  // scratch
+  double* d_partial = nullptr;
+  uint64_t partial_cap = 0;
+  unsigned long long* d_first = nullptr;
+
+  // timing
+  cudaEvent_t ev[6] = {};
+  double last_ms[4] = {0, 0, 0, 0};
+  int32_t last_launches = 0;
+  int kernel_which = 0;
+  int hog_threads_used = 0;
+
+  uint32_t J(int n) const { return ranks[n]; }
+  uint32_t JP(int n) const { return (uint32_t)round_up4((int)ranks[n]); }
+  uint64_t core_size() const {
+    uint64_t s = 1;
+    for (auto j : ranks) s *= j;
+    return s;
+  }
+};
+
+namespace {
+
+int set_err(cmtf_gpu_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CU(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return set_err(ctx, CMTF_ECUDA, "CUDA error %s at %s:%d: %s",           \
+                     cudaGetErrorName(e_), __FILE__, __LINE__,                \
+                     cudaGetErrorString(e_));                                 \
+  } while (0)
+
+#define TRY(expr)             \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ != CMTF_OK) return rc_; \
+  } while (0)
+
+// splitmix-mixed mt19937_64 streams (src/rng.cpp:8-26, rng.hpp:11-36).
+uint64_t splitmix64(uint64_t& s) {
+  s += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+std::mt19937_64 make_rng(uint64_t seed, uint64_t stream, uint64_t index) {
+  uint64_t state = seed;
+  uint64_t mixed = splitmix64(state);
+  state ^= stream * 0xd1b54a32d192ed03ULL;
+  mixed ^= splitmix64(state);
+  state ^= index * 0x9e3779b97f4a7c15ULL;
+  mixed ^= splitmix64(state);
+  return std::mt19937_64(mixed);
+}
+inline double uniform01(std::mt19937_64& g) {
+  return static_cast<double>(g() >> 11) * 0x1.0p-53;
+}
+inline uint64_t bounded(std::mt19937_64& g, uint64_t n) {
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(g()) * n) >> 64);
+}
+
+template <typename T>
+int dalloc(cmtf_gpu_ctx* ctx, T** p, size_t n) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CU(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+  return CMTF_OK;
+}
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// ---------------- preprocessing kernels ----------------
+__global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals,
+                                   uint64_t nnz, int order, ModeTables mt,
+                                   int sort_mode, uint32_t* rec, uint32_t* keys,
+                                   uint32_t* ids, unsigned long long* bad) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    for (int n = 0; n < order; ++n) {
+      const uint32_t i = idx[e * order + n];
+      if (i >= mt.dims[n]) {
+        atomicMin(&bad[0], (unsigned long long)e);
+        continue;
+      }
+      atomicAdd(const_cast<uint32_t*>(mt.count[n]) + i, 1u);
+      rec[e * (order + 1) + n] = i;
+    }
+    const double v = vals[e];
+    if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
+    rec[e * (order + 1) + order] = __float_as_uint((float)v);
+    keys[e] = idx[e * order + sort_mode];
+    ids[e] = (uint32_t)e;
+  }
+}
+
+__global__ void gather_records_kernel(const uint32_t* src, const uint32_t* ids,
+                                      uint64_t n, int words, uint32_t* dst,
+                                      uint32_t* pos) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[s];
+    for (int w = 0; w < words; ++w) dst[s * words + w] = src[(uint64_t)id * words + w];
+    pos[id] = (uint32_t)s;
+  }
+}
+
+__global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
+                           float* reg) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * blockDim.x)
+    reg[i] = count[i] ? lambda / (float)count[i] : 0.f;
+}
+
+__global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
+                                   uint64_t nnz, uint32_t rows, uint32_t cols,
+                                   uint32_t* rec, uint32_t* keys, uint32_t* ids,
+                                   uint32_t* count, unsigned long long* bad) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = idx[2 * e], j = idx[2 * e + 1];
+    if (i >= rows || j >= cols) atomicMin(&bad[0], (unsigned long long)e);
+    else atomicAdd(count + j, 1u);
+    const double v = vals[e];
+    if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
+    rec[3 * e] = i;
+    rec[3 * e + 1] = j;
+    rec[3 * e + 2] = __float_as_uint((float)v);
+    keys[e] = i;
+    ids[e] = (uint32_t)e;
+  }
+}
+
+unsigned grid_for(uint64_t n, unsigned bt = 256) {
+  uint64_t g = (n + bt - 1) / bt;
+  if (g > 148ull * 32) g = 148ull * 32;
+  if (g == 0) g = 1;
+  return (unsigned)g;
+}
+
+// Sort 32-bit keys with 32-bit ids (stable LSD radix sort).
+int sort_ids(cmtf_gpu_ctx* ctx, uint32_t* keys, uint32_t* ids, uint64_t n,
+             uint32_t max_key, uint32_t** sorted_ids_out) {
+  uint32_t *keys_out = nullptr, *ids_out = nullptr;
+  TRY(dalloc(ctx, &keys_out, n));
+  TRY(dalloc(ctx, &ids_out, n));
+  int end_bit = 1;
+  while (end_bit < 32 && (1ull << end_bit) <= max_key) ++end_bit;
+  size_t temp = 0;
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys, keys_out, ids, ids_out,
+                                     (int64_t)n, 0, end_bit, ctx->stream));
+  void* d_temp = nullptr;
+  CU(cudaMalloc(&d_temp, temp ? temp : 1));
+  CU(cub::DeviceRadixSort::SortPairs(d_temp, temp, keys, keys_out, ids, ids_out,
+                                     (int64_t)n, 0, end_bit, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_temp);
+  cudaFree(keys_out);
+  *sorted_ids_out = ids_out;
+  return CMTF_OK;
+}
+
+ModeTables mode_tables(const cmtf_gpu_ctx* ctx) {
+  ModeTables mt{};
+  for (int n = 0; n < ctx->order; ++n) {
+    mt.U[n] = ctx->U[n];
+    mt.reg[n] = ctx->reg[n];
+    mt.count[n] = ctx->count[n];
+    mt.J[n] = ctx->J(n);
+    mt.JP[n] = ctx->JP(n);
+    mt.dims[n] = n < (int)ctx->dims.size() ? ctx->dims[n] : 0;
+  }
+  return mt;
+}
+
+CoreShape core_shape(const cmtf_gpu_ctx* ctx) {
+  CoreShape cs{};
+  cs.order = ctx->order;
+  uint32_t off = 0;
+  for (int n = 0; n < ctx->order; ++n) {
+    cs.J[n] = ctx->ranks[n];
+    cs.off[n] = off;
+    off += ctx->ranks[n];
+  }
+  cs.off[ctx->order] = off;
+  cs.size = (uint32_t)ctx->core_size();
+  return cs;
+}
+
+int ensure_partials(cmtf_gpu_ctx* ctx, uint64_t n) {
+  if (n <= ctx->partial_cap) return CMTF_OK;
+  TRY(dalloc(ctx, &ctx->d_partial, n));
+  ctx->partial_cap = n;
+  return CMTF_OK;
+}
+
+// blocked_sum's pairwise combine over block partials (src/eval.cpp:46-48).
+double pairwise(std::vector<double>& p) {
+  if (p.empty()) return 0.0;
+  for (size_t width = 1; width < p.size(); width *= 2)
+    for (size_t i = 0; i + width < p.size(); i += 2 * width) p[i] += p[i + width];
+  return p[0];
+}
+
+bool fast3_supported(const cmtf_gpu_ctx* ctx, int* J) {
+  if (ctx->order != 3 || ctx->cfg.force_generic) return false;
+  if (ctx->ranks[0] != ctx->ranks[1] || ctx->ranks[1] != ctx->ranks[2]) return false;
+  const int j = (int)ctx->ranks[0];
+  if (j != 2 && j != 4 && j != 5 && j != 8 && j != 10 && j != 16 && j != 20) return false;
+  *J = j;
+  return true;
+}
+
+template <int J, bool OPT, int CM>
+int launch_hog3_t(cmtf_gpu_ctx* ctx, const Hog3Args& args, int threads) {
+  constexpr int BT = J >= 16 ? 128 : 256;
+  auto kern = hog3_kernel<J, J, J, OPT, CM, BT>;
+  const size_t smem = Hog3Layout<J, J, J>::template B<BT>::bytes();
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BT, smem));
+  if (per_sm < 1) per_sm = 1;
+  int blocks = ctx->num_sms * per_sm;
+  if (threads > 0) blocks = std::max(1, threads / BT);
+  else {
+    // auto: keep at least ~64 entries per worker (staleness)
+    const uint64_t cap = std::max<uint64_t>(1, args.nnz / (64ull * BT));
+    blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
+  }
+  ctx->hog_threads_used = blocks * BT;
+  kern<<<blocks, BT, smem, ctx->stream>>>(args);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+template <int J>
+int launch_hog3_j(cmtf_gpu_ctx* ctx, const Hog3Args& args, bool opt, int cm,
+                  int threads) {
+  if (opt) {
+    if (cm == 0) return launch_hog3_t<J, true, 0>(ctx, args, threads);
+    if (cm == 1) return launch_hog3_t<J, true, 1>(ctx, args, threads);
+    return launch_hog3_t<J, true, 2>(ctx, args, threads);
+  }
+  if (cm == 0) return launch_hog3_t<J, false, 0>(ctx, args, threads);
+  if (cm == 1) return launch_hog3_t<J, false, 1>(ctx, args, threads);
+  return launch_hog3_t<J, false, 2>(ctx, args, threads);
+}
+
+int launch_hog3(cmtf_gpu_ctx* ctx, int J, const Hog3Args& args, bool opt,
+                int cm, int threads) {
+  switch (J) {
+    case 2: return launch_hog3_j<2>(ctx, args, opt, cm, threads);
+    case 4: return launch_hog3_j<4>(ctx, args, opt, cm, threads);
+    case 5: return launch_hog3_j<5>(ctx, args, opt, cm, threads);
+    case 8: return launch_hog3_j<8>(ctx, args, opt, cm, threads);
+    case 10: return launch_hog3_j<10>(ctx, args, opt, cm, threads);
+    case 16: return launch_hog3_j<16>(ctx, args, opt, cm, threads);
+    case 20: return launch_hog3_j<20>(ctx, args, opt, cm, threads);
+  }
+  return set_err(ctx, CMTF_EUNSUPPORTED, "no specialised kernel for J=%d", J);
+}
+
+template <int J>
+int launch_eval3_t(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
+                   double* partial) {
+  constexpr int J3P = round_up4(J);
+  const size_t smem = sizeof(float) * (size_t)(J * J * J3P + round_up4(J) * 256);
+  auto kern = eval3_kernel<J, J, J>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  const unsigned nb = (unsigned)((nnz + kEvalBlock - 1) / kEvalBlock);
+  kern<<<nb, 256, smem, ctx->stream>>>(reinterpret_cast<const uint4*>(rec), nnz,
+                                       ctx->U[0], ctx->U[1], ctx->U[2], ctx->G,
+                                       partial);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+// Tensor SSE over a record array (sorted or not) -> deterministic double.
+int tensor_sse(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
+               double* out) {
+  if (nnz == 0) {
+    *out = 0.0;
+    return CMTF_OK;
+  }
+  const uint64_t nb = (nnz + kEvalBlock - 1) / kEvalBlock;
+  TRY(ensure_partials(ctx, nb));
+  int J = 0;
+  if (fast3_supported(ctx, &J)) {
+    switch (J) {
+      case 2: TRY(launch_eval3_t<2>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 4: TRY(launch_eval3_t<4>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 5: TRY(launch_eval3_t<5>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 8: TRY(launch_eval3_t<8>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 10: TRY(launch_eval3_t<10>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 16: TRY(launch_eval3_t<16>(ctx, rec, nnz, ctx->d_partial)); break;
+      case 20: TRY(launch_eval3_t<20>(ctx, rec, nnz, ctx->d_partial)); break;
+    }
+  } else {
+    const CoreShape cs = core_shape(ctx);
+    const int bt = 256;
+    const size_t smem = sizeof(float) * (cs.size + (bt / 32) * cs.off[cs.order]);
+    CU(cudaFuncSetAttribute(eval_generic_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    eval_generic_kernel<<<(unsigned)nb, bt, smem, ctx->stream>>>(
+        cs, ctx->G, rec, nnz, mode_tables(ctx), ctx->d_partial);
+    CU(cudaGetLastError());
+  }
+  std::vector<double> h(nb);
+  CU(cudaMemcpyAsync(h.data(), ctx->d_partial, nb * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out = pairwise(h);
+  return CMTF_OK;
+}
+
+int matrix_sse(cmtf_gpu_ctx* ctx, const DevMatrix& m, double* out) {
+  if (m.nnz == 0) {
+    *out = 0.0;
+    return CMTF_OK;
+  }
+  const uint64_t nb = (m.nnz + kEvalBlock - 1) / kEvalBlock;
+  TRY(ensure_partials(ctx, nb));
+  eval_matrix_kernel<<<(unsigned)nb, 256, 0, ctx->stream>>>(
+      m.rec, m.nnz, ctx->U[m.mode], m.V, ctx->J(m.mode), ctx->JP(m.mode),
+      ctx->d_partial);
+  CU(cudaGetLastError());
+  std::vector<double> h(nb);
+  CU(cudaMemcpyAsync(h.data(), ctx->d_partial, nb * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out = pairwise(h);
+  return CMTF_OK;
+}
+
+int row_norms(cmtf_gpu_ctx* ctx, const float* F, uint32_t rows, uint32_t J,
+              uint32_t JP, const uint32_t* count, double* out) {
+  const unsigned nb = std::min<unsigned>(grid_for(rows), 1024);
+  TRY(ensure_partials(ctx, nb));
+  row_norms_kernel<<<nb, 256, 0, ctx->stream>>>(F, rows, J, JP, count,
+                                                ctx->d_partial);
+  CU(cudaGetLastError());
+  std::vector<double> h(nb);
+  CU(cudaMemcpyAsync(h.data(), ctx->d_partial, nb * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  double s = 0.0;
+  for (double v : h) s += v;
+  *out = s;
+  return CMTF_OK;
+}
+
+int require_bundle(cmtf_gpu_ctx* ctx) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (!ctx->rec) return set_err(ctx, CMTF_EVALIDATION, "no training tensor set");
+  if (!ctx->have_model)
+    return set_err(ctx, CMTF_EVALIDATION, "no model (call cmtf_gpu_make_state)");
+  return CMTF_OK;
+}
+
+// find_non_finite (src/trainer.cpp:239-263) on the device.
+int scan_nonfinite(cmtf_gpu_ctx* ctx, std::string* offender) {
+  const int narr = 1 + ctx->order + (int)ctx->mats.size();
+  CU(cudaMemsetAsync(ctx->d_first, 0xff, sizeof(unsigned long long) * narr,
+                     ctx->stream));
+  const uint64_t core = ctx->core_size();
+  nonfinite_kernel<<<grid_for(core), 256, 0, ctx->stream>>>(
+      ctx->G, 1, (uint32_t)core, (uint32_t)core, ctx->d_first);
+  for (int n = 0; n < ctx->order; ++n)
+    nonfinite_kernel<<<grid_for((uint64_t)ctx->dims[n] * ctx->JP(n)), 256, 0,
+                       ctx->stream>>>(ctx->U[n], ctx->dims[n], ctx->J(n),
+                                      ctx->JP(n), ctx->d_first + 1 + n);
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto& M = ctx->mats[m];
+    nonfinite_kernel<<<grid_for((uint64_t)M.cols * ctx->JP(M.mode)), 256, 0,
+                       ctx->stream>>>(M.V, M.cols, ctx->J(M.mode),
+                                      ctx->JP(M.mode),
+                                      ctx->d_first + 1 + ctx->order + m);
+  }
+  CU(cudaGetLastError());
+  ctx->last_launches += narr;
+  std::vector<unsigned long long> h(narr);
+  CU(cudaMemcpyAsync(h.data(), ctx->d_first, sizeof(unsigned long long) * narr,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  offender->clear();
+  const unsigned long long none = ~0ull;
+  if (h[0] != none) {
+    *offender = "core element " + std::to_string(h[0] + 1);
+    return CMTF_OK;
+  }
+  for (int n = 0; n < ctx->order; ++n)
+    if (h[1 + n] != none) {
+      const uint64_t cols = ctx->J(n);
+      *offender = "factor " + std::to_string(n + 1) + ", row " +
+                  std::to_string(h[1 + n] / cols + 1) + ", column " +
+                  std::to_string(h[1 + n] % cols + 1);
+      return CMTF_OK;
+    }
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto v = h[1 + ctx->order + m];
+    if (v != none) {
+      const uint64_t cols = ctx->J(ctx->mats[m].mode);
+      *offender = "coupled factor " + std::to_string(m + 1) + ", row " +
+                  std::to_string(v / cols + 1) + ", column " +
+                  std::to_string(v % cols + 1);
+      return CMTF_OK;
+    }
+  }
+  return CMTF_OK;
+}
+
+int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M, float eta) {
+  if (M.nnz == 0) return CMTF_OK;
+  const int JP = (int)ctx->JP(M.mode);
+  const int bt = 256;
+  uint64_t threads = std::min<uint64_t>((uint64_t)ctx->num_sms * 2048,
+                                        std::max<uint64_t>(bt, M.nnz / 16));
+  if (ctx->cfg.hog_threads > 0) threads = (uint64_t)ctx->cfg.hog_threads;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, threads / bt);
+  const float w = (float)M.weight;
+  float* U = ctx->U[M.mode];
+#define MS_CASE(JPV)                                                           \
+  case JPV:                                                                   \
+    matrix_sweep_kernel<JPV><<<blocks, bt, 0, ctx->stream>>>(                   \
+        M.rec, M.nnz, U, M.V, M.vreg, w, eta, ctx->cfg.nonnegative);          \
+    break;
+  switch (JP) {
+    MS_CASE(4) MS_CASE(8) MS_CASE(12) MS_CASE(16) MS_CASE(20) MS_CASE(24)
+    MS_CASE(28) MS_CASE(32) MS_CASE(36) MS_CASE(40) MS_CASE(44) MS_CASE(48)
+    MS_CASE(52) MS_CASE(56) MS_CASE(60) MS_CASE(64)
+    default:
+      return set_err(ctx, CMTF_EUNSUPPORTED, "matrix rank %d unsupported",
+                     (int)ctx->J(M.mode));
+  }
+#undef MS_CASE
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
+  const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
+  int J = 0;
+  if (fast3_supported(ctx, &J)) {
+    Hog3Args a{};
+    a.rec = reinterpret_cast<const uint4*>(ctx->rec);
+    a.nnz = ctx->nnz;
+    for (int n = 0; n < 3; ++n) {
+      a.U[n] = ctx->U[n];
+      a.reg[n] = ctx->reg[n];
+    }
+    a.G = ctx->G;
+    a.eta = eta;
+    a.eta_core = eta;
+    a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+    a.nonneg = ctx->cfg.nonnegative;
+    ctx->kernel_which = 1;
+    return launch_hog3(ctx, J, a, opt, ctx->sort_mode, ctx->cfg.hog_threads);
+  }
+  ctx->kernel_which = 0;
+  HogArgs a{};
+  a.cs = core_shape(ctx);
+  a.G = ctx->G;
+  a.rec = ctx->rec;
+  a.nnz = ctx->nnz;
+  a.mt = mode_tables(ctx);
+  a.eta = eta;
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.nonneg = ctx->cfg.nonnegative;
+  const int bt = 256;
+  const size_t smem =
+      sizeof(float) * (2 * a.cs.size + (bt / 32) * 2 * a.cs.off[a.cs.order]);
+  auto kern = opt ? hogwild_generic_kernel<true> : hogwild_generic_kernel<false>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bt, smem));
+  if (per_sm < 1) per_sm = 1;
+  int blocks = ctx->num_sms * per_sm;
+  if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / 32 / (bt / 32));
+  else {
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (16ull * (bt / 32)));
+    blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
+  }
+  ctx->hog_threads_used = blocks * (bt / 32);
+  kern<<<blocks, bt, smem, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+int serial_epoch(cmtf_gpu_ctx* ctx, float eta) {
+  // build_schedule / shuffle_schedule (src/trainer.cpp:114-128), applied to
+  // the persisted schedule so shuffles accumulate across epochs.
+  uint64_t total = ctx->nnz;
+  for (auto& m : ctx->mats) total += m.nnz;
+  if (ctx->schedule.size() != total) {
+    ctx->schedule.resize(total);
+    for (uint64_t i = 0; i < total; ++i) ctx->schedule[i] = i;
+  }
+  auto rng = make_rng(ctx->cfg.seed, 0x02, (uint64_t)ctx->epoch);
+  for (uint64_t i = total; i > 1; --i)
+    std::swap(ctx->schedule[i - 1], ctx->schedule[bounded(rng, i)]);
+  if (ctx->d_sched_cap < total) {
+    TRY(dalloc(ctx, &ctx->d_sched, total));
+    ctx->d_sched_cap = total;
+  }
+  CU(cudaMemcpyAsync(ctx->d_sched, ctx->schedule.data(), total * sizeof(uint64_t),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  SerialArgs a{};
+  a.cs = core_shape(ctx);
+  a.G = ctx->G;
+  a.rec = ctx->rec;
+  a.pos = ctx->pos;
+  a.mt = mode_tables(ctx);
+  a.nnz = ctx->nnz;
+  a.n_mat = (int)ctx->mats.size();
+  a.mat_base[0] = ctx->nnz;
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto& M = ctx->mats[m];
+    a.mats[m] = MatDev{M.mode, M.rows, M.cols, M.nnz, M.rec, M.pos,
+                       M.V, M.vreg, M.count, (float)M.weight};
+    a.mat_base[m + 1] = a.mat_base[m] + M.nnz;
+  }
+  a.sched = ctx->d_sched;
+  a.n_sched = total;
+  a.eta = eta;
+  a.eta_core = eta;  // P = 1: core step eta (src/trainer.cpp:211-219)
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.nonneg = ctx->cfg.nonnegative;
+  const int bt = 256;
+  const size_t smem = sizeof(float) * (a.cs.size + 2 * a.cs.off[a.cs.order] + 32);
+  auto kern = ctx->cfg.kernel == CMTF_KERNEL_OPT ? serial_epoch_kernel<true>
+                                                  : serial_epoch_kernel<false>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  kern<<<1, bt, smem, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  ctx->kernel_which = 0;
+  ctx->hog_threads_used = 1;
+  return CMTF_OK;
+}
+
+int validate_config(const cmtf_gpu_config* c) {
+  if (!c) return set_err(nullptr, CMTF_EVALIDATION, "null config");
+  if (c->order < 2 || c->order > kMaxOrder)
+    return set_err(nullptr, CMTF_EVALIDATION,
+                   "tensor order must be between 2 and %d on the device", kMaxOrder);
+  if (!c->ranks) return set_err(nullptr, CMTF_EVALIDATION, "null ranks");
+  uint64_t size = 1;
+  for (int n = 0; n < c->order; ++n) {
+    if (c->ranks[n] == 0)
+      return set_err(nullptr, CMTF_EVALIDATION, "ranks must be positive");
+    if (c->ranks[n] > (uint32_t)kMaxRank)
+      return set_err(nullptr, CMTF_EUNSUPPORTED, "rank %u exceeds device limit %d",
+                     c->ranks[n], kMaxRank);
+    size *= c->ranks[n];
+  }
+  if (size > (uint64_t)kMaxCore)
+    return set_err(nullptr, CMTF_EUNSUPPORTED,
+                   "core of %llu elements exceeds device limit %d",
+                   (unsigned long long)size, kMaxCore);
+  if (c->core_structure != 0)
+    return set_err(nullptr, CMTF_EUNSUPPORTED,
+                   "CP core structure is not implemented on the device yet");
+  // src/trainer.cpp:79-91
+  if (!(c->eta0 >= 0)) return set_err(nullptr, CMTF_EVALIDATION, "eta0 must be nonnegative");
+  if (!(c->mu >= 0)) return set_err(nullptr, CMTF_EVALIDATION, "mu must be nonnegative");
+  if (!(c->lambda_reg >= 0))
+    return set_err(nullptr, CMTF_EVALIDATION, "lambda_reg must be nonnegative");
+  if (c->workers < 1) return set_err(nullptr, CMTF_EVALIDATION, "workers must be >= 1");
+  if (c->max_epochs < 0)
+    return set_err(nullptr, CMTF_EVALIDATION, "max_epochs must be nonnegative");
+  if (!(c->rel_tol >= 0)) return set_err(nullptr, CMTF_EVALIDATION, "rel_tol must be nonnegative");
+  if (!(c->init_scale > 0))
+    return set_err(nullptr, CMTF_EVALIDATION, "init_scale must be positive");
+  if (c->kernel != CMTF_KERNEL_NAIVE && c->kernel != CMTF_KERNEL_OPT)
+    return set_err(nullptr, CMTF_EVALIDATION, "unknown kernel %d", c->kernel);
+  if (c->exec_mode != CMTF_EXEC_HOGWILD && c->exec_mode != CMTF_EXEC_SERIAL)
+    return set_err(nullptr, CMTF_EVALIDATION, "unknown exec mode %d", c->exec_mode);
+  return CMTF_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+void cmtf_gpu_config_default(cmtf_gpu_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->eta0 = 1e-3;
+  c->mu = 0.1;
+  c->lambda_reg = 0.1;
+  c->workers = 1;
+  c->max_epochs = 100;
+  c->rel_tol = 1e-4;
+  c->seed = 0;
+  c->kernel = CMTF_KERNEL_OPT;
+  c->init_scale = 1.0;
+  c->exec_mode = CMTF_EXEC_HOGWILD;
+  c->sort_mode = -1;
+}
+
+const char* cmtf_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* cmtf_gpu_ctx_error(const cmtf_gpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+int32_t cmtf_gpu_abi_version(void) { return 1; }
+
+int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
+  cmtf_gpu_ctx* ctx = nullptr;
+  if (!out) return set_err(nullptr, CMTF_EVALIDATION, "null output pointer");
+  *out = nullptr;
+  TRY(validate_config(cfg));
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_err(nullptr, CMTF_ECUDA, "no CUDA device available (%s)",
+                   cudaGetErrorString(e));
+  if (cfg->device < 0 || cfg->device >= ndev)
+    return set_err(nullptr, CMTF_EVALIDATION, "device %d out of range", cfg->device);
+  ctx = new cmtf_gpu_ctx();
+  ctx->cfg = *cfg;
+  ctx->order = cfg->order;
+  ctx->ranks.assign(cfg->ranks, cfg->ranks + cfg->order);
+  ctx->cfg.ranks = ctx->ranks.data();
+  ctx->device = cfg->device;
+  ctx->eta = cfg->eta0;
+  auto cleanup = [&](int rc) {
+    delete ctx;
+    return rc;
+  };
+  if (cudaSetDevice(ctx->device) != cudaSuccess)
+    return cleanup(set_err(nullptr, CMTF_ECUDA, "cudaSetDevice failed"));
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  if (cudaMalloc(&ctx->d_first, sizeof(unsigned long long) * (1 + kMaxOrder + kMaxMats)) !=
+      cudaSuccess)
+    return cleanup(set_err(nullptr, CMTF_ECUDA, "allocation failed"));
+  *out = ctx;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
+  if (!ctx) return CMTF_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  dfree(ctx->rec);
+  dfree(ctx->pos);
+  for (int n = 0; n < kMaxOrder; ++n) {
+    dfree(ctx->count[n]);
+    dfree(ctx->reg[n]);
+    dfree(ctx->U[n]);
+  }
+  for (auto& m : ctx->mats) {
+    dfree(m.rec);
+    dfree(m.pos);
+    dfree(m.count);
+    dfree(m.vreg);
+    dfree(m.V);
+  }
+  for (auto& m : ctx->spare) dfree(m.V);
+  dfree(ctx->G);
+  dfree(ctx->d_sched);
+  dfree(ctx->d_partial);
+  dfree(ctx->d_first);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
+                        const uint32_t* idx, const double* vals, uint64_t nnz) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  CU(cudaSetDevice(ctx->device));
+  const int N = ctx->order;
+  if (nnz == 0) return set_err(ctx, CMTF_EVALIDATION, "training tensor has no entries");
+  if (nnz >= 0xffffffffull)
+    return set_err(ctx, CMTF_EUNSUPPORTED, "nnz >= 2^32 per device; shard the tensor");
+  for (int n = 0; n < N; ++n) {
+    if (dims[n] == 0) return set_err(ctx, CMTF_EVALIDATION, "mode sizes must be positive");
+    // validate_config: rank <= dim unless nonnegative (src/trainer.cpp:70-76)
+    if (!ctx->cfg.nonnegative && ctx->ranks[n] > dims[n])
+      return set_err(ctx, CMTF_EVALIDATION,
+                     "rank of mode %d exceeds its size; orthogonalization needs J_n <= I_n",
+                     n + 1);
+  }
+  const bool same_shape =
+      ctx->dims.size() == (size_t)N && std::equal(ctx->dims.begin(), ctx->dims.end(), dims);
+  ctx->dims.assign(dims, dims + N);
+  ctx->nnz = nnz;
+  if (!same_shape) ctx->have_model = false;
+  int sm = ctx->cfg.sort_mode;
+  if (sm < 0 || sm >= N) {
+    sm = 0;  // auto: the mode with the most rows (ties: lowest index)
+    for (int n = 1; n < N; ++n)
+      if (dims[n] > dims[sm]) sm = n;
+  }
+  ctx->sort_mode = sm;
+
+  uint32_t* d_idx = nullptr;
+  double* d_vals = nullptr;
+  uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
+  TRY(dalloc(ctx, &d_idx, nnz * N));
+  TRY(dalloc(ctx, &d_vals, nnz));
+  TRY(dalloc(ctx, &d_rec, nnz * (N + 1)));
+  TRY(dalloc(ctx, &d_keys, nnz));
+  TRY(dalloc(ctx, &d_ids, nnz));
+  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  for (int n = 0; n < N; ++n) {
+    TRY(dalloc(ctx, &ctx->count[n], dims[n]));
+    TRY(dalloc(ctx, &ctx->reg[n], dims[n]));
+    CU(cudaMemsetAsync(ctx->count[n], 0, dims[n] * sizeof(uint32_t), ctx->stream));
+  }
+  CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+  ModeTables mt = mode_tables(ctx);
+  pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+      d_idx, d_vals, nnz, N, mt, sm, d_rec, d_keys, d_ids, ctx->d_first);
+  CU(cudaGetLastError());
+  unsigned long long bad[2];
+  CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_idx);
+  cudaFree(d_vals);
+  if (bad[0] != ~0ull || bad[1] != ~0ull) {
+    cudaFree(d_rec);
+    cudaFree(d_keys);
+    cudaFree(d_ids);
+    dfree(ctx->rec);
+    if (bad[0] != ~0ull) {
+      const uint64_t e = bad[0];
+      for (int n = 0; n < N; ++n)
+        if (idx[e * N + n] >= dims[n])
+          return set_err(ctx, CMTF_EVALIDATION,
+                         "tensor index out of range: mode %d index %u > size %u", n + 1,
+                         idx[e * N + n] + 1, dims[n]);
+    }
+    return set_err(ctx, CMTF_EVALIDATION, "tensor value is not finite");
+  }
+  uint32_t* sorted_ids = nullptr;
+  TRY(sort_ids(ctx, d_keys, d_ids, nnz, dims[sm], &sorted_ids));
+  cudaFree(d_keys);
+  cudaFree(d_ids);
+  TRY(dalloc(ctx, &ctx->rec, nnz * (N + 1)));
+  TRY(dalloc(ctx, &ctx->pos, nnz));
+  gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+      d_rec, sorted_ids, nnz, N + 1, ctx->rec, ctx->pos);
+  CU(cudaGetLastError());
+  for (int n = 0; n < N; ++n)
+    reg_kernel<<<grid_for(dims[n]), 256, 0, ctx->stream>>>(
+        ctx->count[n], dims[n], (float)ctx->cfg.lambda_reg, ctx->reg[n]);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_rec);
+  cudaFree(sorted_ids);
+  // model buffers (allocated with the bundle's shapes; kept on re-upload of a
+  // same-shaped bundle, as run_epoch(state, bundle) keeps the state's model)
+  if (!same_shape || !ctx->G) {
+    for (int n = 0; n < N; ++n)
+      TRY(dalloc(ctx, &ctx->U[n], (uint64_t)dims[n] * ctx->JP(n)));
+    TRY(dalloc(ctx, &ctx->G, ctx->core_size()));
+    ctx->have_model = false;
+  }
+  return CMTF_OK;
+}
+
+int cmtf_gpu_clear_matrices(cmtf_gpu_ctx* ctx) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  for (auto& v : ctx->spare) dfree(v.V);
+  ctx->spare.clear();
+  for (auto& m : ctx->mats) {
+    dfree(m.rec);
+    dfree(m.pos);
+    dfree(m.count);
+    dfree(m.vreg);
+    ctx->spare.push_back(m);  // coupled factor kept for a same-shaped re-add
+  }
+  ctx->mats.clear();
+  return CMTF_OK;
+}
+
+int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
+                        uint32_t cols, const uint32_t* idx, const double* vals,
+                        uint64_t nnz, double weight) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (ctx->dims.empty())
+    return set_err(ctx, CMTF_EVALIDATION, "set the tensor before adding matrices");
+  CU(cudaSetDevice(ctx->device));
+  // CoupledMatrix ctor + make_bundle checks (src/sparse_data.cpp:230-240,364-375)
+  if (mode0 < 0 || mode0 >= ctx->order)
+    return set_err(ctx, CMTF_EVALIDATION, "coupled mode out of range");
+  if (!(weight > 0)) return set_err(ctx, CMTF_EVALIDATION, "lambda_m must be positive");
+  if (rows != ctx->dims[mode0])
+    return set_err(ctx, CMTF_EVALIDATION,
+                   "coupled matrix row space does not match mode %d", mode0 + 1);
+  if (cols == 0) return set_err(ctx, CMTF_EVALIDATION, "mode sizes must be positive");
+  if ((int)ctx->mats.size() >= kMaxMats)
+    return set_err(ctx, CMTF_EUNSUPPORTED, "at most %d coupled matrices", kMaxMats);
+  if (nnz >= 0xffffffffull)
+    return set_err(ctx, CMTF_EUNSUPPORTED, "matrix nnz >= 2^32 per device");
+  DevMatrix M;
+  M.mode = mode0;
+  M.rows = rows;
+  M.cols = cols;
+  M.nnz = nnz;
+  M.weight = weight;
+  TRY(dalloc(ctx, &M.count, cols));
+  TRY(dalloc(ctx, &M.vreg, cols));
+  CU(cudaMemsetAsync(M.count, 0, cols * sizeof(uint32_t), ctx->stream));
+  const size_t slot = ctx->mats.size();
+  if (slot < ctx->spare.size() && ctx->spare[slot].V && ctx->spare[slot].mode == mode0 &&
+      ctx->spare[slot].cols == cols) {
+    M.V = ctx->spare[slot].V;  // keep the coupled factor of the state
+    ctx->spare[slot].V = nullptr;
+  } else {
+    TRY(dalloc(ctx, &M.V, (uint64_t)cols * ctx->JP(mode0)));
+    ctx->have_model = false;
+  }
+  TRY(dalloc(ctx, &M.rec, nnz * 3));
+  TRY(dalloc(ctx, &M.pos, nnz));
+  if (nnz > 0) {
+    uint32_t* d_idx = nullptr;
+    double* d_vals = nullptr;
+    uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
+    TRY(dalloc(ctx, &d_idx, nnz * 2));
+    TRY(dalloc(ctx, &d_vals, nnz));
+    TRY(dalloc(ctx, &d_rec, nnz * 3));
+    TRY(dalloc(ctx, &d_keys, nnz));
+    TRY(dalloc(ctx, &d_ids, nnz));
+    CU(cudaMemcpyAsync(d_idx, idx, nnz * 2 * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+    pack_matrix_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+        d_idx, d_vals, nnz, rows, cols, d_rec, d_keys, d_ids, M.count, ctx->d_first);
+    CU(cudaGetLastError());
+    unsigned long long bad[2];
+    CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_idx);
+    cudaFree(d_vals);
+    if (bad[0] != ~0ull || bad[1] != ~0ull) {
+      cudaFree(d_rec);
+      cudaFree(d_keys);
+      cudaFree(d_ids);
+      dfree(M.count);
+      dfree(M.vreg);
+      dfree(M.V);
+      dfree(M.rec);
+      dfree(M.pos);
+      if (bad[0] != ~0ull)
+        return set_err(ctx, CMTF_EVALIDATION, "matrix index out of range (entry %llu)",
+                       bad[0] + 1);
+      return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
+    }
+    uint32_t* sorted_ids = nullptr;
+    TRY(sort_ids(ctx, d_keys, d_ids, nnz, rows, &sorted_ids));
+    cudaFree(d_keys);
+    cudaFree(d_ids);
+    gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+        d_rec, sorted_ids, nnz, 3, M.rec, M.pos);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_rec);
+    cudaFree(sorted_ids);
+  }
+  reg_kernel<<<grid_for(cols), 256, 0, ctx->stream>>>(
+      M.count, cols, (float)(weight * ctx->cfg.lambda_reg), M.vreg);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->mats.push_back(M);
+  return CMTF_OK;
+}
+
+// random_model (src/trainer.cpp:30-58) with make_rng(seed, Init)
+// (src/trainer.cpp:100); uploaded as f32 with zeroed row padding.
+int cmtf_gpu_make_state(cmtf_gpu_ctx* ctx) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (!ctx->rec) return set_err(ctx, CMTF_EVALIDATION, "no training tensor set");
+  CU(cudaSetDevice(ctx->device));
+  auto rng = make_rng(ctx->cfg.seed, 0x01, 0);
+  const double scale = ctx->cfg.init_scale;
+  std::vector<float> core(ctx->core_size());
+  for (auto& g : core) g = (float)(0.0 + (scale - 0.0) * uniform01(rng));
+  CU(cudaMemcpyAsync(ctx->G, core.data(), core.size() * sizeof(float),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  auto draw = [&](float* dst, uint32_t rows, uint32_t J, uint32_t JP) -> int {
+    const double hi = scale / std::sqrt((double)J);
+    std::vector<float> h((uint64_t)rows * JP, 0.f);
+    for (uint64_t i = 0; i < rows; ++i)
+      for (uint32_t k = 0; k < J; ++k)
+        h[i * JP + k] = (float)(0.0 + (hi - 0.0) * uniform01(rng));
+    CU(cudaMemcpy(dst, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return CMTF_OK;
+  };
+  for (int n = 0; n < ctx->order; ++n)
+    TRY(draw(ctx->U[n], ctx->dims[n], ctx->J(n), ctx->JP(n)));
+  for (auto& M : ctx->mats) TRY(draw(M.V, M.cols, ctx->J(M.mode), ctx->JP(M.mode)));
+  ctx->have_model = true;
+  ctx->epoch = 0;
+  ctx->eta = ctx->cfg.eta0;
+  ctx->schedule.clear();
+  return CMTF_OK;
+}
+
+int cmtf_gpu_set_model(cmtf_gpu_ctx* ctx, const double* core,
+                       const double* const* factors, const double* const* couplings) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (!ctx->rec) return set_err(ctx, CMTF_EVALIDATION, "no training tensor set");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<float> c(ctx->core_size());
+  for (size_t d = 0; d < c.size(); ++d) c[d] = (float)core[d];
+  CU(cudaMemcpy(ctx->G, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice));
+  auto put = [&](float* dst, const double* src, uint32_t rows, uint32_t J,
+                 uint32_t JP) -> int {
+    std::vector<float> h((uint64_t)rows * JP, 0.f);
+    for (uint64_t i = 0; i < rows; ++i)
+      for (uint32_t k = 0; k < J; ++k) h[i * JP + k] = (float)src[i * J + k];
+    CU(cudaMemcpy(dst, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    return CMTF_OK;
+  };
+  for (int n = 0; n < ctx->order; ++n)
+    TRY(put(ctx->U[n], factors[n], ctx->dims[n], ctx->J(n), ctx->JP(n)));
+  for (size_t m = 0; m < ctx->mats.size(); ++m)
+    TRY(put(ctx->mats[m].V, couplings[m], ctx->mats[m].cols, ctx->J(ctx->mats[m].mode),
+            ctx->JP(ctx->mats[m].mode)));
+  ctx->have_model = true;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_get_model(cmtf_gpu_ctx* ctx, double* core, double* const* factors,
+                       double* const* couplings) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (core) {
+    std::vector<float> c(ctx->core_size());
+    CU(cudaMemcpy(c.data(), ctx->G, c.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t d = 0; d < c.size(); ++d) core[d] = c[d];
+  }
+  auto get = [&](double* dst, const float* src, uint32_t rows, uint32_t J,
+                 uint32_t JP) -> int {
+    std::vector<float> h((uint64_t)rows * JP);
+    CU(cudaMemcpy(h.data(), src, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < rows; ++i)
+      for (uint32_t k = 0; k < J; ++k) dst[i * J + k] = h[i * JP + k];
+    return CMTF_OK;
+  };
+  if (factors)
+    for (int n = 0; n < ctx->order; ++n)
+      TRY(get(factors[n], ctx->U[n], ctx->dims[n], ctx->J(n), ctx->JP(n)));
+  if (couplings)
+    for (size_t m = 0; m < ctx->mats.size(); ++m)
+      TRY(get(couplings[m], ctx->mats[m].V, ctx->mats[m].cols,
+              ctx->J(ctx->mats[m].mode), ctx->JP(ctx->mats[m].mode)));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_get_state(cmtf_gpu_ctx* ctx, int32_t* epoch, double* eta) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (epoch) *epoch = ctx->epoch;
+  if (eta) *eta = ctx->eta;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_set_state(cmtf_gpu_ctx* ctx, int32_t epoch, double eta) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  ctx->epoch = epoch;
+  ctx->eta = eta;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  const float eta = (float)ctx->eta;
+  ctx->last_launches = 0;
+  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (ctx->cfg.exec_mode == CMTF_EXEC_SERIAL) {
+    TRY(serial_epoch(ctx, eta));
+    ctx->last_launches += 1;
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  } else {
+    TRY(hogwild_tensor_sweep(ctx, eta));
+    ctx->last_launches += 1;
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    for (auto& M : ctx->mats) {
+      TRY(matrix_sweep(ctx, M, eta));
+      ctx->last_launches += M.nnz ? 1 : 0;
+    }
+    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  }
+  std::string offender;
+  TRY(scan_nonfinite(ctx, &offender));
+  CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  CU(cudaEventSynchronize(ctx->ev[3]));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  ctx->last_ms[0] = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+  ctx->last_ms[1] = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  ctx->last_ms[2] = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
+  ctx->last_ms[3] = ms;
+  // src/trainer.cpp:309-315
+  ctx->epoch += 1;
+  ctx->eta = ctx->cfg.eta0 / (1.0 + ctx->cfg.mu * ctx->epoch);
+  if (!offender.empty())
+    return set_err(ctx, CMTF_EDIVERGENCE,
+                   "non-finite parameter after epoch %d: %s; try a smaller initial "
+                   "learning rate",
+                   ctx->epoch, offender.c_str());
+  return CMTF_OK;
+}
+
+int cmtf_gpu_epoch_stats(cmtf_gpu_ctx* ctx, double lambda_reg, double* train_rmse,
+                         double* objective) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  double sse = 0.0;
+  TRY(tensor_sse(ctx, ctx->rec, ctx->nnz, &sse));
+  std::vector<float> core(ctx->core_size());
+  CU(cudaMemcpy(core.data(), ctx->G, core.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  double gn = 0.0;
+  for (float g : core) gn += (double)g * g;
+  double f_t = sse + lambda_reg * gn;
+  for (int n = 0; n < ctx->order; ++n) {
+    double rn = 0.0;
+    TRY(row_norms(ctx, ctx->U[n], ctx->dims[n], ctx->J(n), ctx->JP(n), ctx->count[n], &rn));
+    f_t += lambda_reg * rn;
+  }
+  double obj = 0.5 * f_t;
+  for (auto& M : ctx->mats) {
+    double f_m = 0.0, rn = 0.0;
+    TRY(matrix_sse(ctx, M, &f_m));
+    TRY(row_norms(ctx, M.V, M.cols, ctx->J(M.mode), ctx->JP(M.mode), M.count, &rn));
+    f_m += lambda_reg * rn;
+    obj += 0.5 * M.weight * f_m;
+  }
+  if (train_rmse) *train_rmse = std::sqrt(sse / (double)ctx->nnz);
+  if (objective) *objective = obj;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_test_rmse(cmtf_gpu_ctx* ctx, const uint32_t* idx, const double* vals,
+                       uint64_t nnz, double* rmse) {
+  TRY(require_bundle(ctx));
+  if (nnz == 0) return set_err(ctx, CMTF_EVALIDATION, "cannot evaluate an empty tensor");
+  CU(cudaSetDevice(ctx->device));
+  const int N = ctx->order;
+  uint32_t* d_idx = nullptr;
+  double* d_vals = nullptr;
+  uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
+  TRY(dalloc(ctx, &d_idx, nnz * N));
+  TRY(dalloc(ctx, &d_vals, nnz));
+  TRY(dalloc(ctx, &d_rec, nnz * (N + 1)));
+  TRY(dalloc(ctx, &d_keys, nnz));
+  TRY(dalloc(ctx, &d_ids, nnz));
+  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  // counts of a test tensor must not touch the training counts: use scratch
+  std::vector<uint32_t*> scratch(N, nullptr);
+  ModeTables mt = mode_tables(ctx);
+  for (int n = 0; n < N; ++n) {
+    TRY(dalloc(ctx, &scratch[n], ctx->dims[n]));
+    CU(cudaMemsetAsync(scratch[n], 0, ctx->dims[n] * sizeof(uint32_t), ctx->stream));
+    mt.count[n] = scratch[n];
+  }
+  CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+  pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+      d_idx, d_vals, nnz, N, mt, 0, d_rec, d_keys, d_ids, ctx->d_first);
+  CU(cudaGetLastError());
+  unsigned long long bad[2];
+  CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  int rc = CMTF_OK;
+  if (bad[0] != ~0ull) rc = set_err(ctx, CMTF_EVALIDATION, "test tensor index out of range");
+  else if (bad[1] != ~0ull) rc = set_err(ctx, CMTF_EVALIDATION, "test tensor value is not finite");
+  double sse = 0.0;
+  if (rc == CMTF_OK) rc = tensor_sse(ctx, d_rec, nnz, &sse);
+  cudaFree(d_idx);
+  cudaFree(d_vals);
+  cudaFree(d_rec);
+  cudaFree(d_keys);
+  cudaFree(d_ids);
+  for (auto p : scratch) cudaFree(p);
+  if (rc != CMTF_OK) return rc;
+  *rmse = std::sqrt(sse / (double)nnz);
+  return CMTF_OK;
+}
+
+int cmtf_gpu_matrix_rmse(cmtf_gpu_ctx* ctx, int32_t m, double* rmse) {
+  TRY(require_bundle(ctx));
+  if (m < 0 || m >= (int)ctx->mats.size())
+    return set_err(ctx, CMTF_EVALIDATION, "no coupled factor for this matrix");
+  if (ctx->mats[m].nnz == 0)
+    return set_err(ctx, CMTF_EVALIDATION, "cannot evaluate an empty matrix");
+  double sse = 0.0;
+  TRY(matrix_sse(ctx, ctx->mats[m], &sse));
+  *rmse = std::sqrt(sse / (double)ctx->mats[m].nnz);
+  return CMTF_OK;
+}
+
+// train (src/trainer.cpp:318-346) minus the QR finalisation.
+int cmtf_gpu_train(cmtf_gpu_ctx* ctx, double* log, int32_t log_capacity,
+                   int32_t* n_log) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  TRY(cmtf_gpu_make_state(ctx));
+  const auto start = std::chrono::steady_clock::now();
+  double prev = std::numeric_limits<double>::quiet_NaN();
+  int32_t nl = 0;
+  if (n_log) *n_log = 0;
+  for (int ep = 0; ep < ctx->cfg.max_epochs; ++ep) {
+    TRY(cmtf_gpu_run_epoch(ctx));
+    double rmse = 0, obj = 0;
+    TRY(cmtf_gpu_epoch_stats(ctx, ctx->cfg.lambda_reg, &rmse, &obj));
+    const double secs =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+    if (log && nl < log_capacity) {
+      log[4 * nl + 0] = ctx->epoch;
+      log[4 * nl + 1] = rmse;
+      log[4 * nl + 2] = obj;
+      log[4 * nl + 3] = secs;
+    }
+    ++nl;
+    if (n_log) *n_log = nl;
+    if (std::isfinite(prev) && prev > 0 && std::abs(prev - rmse) / prev < ctx->cfg.rel_tol)
+      break;
+    prev = rmse;
+  }
+  return CMTF_OK;
+}
+
+int cmtf_gpu_entry_grads(cmtf_gpu_ctx* ctx, const uint64_t* ids, uint64_t n,
+                         double* xhat, double* residual, double* grow, double* gcore) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (n == 0) return CMTF_OK;
+  for (uint64_t e = 0; e < n; ++e)
+    if (ids[e] >= ctx->nnz) return set_err(ctx, CMTF_EVALIDATION, "entry id out of range");
+  const CoreShape cs = core_shape(ctx);
+  const uint32_t sumJ = cs.off[cs.order];
+  uint64_t* d_ids = nullptr;
+  float *d_x = nullptr, *d_r = nullptr, *d_grow = nullptr, *d_gcore = nullptr;
+  TRY(dalloc(ctx, &d_ids, n));
+  TRY(dalloc(ctx, &d_x, n));
+  TRY(dalloc(ctx, &d_r, n));
+  TRY(dalloc(ctx, &d_grow, n * sumJ));
+  if (gcore) TRY(dalloc(ctx, &d_gcore, n * cs.size));
+  CU(cudaMemcpyAsync(d_ids, ids, n * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  ProbeArgs a{};
+  a.cs = cs;
+  a.G = ctx->G;
+  a.rec = ctx->rec;
+  a.pos = ctx->pos;
+  a.ids = d_ids;
+  a.mt = mode_tables(ctx);
+  a.n = n;
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.with_core = gcore != nullptr;
+  a.xhat = d_x;
+  a.resid = d_r;
+  a.grow = d_grow;
+  a.gcore = d_gcore;
+  const int bt = 128;
+  const size_t smem = sizeof(float) * (bt / 32) * 2 * sumJ;
+  auto kern = ctx->cfg.kernel == CMTF_KERNEL_OPT ? probe_kernel<true> : probe_kernel<false>;
+  kern<<<grid_for(n, bt / 32), bt, smem, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  std::vector<float> hx(n), hr(n), hg(n * sumJ), hc(gcore ? n * cs.size : 0);
+  CU(cudaMemcpyAsync(hx.data(), d_x, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hr.data(), d_r, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(hg.data(), d_grow, n * sumJ * sizeof(float), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  if (gcore)
+    CU(cudaMemcpyAsync(hc.data(), d_gcore, hc.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_ids);
+  cudaFree(d_x);
+  cudaFree(d_r);
+  cudaFree(d_grow);
+  if (d_gcore) cudaFree(d_gcore);
+  for (uint64_t e = 0; e < n; ++e) {
+    if (xhat) xhat[e] = hx[e];
+    if (residual) residual[e] = hr[e];
+  }
+  for (uint64_t q = 0; q < n * sumJ; ++q) grow[q] = hg[q];
+  if (gcore)
+    for (uint64_t q = 0; q < hc.size(); ++q) gcore[q] = hc[q];
+  return CMTF_OK;
+}
+
+int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ranks,
+                              const double* core, uint64_t n, const double* x,
+                              const double* rows, const uint32_t* counts,
+                              double lambda_reg, uint64_t nnz_total, int32_t with_core,
+                              double* grow, double* gcore, double* residual,
+                              int32_t device) {
+  cmtf_gpu_ctx* ctx = nullptr;
+  if (order < 1 || order > kMaxOrder)
+    return set_err(nullptr, CMTF_EVALIDATION, "kernel argument order mismatch");
+  CoreShape cs{};
+  cs.order = order;
+  uint32_t off = 0;
+  uint64_t size = 1;
+  for (int q = 0; q < order; ++q) {
+    if (ranks[q] == 0 || ranks[q] > (uint32_t)kMaxRank)
+      return set_err(nullptr, CMTF_EVALIDATION, "bad rank");
+    cs.J[q] = ranks[q];
+    cs.off[q] = off;
+    off += ranks[q];
+    size *= ranks[q];
+  }
+  if (size > (uint64_t)kMaxCore)
+    return set_err(nullptr, CMTF_EUNSUPPORTED, "core too large for the device kernels");
+  cs.off[order] = off;
+  cs.size = (uint32_t)size;
+  for (uint64_t e = 0; e < n * order; ++e)
+    if (counts[e] == 0)
+      return set_err(nullptr, CMTF_EVALIDATION, "mode counts must be >= 1");
+  if (n == 0) return CMTF_OK;
+  CU(cudaSetDevice(device));
+  std::vector<float> hcore(size), hrows(n * off), hx(n);
+  for (uint64_t q = 0; q < size; ++q) hcore[q] = (float)core[q];
+  for (uint64_t q = 0; q < n * off; ++q) hrows[q] = (float)rows[q];
+  for (uint64_t q = 0; q < n; ++q) hx[q] = (float)x[q];
+  float *d_core = nullptr, *d_rows = nullptr, *d_x = nullptr, *d_r = nullptr,
+        *d_grow = nullptr, *d_gcore = nullptr;
+  uint32_t* d_counts = nullptr;
+  TRY(dalloc(ctx, &d_core, size));
+  TRY(dalloc(ctx, &d_rows, n * off));
+  TRY(dalloc(ctx, &d_x, n));
+  TRY(dalloc(ctx, &d_r, n));
+  TRY(dalloc(ctx, &d_grow, n * off));
+  TRY(dalloc(ctx, &d_counts, n * order));
+  if (with_core) TRY(dalloc(ctx, &d_gcore, n * size));
+  CU(cudaMemcpy(d_core, hcore.data(), size * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_rows, hrows.data(), n * off * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_x, hx.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_counts, counts, n * order * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  ProbeArgs a{};
+  a.cs = cs;
+  a.G = d_core;
+  a.rows = d_rows;
+  a.x = d_x;
+  a.counts = d_counts;
+  a.lambda = (float)lambda_reg;
+  a.n = n;
+  a.core_reg = (float)(lambda_reg / (double)nnz_total);
+  a.with_core = with_core;
+  a.resid = d_r;
+  a.grow = d_grow;
+  a.gcore = d_gcore;
+  const int bt = 128;
+  const size_t smem = sizeof(float) * (bt / 32) * 2 * off;
+  if (kernel == CMTF_KERNEL_OPT)
+    probe_kernel<true><<<grid_for(n, bt / 32), bt, smem>>>(a);
+  else
+    probe_kernel<false><<<grid_for(n, bt / 32), bt, smem>>>(a);
+  CU(cudaGetLastError());
+  std::vector<float> hr(n), hg(n * off), hc(with_core ? n * size : 0);
+  CU(cudaMemcpy(hr.data(), d_r, n * sizeof(float), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hg.data(), d_grow, n * off * sizeof(float), cudaMemcpyDeviceToHost));
+  if (with_core)
+    CU(cudaMemcpy(hc.data(), d_gcore, hc.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  cudaFree(d_core);
+  cudaFree(d_rows);
+  cudaFree(d_x);
+  cudaFree(d_r);
+  cudaFree(d_grow);
+  cudaFree(d_counts);
+  if (d_gcore) cudaFree(d_gcore);
+  for (uint64_t q = 0; q < n; ++q)
+    if (residual) residual[q] = hr[q];
+  for (uint64_t q = 0; q < n * off; ++q) grow[q] = hg[q];
+  if (with_core && gcore)
+    for (uint64_t q = 0; q < hc.size(); ++q) gcore[q] = hc[q];
+  return CMTF_OK;
+}
+
+int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double* y,
+                                    const double* u, const double* v, double lambda_m,
+                                    double lambda_reg, const uint32_t* col_count,
+                                    double* du, double* dv, double* residual,
+                                    int32_t device) {
+  cmtf_gpu_ctx* ctx = nullptr;
+  if (n == 0) return CMTF_OK;
+  if (j == 0) return set_err(nullptr, CMTF_EVALIDATION, "coupled rows must have equal length");
+  CU(cudaSetDevice(device));
+  std::vector<float> hy(n), hu(n * j), hv(n * j);
+  for (uint64_t q = 0; q < n; ++q) hy[q] = (float)y[q];
+  for (uint64_t q = 0; q < n * j; ++q) {
+    hu[q] = (float)u[q];
+    hv[q] = (float)v[q];
+  }
+  float *d_y = nullptr, *d_u = nullptr, *d_v = nullptr, *d_du = nullptr, *d_dv = nullptr,
+        *d_r = nullptr;
+  uint32_t* d_c = nullptr;
+  TRY(dalloc(ctx, &d_y, n));
+  TRY(dalloc(ctx, &d_u, n * j));
+  TRY(dalloc(ctx, &d_v, n * j));
+  TRY(dalloc(ctx, &d_du, n * j));
+  TRY(dalloc(ctx, &d_dv, n * j));
+  TRY(dalloc(ctx, &d_r, n));
+  TRY(dalloc(ctx, &d_c, n));
+  CU(cudaMemcpy(d_y, hy.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_u, hu.data(), n * j * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_v, hv.data(), n * j * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_c, col_count, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  matrix_probe_kernel<<<grid_for(n), 256>>>(n, j, d_y, d_u, d_v, (float)lambda_m,
+                                            (float)lambda_reg, d_c, d_du, d_dv, d_r);
+  CU(cudaGetLastError());
+  std::vector<float> hdu(n * j), hdv(n * j), hr(n);
+  CU(cudaMemcpy(hdu.data(), d_du, n * j * sizeof(float), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hdv.data(), d_dv, n * j * sizeof(float), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hr.data(), d_r, n * sizeof(float), cudaMemcpyDeviceToHost));
+  for (auto p : {d_y, d_u, d_v, d_du, d_dv, d_r}) cudaFree(p);
+  cudaFree(d_c);
+  for (uint64_t q = 0; q < n * j; ++q) {
+    du[q] = hdu[q];
+    dv[q] = hdv[q];
+  }
+  for (uint64_t q = 0; q < n; ++q)
+    if (residual) residual[q] = hr[q];
+  return CMTF_OK;
+}
+
+int cmtf_gpu_last_epoch_timing(cmtf_gpu_ctx* ctx, double* kernel_ms, int32_t* launches) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (kernel_ms)
+    for (int i = 0; i < 4; ++i) kernel_ms[i] = ctx->last_ms[i];
+  if (launches) *launches = ctx->last_launches;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_kernel_info(cmtf_gpu_ctx* ctx, int32_t* which, int32_t* hog_threads,
+                         int32_t* sort_mode) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (which) *which = ctx->kernel_which;
+  if (hog_threads) *hog_threads = ctx->hog_threads_used;
+  if (sort_mode) *sort_mode = ctx->sort_mode;
+  return CMTF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+identical seeded inputs.  Tolerances (BASELINE.json north_star):
+  * per-entry prediction/gradient pass: 1e-5 relative in fp32 (scale-aware:
+    |a-b| <= 1e-5 * max(|ref|, |r| * |contraction| + reg * |u|), inputs rounded
+    to fp32 before being fed to the f64 oracle);
+  * serial-order single epoch: factors/core within 1e-4 of run_epoch(workers=1);
+  * final train/test RMSE after a fixed number of epochs: within 1%.
+"""
+import numpy as np
+import pytest
+
+from conftest import bundle_from, load_npz, model_from
+from oracle import oracle as O
+from paper_1708_08640_b200 import api, synth
+from paper_1708_08640_b200.api import TrainConfig
+
+pytestmark = pytest.mark.gpu
+
+f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+
+
+def scale_close(a, ref, scale, tol):
+    err = np.abs(np.asarray(a) - np.asarray(ref))
+    bound = tol * np.maximum(np.abs(ref), scale)
+    assert np.all(err <= bound), f"max err {err.max():.3e} vs bound {bound[np.argmax(err - bound)]:.3e}"
+
+
+# ----------------------------------------------------------------------
+# per-entry kernels (compute_gradient / _opt / matrix_entry_gradients)
+# ----------------------------------------------------------------------
+@pytest.mark.parametrize("opt", [0, 1])
+def test_compute_gradient_matches_oracle(opt):
+    d = load_npz("kernels.npz")
+    for rep in range(int(d["n_kernel_cases"])):
+        ranks = [int(r) for r in d[f"k{rep}_ranks"]]
+        core = f32(d[f"k{rep}_core"]).reshape(ranks)
+        flat = f32(d[f"k{rep}_rows"])
+        x, lam, nnz_total = d[f"k{rep}_scalars"]
+        x = float(np.float32(x))
+        counts = d[f"k{rep}_counts"]
+        rows, off = [], 0
+        for r in ranks:
+            rows.append(flat[off:off + r])
+            off += r
+        g_ref, c_ref, r_ref = O.compute_gradient(opt, x, core, rows, lam, counts, int(nnz_total))
+        fn = api.compute_gradient_opt if opt else api.compute_gradient
+        grow, gcore, res = fn(x, core, flat[None, :], lam, counts[None, :], int(nnz_total))
+        # scale of each component: |r| * |G x_{-n} u| + reg * |u|
+        cont_scale = np.abs(r_ref) * np.max(np.abs(core)) * np.prod(
+            [np.max(np.abs(r_)) + 1e-30 for r_ in rows]) * 2 + 1e-6
+        scale_close(res, [r_ref], max(abs(x), 1.0), 1e-5)
+        scale_close(grow[0], g_ref, cont_scale, 1e-5)
+        scale_close(gcore[0], c_ref, cont_scale, 1e-5)
+
+
+def test_hand_computed_rank1_on_gpu():
+    # test_gradients.cpp:158-170
+    grow, gcore, r = api.compute_gradient(40.0, np.array([[2.0]]), np.array([[3.0, 5.0]]),
+                                          0.0, np.array([[1, 1]]), 1)
+    assert r[0] == 10.0 and list(grow[0]) == [-100.0, -60.0] and gcore[0, 0] == -150.0
+    # test_gradients.cpp:322-330
+    du, dv, r = api.matrix_entry_gradients(10.0, [[2.0]], [[3.0]], 10.0, 0.0, 1)
+    assert r[0] == 4.0 and du[0, 0] == -120.0 and dv[0, 0] == -80.0
+
+
+def test_zero_residual_zero_lambda_gives_zero():
+    # test_gradients.cpp:144-156
+    core = f32(np.random.default_rng(43).uniform(-1, 1, (2, 2)))
+    rows = f32(np.random.default_rng(44).uniform(-1, 1, (1, 4)))
+    x = O.predict(core, [rows[0, :2], rows[0, 2:]])
+    grow, gcore, r = api.compute_gradient(x, core, rows, 0.0, [[5, 7]], 12)
+    assert abs(r[0]) < 1e-6 and np.abs(grow).max() < 1e-6 and np.abs(gcore).max() < 1e-6
+
+
+def test_matrix_gradients_match_oracle():
+    d = load_npz("kernels.npz")
+    rep = 0
+    while f"m{rep}_in" in d:
+        inp = d[f"m{rep}_in"]
+        y, lm, lam, cc = inp[:4]
+        j = (inp.shape[0] - 4) // 2
+        u, v, y = f32(inp[4:4 + j]), f32(inp[4 + j:]), float(np.float32(y))
+        du_r, dv_r, r_r = O.matrix_entry_gradients(y, u, v, lm, lam, int(cc))
+        du, dv, r = api.matrix_entry_gradients(y, u[None], v[None], lm, lam, int(cc))
+        sc = abs(r_r) * lm * (np.abs(u).max() + np.abs(v).max()) + 1e-6
+        scale_close(du[0], du_r, sc, 1e-5)
+        scale_close(dv[0], dv_r, sc, 1e-5)
+        scale_close(r, [r_r], max(abs(y), 1.0), 1e-5)
+        rep += 1
+
+
+# ----------------------------------------------------------------------
+# probes on a device-resident bundle
+# ----------------------------------------------------------------------
+def _config1_small():
+    d = load_npz("config1_small.npz")
+    b = bundle_from(d, "c_")
+    test = api.SparseTensor(b.tensor.dims, d["c_test_idx"], d["c_test_vals"])
+    return d, b, test
+
+
+@pytest.mark.parametrize("kernel", ["opt", "naive"])
+def test_entry_grads_at_init_and_midtraining(kernel):
+    d, b, _ = _config1_small()
+    cfg = TrainConfig(ranks=[5, 5, 5], seed=0, eta0=0.01, lambda_reg=0.01, kernel=kernel)
+    st = api.make_state(cfg, b)
+    ids = np.arange(0, b.tensor.nnz, 37, dtype=np.uint64)
+    for snapshot in ("init", "trained"):
+        if snapshot == "trained":
+            api.run_epoch(st)
+        m = st.model  # fp32 values widened to f64: identical inputs to both sides
+        xh, r, grow, gcore = api.entry_grads(st, ids)
+        counts = O.count_modes(b, [5, 5, 5])
+        offs = np.cumsum([0] + list(b.tensor.dims))
+        for k, e in enumerate(ids):
+            idx = b.tensor.indices[e]
+            rows = [m.factors[n][idx[n]] for n in range(3)]
+            cn = [counts[offs[n] + idx[n]] for n in range(3)]
+            x = float(np.float32(b.tensor.values[e]))
+            g_ref, c_ref, r_ref = O.compute_gradient(kernel == "opt", x, m.core, rows, 0.01, cn,
+                                                     b.tensor.nnz)
+            xs = np.max(np.abs(m.core)) * np.prod([np.abs(r_).sum() for r_ in rows])
+            scale_close([xh[k]], [x - r_ref], xs, 1e-5)
+            sc = abs(r_ref) * xs + 0.01 * max(np.abs(r_).max() for r_ in rows) + 1e-7
+            scale_close(grow[k], g_ref, sc, 1e-5)
+            scale_close(gcore[k], c_ref, sc, 1e-5)
+
+
+def test_epoch_stats_and_test_rmse_match_oracle():
+    d, b, test = _config1_small()
+    cfg = TrainConfig(ranks=[5, 5, 5], seed=0, eta0=0.01, lambda_reg=0.01)
+    st = api.make_state(cfg, b)
+    api.run_epoch(st)
+    m = st.model
+    om = O.OracleModel(b, [5, 5, 5]).copy_from(m)
+    r_ref, o_ref = O.epoch_stats(b, om, 0.01)
+    s = api.epoch_stats(st, 0.01)
+    assert abs(s.train_rmse - r_ref) <= 1e-5 * r_ref
+    assert abs(s.objective - o_ref) <= 1e-5 * o_ref
+    t_ref = O.tensor_rmse(test, om)
+    assert abs(api.test_rmse(st, test) - t_ref) <= 1e-5 * t_ref
+
+
+def test_initial_model_matches_reference_law():
+    # random_model draw law and stream (src/trainer.cpp:30-58,100)
+    d = load_npz("epochs.npz")
+    b = bundle_from(d, "b_")
+    st = api.make_state(TrainConfig(ranks=[2, 2, 2], seed=17, eta0=0.01), b)
+    m = st.model
+    ref = model_from(d, "opt1_init_", 3, len(b.matrices))
+    np.testing.assert_array_equal(m.core.reshape(-1), f32(ref.core).reshape(-1))
+    for a, c in zip(m.factors + m.couplings, ref.factors + ref.couplings):
+        np.testing.assert_array_equal(a, f32(c))
+
+
+# ----------------------------------------------------------------------
+# serial-order single epoch (exact reference schedule, P=1)
+# ----------------------------------------------------------------------
+@pytest.mark.parametrize("kernel", ["opt", "naive"])
+@pytest.mark.parametrize("fixture", ["epochs", "config1"])
+def test_serial_epoch_reproduces_reference(kernel, fixture):
+    if fixture == "epochs":
+        d = load_npz("epochs.npz")
+        b = bundle_from(d, "b_")
+        ranks, seed, lr, lam = [2, 2, 2], 17, 0.01, 0.1
+    else:
+        d, b, _ = _config1_small()
+        ranks, seed, lr, lam = [5, 5, 5], 0, 0.01, 0.01
+    cfg = TrainConfig(ranks=ranks, seed=seed, eta0=lr, lambda_reg=lam, kernel=kernel,
+                      exec_mode="serial")
+    st = api.make_state(cfg, b)
+    tr = O.SerialTrainer(b, ranks, seed=seed, eta0=lr, mu=0.1, lambda_reg=lam,
+                         kernel_opt=kernel == "opt")
+    tr.model.copy_from(st.model)  # same fp32-rounded start
+    tr.run_epoch()
+    api.run_epoch(st)
+    m = st.model
+    assert st.epoch == 1 and st.eta == pytest.approx(lr / 1.1, rel=0, abs=1e-18)
+    for a, ref in zip([m.core.reshape(-1)] + m.factors + m.couplings,
+                      [tr.model.core] + tr.model.factors + tr.model.couplings):
+        scale_close(a, ref, 1e-2 * np.abs(ref).max(), 1e-4)
+
+
+# ----------------------------------------------------------------------
+# Hogwild epochs: RMSE parity after a fixed number of epochs
+# ----------------------------------------------------------------------
+@pytest.mark.parametrize("kernel", ["opt", "naive"])
+@pytest.mark.parametrize("generic", [False, True])
+def test_hogwild_rmse_within_1pct_of_oracle(kernel, generic):
+    spec = synth.config1(literal=False)  # reference law, lr 0.01: converges to the noise
+    b, test, _ = synth.generate(spec)
+    epochs = 10
+    tr = O.SerialTrainer(b, [5, 5, 5], seed=0, eta0=0.01, mu=0.1, lambda_reg=0.01)
+    for _ in range(epochs):
+        assert tr.run_epoch() == 0
+    ref_test = O.tensor_rmse(test, tr.model)
+    ref_train, _ = O.epoch_stats(b, tr.model, 0.01)
+    cfg = TrainConfig(ranks=[5, 5, 5], seed=0, eta0=0.01, lambda_reg=0.01, kernel=kernel,
+                      force_generic=generic)
+    st = api.make_state(cfg, b)
+    for _ in range(epochs):
+        api.run_epoch(st)
+    info = st.kernel_info()
+    assert info["kernel"] == ("generic" if generic else "order3")
+    gpu_test = api.test_rmse(st, test)
+    gpu_train = api.epoch_stats(st, 0.01).train_rmse
+    assert abs(gpu_test - ref_test) <= 0.01 * ref_test, (gpu_test, ref_test, info)
+    assert abs(gpu_train - ref_train) <= 0.01 * ref_train, (gpu_train, ref_train)
+
+
+def test_zero_learning_rate_changes_nothing():
+    # test_trainer.cpp:105-113
+    d = load_npz("epochs.npz")
+    b = bundle_from(d, "b_")
+    st = api.make_state(TrainConfig(ranks=[2, 2, 2], seed=17, eta0=0.0), b)
+    before = st.model
+    api.run_epoch(st)
+    after = st.model
+    for a, c in zip([before.core] + before.factors + before.couplings,
+                    [after.core] + after.factors + after.couplings):
+        np.testing.assert_array_equal(a, c)
+
+
+def test_learning_rate_decay_law():
+    # test_trainer.cpp:91-103
+    d = load_npz("epochs.npz")
+    b = bundle_from(d, "b_")
+    st = api.make_state(TrainConfig(ranks=[2, 2, 2], seed=17, eta0=0.002, mu=0.3), b)
+    assert st.eta == 0.002
+    for t in range(1, 6):
+        api.run_epoch(st)
+        assert st.epoch == t and st.eta == 0.002 / (1.0 + 0.3 * t)
+
+
+def test_divergence_raises_named_error():
+    # test_trainer.cpp:294-303
+    d = load_npz("epochs.npz")
+    b = bundle_from(d, "b_")
+    cfg = TrainConfig(ranks=[2, 2, 2], seed=17, eta0=1e8, max_epochs=20)
+    with pytest.raises(api.DivergenceError, match="try a smaller initial learning rate"):
+        api.train(b, cfg)
+
+
+def test_validation_errors_on_bad_bundle():
+    t = api.SparseTensor([4, 4, 4], [[0, 0, 9]], [1.0])
+    with pytest.raises(api.ValidationError, match="index out of range"):
+        api.make_state(TrainConfig(ranks=[2, 2, 2]), api.DataBundle(t, []))
+    t = api.SparseTensor([4, 4, 4], [[0, 0, 1]], [np.nan])
+    with pytest.raises(api.ValidationError, match="not finite"):
+        api.make_state(TrainConfig(ranks=[2, 2, 2]), api.DataBundle(t, []))
+    t = api.SparseTensor([4, 4, 4], [[0, 0, 1]], [1.0])
+    with pytest.raises(api.ValidationError, match="exceeds its size"):
+        api.make_state(TrainConfig(ranks=[5, 2, 2]), api.DataBundle(t, []))
+
+
+def test_order4_and_ragged_ranks_use_generic_path():
+    rng = np.random.default_rng(7)
+    dims, ranks = [9, 7, 6, 5], [3, 2, 4, 2]
+    idx = np.unique(np.stack([rng.integers(0, d, 600) for d in dims], 1), axis=0)
+    vals = rng.uniform(0, 2, idx.shape[0])
+    b = api.DataBundle(api.SparseTensor(dims, idx, vals), [])
+    cfg = TrainConfig(ranks=ranks, seed=3, eta0=0.01, exec_mode="serial")
+    st = api.make_state(cfg, b)
+    tr = O.SerialTrainer(b, ranks, seed=3, eta0=0.01, mu=0.1, lambda_reg=0.1)
+    tr.model.copy_from(st.model)
+    tr.run_epoch()
+    api.run_epoch(st)
+    m = st.model
+    for a, ref in zip([m.core.reshape(-1)] + m.factors, [tr.model.core] + tr.model.factors):
+        scale_close(a, ref, 1e-2 * np.abs(ref).max(), 1e-4)
+    # Hogwild generic sweep runs and decreases the objective
+    st2 = api.make_state(TrainConfig(ranks=ranks, seed=3, eta0=0.01), b)
+    o0 = api.epoch_stats(st2, 0.1).objective
+    for _ in range(3):
+        api.run_epoch(st2)
+    assert api.epoch_stats(st2, 0.1).objective < o0
+    assert st2.kernel_info()["kernel"] == "generic"
+
+
+def test_nonnegative_clamp_keeps_parameters_nonnegative():
+    spec = synth.config1(literal=False)
+    spec.nnz, spec.dims = 5000, [50, 50, 50]
+    spec.matrices[0].cols, spec.matrices[0].nnz = 20, 500
+    b, _, _ = synth.generate(spec)
+    st = api.make_state(TrainConfig(ranks=[5, 5, 5], eta0=0.05, nonnegative=True), b)
+    for _ in range(3):
+        api.run_epoch(st)
+    m = st.model
+    for a in [m.core] + m.factors + m.couplings:
+        assert a.min() >= 0.0
+
+
+def test_empty_matrix_is_allowed():
+    d = load_npz("epochs.npz")
+    b = bundle_from(d, "b_")
+    b.matrices.append(api.CoupledMatrix(1, b.tensor.dims[1], 4, np.zeros((0, 2)), np.zeros(0), 1.0))
+    st = api.make_state(TrainConfig(ranks=[2, 2, 2], seed=17, eta0=0.01), b)
+    api.run_epoch(st)
+    assert np.isfinite(api.epoch_stats(st, 0.1).objective)
