@@ -69,6 +69,10 @@ typedef struct cmtf_gpu_config {
   int32_t sort_mode;     /* mode the COO is sorted by; -1 = auto        */
   int32_t force_generic; /* 1: use the generic-N kernels even when a
                             specialised one exists (testing)            */
+  int32_t order_policy;  /* entry order of the Hogwild sweep: 0 = sorted
+                            by sort_mode (row caching), 1 = a seeded random
+                            permutation (the reference's shuffled
+                            schedule, src/trainer.cpp:122-128)          */
 } cmtf_gpu_config;
 
 typedef struct cmtf_gpu_ctx cmtf_gpu_ctx;

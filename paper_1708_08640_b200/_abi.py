@@ -41,6 +41,7 @@ class cmtf_gpu_config(C.Structure):
         ("hog_threads", C.c_int32),
         ("sort_mode", C.c_int32),
         ("force_generic", C.c_int32),
+        ("order_policy", C.c_int32),
     ]
 
 

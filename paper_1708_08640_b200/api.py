@@ -140,6 +140,7 @@ class TrainConfig:
     hog_threads: int = 0
     sort_mode: int = -1
     force_generic: bool = False
+    order_policy: str = "sorted"  # "sorted" | "random"
 
     def to_c(self):
         c = _abi.cmtf_gpu_config()
@@ -159,6 +160,7 @@ class TrainConfig:
         c.hog_threads = self.hog_threads
         c.sort_mode = self.sort_mode
         c.force_generic = int(self.force_generic)
+        c.order_policy = 1 if self.order_policy == "random" else 0
         return c, ranks
 
 

@@ -161,10 +161,23 @@ void dfree(T*& p) {
 }
 
 // ---------------- preprocessing kernels ----------------
+// 32-bit avalanche hash (murmur3 finaliser) keyed by the seed: sorting by it
+// gives a seeded random permutation of the entries.
+__device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t seed) {
+  x ^= seed * 0x9e3779b9u;
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+
 __global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals,
                                    uint64_t nnz, int order, ModeTables mt,
-                                   int sort_mode, uint32_t* rec, uint32_t* keys,
-                                   uint32_t* ids, unsigned long long* bad) {
+                                   int sort_mode, uint32_t seed, uint32_t* rec,
+                                   uint32_t* keys, uint32_t* ids,
+                                   unsigned long long* bad) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     for (int n = 0; n < order; ++n) {
@@ -179,7 +192,7 @@ __global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals,
     const double v = vals[e];
     if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
     rec[e * (order + 1) + order] = __float_as_uint((float)v);
-    keys[e] = idx[e * order + sort_mode];
+    keys[e] = sort_mode >= 0 ? idx[e * order + sort_mode] : mix32((uint32_t)e, seed);
     ids[e] = (uint32_t)e;
   }
 }
@@ -204,8 +217,9 @@ __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
 
 __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
                                    uint64_t nnz, uint32_t rows, uint32_t cols,
-                                   uint32_t* rec, uint32_t* keys, uint32_t* ids,
-                                   uint32_t* count, unsigned long long* bad) {
+                                   int shuffled, uint32_t seed, uint32_t* rec,
+                                   uint32_t* keys, uint32_t* ids, uint32_t* count,
+                                   unsigned long long* bad) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = idx[2 * e], j = idx[2 * e + 1];
@@ -216,7 +230,7 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
     rec[3 * e] = i;
     rec[3 * e + 1] = j;
     rec[3 * e + 2] = __float_as_uint((float)v);
-    keys[e] = i;
+    keys[e] = shuffled ? mix32((uint32_t)e, seed) : i;
     ids[e] = (uint32_t)e;
   }
 }
@@ -546,7 +560,8 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
     a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
     a.nonneg = ctx->cfg.nonnegative;
     ctx->kernel_which = 1;
-    return launch_hog3(ctx, J, a, opt, ctx->sort_mode, ctx->cfg.hog_threads);
+    return launch_hog3(ctx, J, a, opt, ctx->cfg.order_policy == 1 ? 0 : ctx->sort_mode,
+                       ctx->cfg.hog_threads);
   }
   ctx->kernel_which = 0;
   HogArgs a{};
@@ -813,8 +828,10 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
   ModeTables mt = mode_tables(ctx);
+  const bool shuffled = ctx->cfg.order_policy == 1;
   pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-      d_idx, d_vals, nnz, N, mt, sm, d_rec, d_keys, d_ids, ctx->d_first);
+      d_idx, d_vals, nnz, N, mt, shuffled ? -1 : sm, (uint32_t)ctx->cfg.seed + 0x5bd1e995u,
+      d_rec, d_keys, d_ids, ctx->d_first);
   CU(cudaGetLastError());
   unsigned long long bad[2];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
@@ -837,7 +854,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
     return set_err(ctx, CMTF_EVALIDATION, "tensor value is not finite");
   }
   uint32_t* sorted_ids = nullptr;
-  TRY(sort_ids(ctx, d_keys, d_ids, nnz, dims[sm], &sorted_ids));
+  TRY(sort_ids(ctx, d_keys, d_ids, nnz, shuffled ? 0xffffffffu : dims[sm], &sorted_ids));
   cudaFree(d_keys);
   cudaFree(d_ids);
   TRY(dalloc(ctx, &ctx->rec, nnz * (N + 1)));
@@ -931,8 +948,11 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
                        ctx->stream));
     CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+    const int shuffled = ctx->cfg.order_policy == 1;
     pack_matrix_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-        d_idx, d_vals, nnz, rows, cols, d_rec, d_keys, d_ids, M.count, ctx->d_first);
+        d_idx, d_vals, nnz, rows, cols, shuffled,
+        (uint32_t)ctx->cfg.seed + 0x27d4eb2fu + (uint32_t)ctx->mats.size(), d_rec, d_keys,
+        d_ids, M.count, ctx->d_first);
     CU(cudaGetLastError());
     unsigned long long bad[2];
     CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
@@ -954,7 +974,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
     }
     uint32_t* sorted_ids = nullptr;
-    TRY(sort_ids(ctx, d_keys, d_ids, nnz, rows, &sorted_ids));
+    TRY(sort_ids(ctx, d_keys, d_ids, nnz, shuffled ? 0xffffffffu : rows, &sorted_ids));
     cudaFree(d_keys);
     cudaFree(d_ids);
     gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
@@ -1173,7 +1193,7 @@ int cmtf_gpu_test_rmse(cmtf_gpu_ctx* ctx, const uint32_t* idx, const double* val
   }
   CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
   pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-      d_idx, d_vals, nnz, N, mt, 0, d_rec, d_keys, d_ids, ctx->d_first);
+      d_idx, d_vals, nnz, N, mt, 0, 0u, d_rec, d_keys, d_ids, ctx->d_first);
   CU(cudaGetLastError());
   unsigned long long bad[2];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));

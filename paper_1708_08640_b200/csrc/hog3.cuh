@@ -48,7 +48,7 @@ struct Hog3Layout {
   struct B {
     static constexpr int NG = TILES >= BT ? 1 : BT / TILES;  // entry groups
     static constexpr int G_FLOATS = J1 * J2 * J3P;
-    static constexpr int PART_FLOATS = (NG - 1) * TILES * J3;
+    static constexpr int PART_FLOATS = round_up4((NG - 1) * TILES * J3);
     static constexpr int U1_FLOATS = J1P * BT;   // per-thread mode-1 row
     static constexpr int W1_FLOATS = J1 * BT;    // per-thread W1
     static constexpr int STAGE_FLOATS = SW * BT;
