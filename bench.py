@@ -42,6 +42,9 @@ def parse():
     p.add_argument("--scale", type=float, default=1.0)
     p.add_argument("--kernel", default="opt", choices=["opt", "naive"])
     p.add_argument("--hog-threads", type=int, default=0)
+    p.add_argument("--order", default="sorted", choices=["sorted", "random"])
+    p.add_argument("--uniform", action="store_true",
+                   help="diagnostic: uniform instead of Zipf indices")
     p.add_argument("--cpu-sample", type=int, default=600_000,
                    help="tensor entries in the bounded CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -58,6 +61,10 @@ def make_workload(args):
     from paper_1708_08640_b200 import synth
     if args.config == "config2":
         spec = synth.config2(args.scale)
+        if args.uniform:
+            spec.laws = ["uniform"] * 3
+            for m in spec.matrices:
+                m.row_law = m.col_law = "uniform"
         ranks = [10, 10, 10]
         lr, lam = 1e-3, 0.01
     elif args.config == "config1":
@@ -185,7 +192,8 @@ def run_ours(args):
         dist.init_process_group("nccl")
     spec, bundle, test, ranks, lr, lam = make_workload(args)
     cfg = api.TrainConfig(ranks=ranks, seed=rank, eta0=lr, lambda_reg=lam, kernel=args.kernel,
-                          device=local, hog_threads=args.hog_threads)
+                          device=local, hog_threads=args.hog_threads,
+                          order_policy=args.order)
     st = api.make_state(cfg, bundle)
     nt, Bt, Ft, mats = algorithmic(bundle, ranks)
     n_upd = nt + sum(n for n, _ in mats)

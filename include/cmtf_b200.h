@@ -73,6 +73,15 @@ typedef struct cmtf_gpu_config {
                             by sort_mode (row caching), 1 = a seeded random
                             permutation (the reference's shuffled
                             schedule, src/trainer.cpp:122-128)          */
+  float hot_tau;         /* rows whose expected concurrent updates
+                            (count * workers / nnz) reach hot_tau get a
+                            per-block shared-memory replica; 0 = default
+                            (2.0), < 0 disables                         */
+  float kappa;           /* damping of batched hot-row / core steps;
+                            0 = default (0.5)                           */
+  int32_t flush_every;   /* sweep iterations between replica/core merges;
+                            0 = default (8)                             */
+  int32_t kernel_version;/* 0 = auto (v2 where specialised), 1 = v1     */
 } cmtf_gpu_config;
 
 typedef struct cmtf_gpu_ctx cmtf_gpu_ctx;

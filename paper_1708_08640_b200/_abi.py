@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcmtf_b200.so")
+LIB_PATH = os.environ.get("CMTF_B200_LIB") or os.path.join(_HERE, "libcmtf_b200.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -42,6 +42,10 @@ class cmtf_gpu_config(C.Structure):
         ("sort_mode", C.c_int32),
         ("force_generic", C.c_int32),
         ("order_policy", C.c_int32),
+        ("hot_tau", C.c_float),
+        ("kappa", C.c_float),
+        ("flush_every", C.c_int32),
+        ("kernel_version", C.c_int32),
     ]
 
 

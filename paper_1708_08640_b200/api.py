@@ -140,7 +140,11 @@ class TrainConfig:
     hog_threads: int = 0
     sort_mode: int = -1
     force_generic: bool = False
-    order_policy: str = "sorted"  # "sorted" | "random"
+    order_policy: str = "random"  # "random" | "sorted"
+    hot_tau: float = 0.0  # 0 = default 2.0, < 0 disables hot-row replicas
+    kappa: float = 0.0  # 0 = default 0.5
+    flush_every: int = 0  # 0 = default 8
+    kernel_version: int = 0  # 0 = auto (v2), 1 = v1
 
     def to_c(self):
         c = _abi.cmtf_gpu_config()
@@ -161,6 +165,8 @@ class TrainConfig:
         c.sort_mode = self.sort_mode
         c.force_generic = int(self.force_generic)
         c.order_policy = 1 if self.order_policy == "random" else 0
+        c.hot_tau, c.kappa = self.hot_tau, self.kappa
+        c.flush_every, c.kernel_version = self.flush_every, self.kernel_version
         return c, ranks
 
 
@@ -278,7 +284,7 @@ class TrainState:
         w, t, s = C.c_int32(), C.c_int32(), C.c_int32()
         self._check(self._L.cmtf_gpu_kernel_info(self._h, C.byref(w), C.byref(t),
                                                   C.byref(s)))
-        return {"kernel": ["generic", "order3", "order4"][w.value],
+        return {"kernel": ["generic", "order3", "order4", "order3v2"][w.value],
                 "hog_threads": t.value, "sort_mode": s.value}
 
     def close(self):

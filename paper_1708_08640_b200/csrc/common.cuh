@@ -17,14 +17,37 @@ __host__ __device__ constexpr int round_up4(int j) { return (j + 3) & ~3; }
 // (L1 is not coherent across SMs, so an L1 hit could return a row this SM
 // read long ago); stores are plain global stores, which land in L2.
 // Lost updates and stale reads are allowed by design.
+#ifndef CMTF_ROW_LOAD
+#define CMTF_ROW_LOAD 0
+#endif
 __device__ __forceinline__ float4 ld_row4(const float* p) {
+#if CMTF_ROW_LOAD == 0
   return __ldcg(reinterpret_cast<const float4*>(p));
+#else
+  return *reinterpret_cast<const float4*>(p);
+#endif
 }
-__device__ __forceinline__ float ld_row1(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ float ld_row1(const float* p) {
+#if CMTF_ROW_LOAD == 0
+  return __ldcg(p);
+#else
+  return *p;
+#endif
+}
 __device__ __forceinline__ void st_row4(float* p, float4 v) {
+#if CMTF_ROW_LOAD == 2
+  *reinterpret_cast<float4*>(p) = v;
+#else
   __stcg(reinterpret_cast<float4*>(p), v);
+#endif
 }
-__device__ __forceinline__ void st_row1(float* p, float v) { __stcg(p, v); }
+__device__ __forceinline__ void st_row1(float* p, float v) {
+#if CMTF_ROW_LOAD == 2
+  *p = v;
+#else
+  __stcg(p, v);
+#endif
+}
 
 // Per-mode/per-matrix device tables passed by value to kernels.
 struct ModeTables {

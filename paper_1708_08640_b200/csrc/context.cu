@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "generic.cuh"
 #include "hog3.cuh"
+#include "hog3v2.cuh"
 
 using namespace cmtfb;
 
@@ -77,6 +78,23 @@ struct cmtf_gpu_ctx {
   double* d_partial = nullptr;
   uint64_t partial_cap = 0;
   unsigned long long* d_first = nullptr;
+
+  // v2 sweep state (built lazily after a bundle change)
+  bool v2_dirty = true;
+  uint4* mrec = nullptr;  // merged matrix records {row, col, bits(y), m}, random order
+  uint64_t mnnz = 0;
+  struct HotHost {
+    int32_t* slot = nullptr;
+    uint32_t* row_of = nullptr;
+    uint32_t H = 0;
+    float* base = nullptr;
+    uint64_t base_cap = 0;
+    uint32_t off = 0, stat_off = 0;
+  };
+  HotHost hot[kMaxOrder];
+  HotHost hotV[kMaxMats];
+  int v2_blocks = 0;
+  size_t v2_smem = 0;
 
   // timing
   cudaEvent_t ev[6] = {};
@@ -543,6 +561,234 @@ int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M, float eta) {
   return CMTF_OK;
 }
 
+// ---------------------------------------------------------------------
+// v2 epoch kernel (order 3, equal ranks): preparation and launch
+// ---------------------------------------------------------------------
+constexpr int kV2Warps = 8;
+
+bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
+  if (ctx->cfg.kernel_version == 1) return false;
+  if (!fast3_supported(ctx, J)) return false;
+  return *J == 4 || *J == 5 || *J == 8 || *J == 10;
+}
+
+__global__ void merge_matrix_kernel(const uint32_t* rec, uint64_t n, uint32_t m, uint64_t base,
+                                    uint32_t seed, uint4* out, uint32_t* keys, uint32_t* ids) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    out[base + e] = make_uint4(rec[3 * e], rec[3 * e + 1], rec[3 * e + 2], m);
+    keys[base + e] = mix32((uint32_t)(base + e), seed);
+    ids[base + e] = (uint32_t)(base + e);
+  }
+}
+
+__global__ void gather_uint4_kernel(const uint4* src, const uint32_t* ids, uint64_t n,
+                                    uint4* dst) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x)
+    dst[s] = src[ids[s]];
+}
+
+template <int J>
+size_t v2_fixed_bytes() {
+  return sizeof(float) * (size_t)V2Layout<J, true, kV2Warps>::FIXED_FLOATS;
+}
+
+size_t v2_fixed_bytes_rt(int J) {
+  switch (J) {
+    case 4: return v2_fixed_bytes<4>();
+    case 5: return v2_fixed_bytes<5>();
+    case 8: return v2_fixed_bytes<8>();
+    default: return v2_fixed_bytes<10>();
+  }
+}
+
+// Build the merged random-order matrix records and the hot-row replicas.
+int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
+  const uint32_t JP = (uint32_t)round_up4(J);
+  // grid: one block of kV2Warps warps per SM unless the caller caps workers
+  int blocks = ctx->num_sms;
+  if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (kV2Warps * 32));
+  else {
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (16ull * kV2Warps * 32));
+    blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
+  }
+  ctx->v2_blocks = blocks;
+  const double W = (double)blocks * kV2Warps * 32;
+
+  // merged matrix records (random order, seeded)
+  ctx->mnnz = 0;
+  for (auto& M : ctx->mats) ctx->mnnz += M.nnz;
+  dfree(ctx->mrec);
+  if (ctx->mnnz) {
+    uint4* tmp = nullptr;
+    uint32_t *keys = nullptr, *ids = nullptr, *sorted = nullptr;
+    TRY(dalloc(ctx, &tmp, ctx->mnnz));
+    TRY(dalloc(ctx, &keys, ctx->mnnz));
+    TRY(dalloc(ctx, &ids, ctx->mnnz));
+    uint64_t base = 0;
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      const auto& M = ctx->mats[m];
+      if (M.nnz)
+        merge_matrix_kernel<<<grid_for(M.nnz), 256, 0, ctx->stream>>>(
+            M.rec, M.nnz, (uint32_t)m, base, (uint32_t)ctx->cfg.seed + 0x27d4eb2fu, tmp, keys,
+            ids);
+      base += M.nnz;
+    }
+    CU(cudaGetLastError());
+    TRY(sort_ids(ctx, keys, ids, ctx->mnnz, 0xffffffffu, &sorted));
+    TRY(dalloc(ctx, &ctx->mrec, ctx->mnnz));
+    gather_uint4_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(tmp, sorted, ctx->mnnz,
+                                                                       ctx->mrec);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    cudaFree(tmp);
+    cudaFree(keys);
+    cudaFree(ids);
+    cudaFree(sorted);
+  }
+
+  // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
+  // within the shared-memory budget left after the fixed layout
+  float tau = ctx->cfg.hot_tau == 0.f ? 2.0f : ctx->cfg.hot_tau;
+  const size_t fixed = v2_fixed_bytes_rt(J);
+  const size_t limit = 227 * 1024 - 1024;
+  const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
+  struct Cand {
+    uint32_t count;
+    int arr;  // 0..N-1 modes, 100+m matrices
+    uint32_t row;
+  };
+  std::vector<Cand> cand;
+  std::vector<std::vector<uint32_t>> hcounts(ctx->order), vcounts(ctx->mats.size());
+  const uint64_t thr = tau > 0 ? (uint64_t)std::ceil(tau * (double)ctx->nnz / W) : ~0ull;
+  for (int n = 0; n < ctx->order; ++n) {
+    hcounts[n].resize(ctx->dims[n]);
+    CU(cudaMemcpy(hcounts[n].data(), ctx->count[n], ctx->dims[n] * sizeof(uint32_t),
+                  cudaMemcpyDeviceToHost));
+    if (tau > 0)
+      for (uint32_t i = 0; i < ctx->dims[n]; ++i)
+        if (hcounts[n][i] >= std::max<uint64_t>(thr, 1)) cand.push_back({hcounts[n][i], n, i});
+  }
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto& M = ctx->mats[m];
+    vcounts[m].resize(M.cols);
+    CU(cudaMemcpy(vcounts[m].data(), M.count, M.cols * sizeof(uint32_t),
+                  cudaMemcpyDeviceToHost));
+    // a V row's updates are spread over the same iterations as the tensor's
+    if (tau > 0)
+      for (uint32_t j = 0; j < M.cols; ++j)
+        if (vcounts[m][j] >= std::max<uint64_t>(thr, 1))
+          cand.push_back({vcounts[m][j], 100 + (int)m, j});
+  }
+  std::stable_sort(cand.begin(), cand.end(),
+                   [](const Cand& x, const Cand& y) { return x.count > y.count; });
+  const size_t per_row = JP + 2;
+  const size_t slack = 4 * (ctx->order + ctx->mats.size());  // alignment padding
+  size_t take = std::min(cand.size(), budget_floats > slack ? (budget_floats - slack) / per_row : 0);
+  std::vector<std::vector<uint32_t>> rows_of(ctx->order), vrows_of(ctx->mats.size());
+  for (size_t q = 0; q < take; ++q) {
+    if (cand[q].arr < 100) rows_of[cand[q].arr].push_back(cand[q].row);
+    else vrows_of[cand[q].arr - 100].push_back(cand[q].row);
+  }
+  uint32_t off = (uint32_t)(fixed / sizeof(float));
+  auto build = [&](cmtf_gpu_ctx::HotHost& h, const std::vector<uint32_t>& rows,
+                   uint32_t nrows) -> int {
+    dfree(h.slot);
+    dfree(h.row_of);
+    h.H = (uint32_t)rows.size();
+    if (!h.H) return CMTF_OK;
+    std::vector<int32_t> slot(nrows, -1);
+    for (uint32_t s = 0; s < h.H; ++s) slot[rows[s]] = (int32_t)s;
+    TRY(dalloc(ctx, &h.slot, nrows));
+    TRY(dalloc(ctx, &h.row_of, h.H));
+    CU(cudaMemcpy(h.slot, slot.data(), nrows * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h.row_of, rows.data(), h.H * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    const uint64_t need = (uint64_t)blocks * h.H * JP;
+    if (h.base_cap < need) {
+      TRY(dalloc(ctx, &h.base, need));
+      h.base_cap = need;
+    }
+    h.off = off;  // float4-aligned (off and H*JP are multiples of 4)
+    off += h.H * JP;
+    h.stat_off = off;
+    off += (2 * h.H + 3) & ~3u;
+    return CMTF_OK;
+  };
+  for (int n = 0; n < ctx->order; ++n) TRY(build(ctx->hot[n], rows_of[n], ctx->dims[n]));
+  for (size_t m = 0; m < ctx->mats.size(); ++m)
+    TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
+  ctx->v2_smem = (size_t)off * sizeof(float);
+  ctx->v2_dirty = false;
+  return CMTF_OK;
+}
+
+template <int J, bool OPT>
+int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
+  auto kern = hog3v2_kernel<J, OPT, kV2Warps>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->v2_smem));
+  kern<<<ctx->v2_blocks, kV2Warps * 32, ctx->v2_smem, ctx->stream>>>(args);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
+  if (ctx->v2_dirty) TRY(prepare_v2(ctx, J));
+  Hog3v2Args a{};
+  a.rec = reinterpret_cast<const uint4*>(ctx->rec);
+  a.nnz = ctx->nnz;
+  a.mrec = ctx->mrec;
+  a.mnnz = ctx->mnnz;
+  a.n_mat = (int)ctx->mats.size();
+  const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 8;
+  const double W = (double)ctx->v2_blocks * kV2Warps * 32;
+  const float nhat_scale = (float)(W * F / (double)ctx->nnz);
+  auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count) {
+    HotDesc d{};
+    d.slot = h.H ? h.slot : nullptr;
+    d.row_of = h.row_of;
+    d.count = count;
+    d.H = h.H;
+    d.off = h.off;
+    d.stat_off = h.stat_off;
+    d.base = h.base;
+    d.nhat_scale = nhat_scale;
+    return d;
+  };
+  for (int n = 0; n < 3; ++n) {
+    a.U[n] = ctx->U[n];
+    a.reg[n] = ctx->reg[n];
+    a.hot[n] = hd(ctx->hot[n], ctx->count[n]);
+  }
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto& M = ctx->mats[m];
+    a.mats[m].mode = M.mode;
+    a.mats[m].V = M.V;
+    a.mats[m].vreg = M.vreg;
+    a.mats[m].weight = (float)M.weight;
+    a.mats[m].hotV = hd(ctx->hotV[m], M.count);
+  }
+  a.G = ctx->G;
+  a.eta = eta;
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.kappa = ctx->cfg.kappa > 0.f ? ctx->cfg.kappa : 0.5f;
+  a.nhat_core = (float)(W * F);
+  a.flush_every = F;
+  a.nonneg = ctx->cfg.nonnegative;
+  ctx->kernel_which = 3;
+  ctx->hog_threads_used = (int)W;
+  const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
+#define V2_CASE(JV)                                                            \
+  case JV:                                                                     \
+    return opt ? launch_v2_t<JV, true>(ctx, a) : launch_v2_t<JV, false>(ctx, a);
+  switch (J) {
+    V2_CASE(4) V2_CASE(5) V2_CASE(8) V2_CASE(10)
+  }
+#undef V2_CASE
+  return set_err(ctx, CMTF_EUNSUPPORTED, "no v2 kernel for J=%d", J);
+}
+
 int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
   int J = 0;
@@ -706,6 +952,7 @@ void cmtf_gpu_config_default(cmtf_gpu_config* c) {
   c->init_scale = 1.0;
   c->exec_mode = CMTF_EXEC_HOGWILD;
   c->sort_mode = -1;
+  c->order_policy = 1;
 }
 
 const char* cmtf_gpu_last_error(void) { return g_last_error.c_str(); }
@@ -769,6 +1016,9 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
     dfree(m.V);
   }
   for (auto& m : ctx->spare) dfree(m.V);
+  dfree(ctx->mrec);
+  for (auto& h : ctx->hot) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
+  for (auto& h : ctx->hotV) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   dfree(ctx->G);
   dfree(ctx->d_sched);
   dfree(ctx->d_partial);
@@ -800,6 +1050,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
       ctx->dims.size() == (size_t)N && std::equal(ctx->dims.begin(), ctx->dims.end(), dims);
   ctx->dims.assign(dims, dims + N);
   ctx->nnz = nnz;
+  ctx->v2_dirty = true;
   if (!same_shape) ctx->have_model = false;
   int sm = ctx->cfg.sort_mode;
   if (sm < 0 || sm >= N) {
@@ -989,6 +1240,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->mats.push_back(M);
+  ctx->v2_dirty = true;
   return CMTF_OK;
 }
 
@@ -1103,14 +1355,22 @@ int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
     CU(cudaEventRecord(ctx->ev[1], ctx->stream));
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
   } else {
-    TRY(hogwild_tensor_sweep(ctx, eta));
-    ctx->last_launches += 1;
-    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-    for (auto& M : ctx->mats) {
-      TRY(matrix_sweep(ctx, M, eta));
-      ctx->last_launches += M.nnz ? 1 : 0;
+    int J = 0;
+    if (v2_supported(ctx, &J)) {
+      TRY(v2_epoch(ctx, J, eta));  // tensor + interleaved matrix entries
+      ctx->last_launches += 1;
+      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+      CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    } else {
+      TRY(hogwild_tensor_sweep(ctx, eta));
+      ctx->last_launches += 1;
+      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+      for (auto& M : ctx->mats) {
+        TRY(matrix_sweep(ctx, M, eta));
+        ctx->last_launches += M.nnz ? 1 : 0;
+      }
+      CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     }
-    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
   }
   std::string offender;
   TRY(scan_nonfinite(ctx, &offender));

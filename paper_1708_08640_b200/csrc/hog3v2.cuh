@@ -1,0 +1,635 @@
+// hog3v2.cuh -- order-3 S^3CMTF epoch kernel, B200 design (v2).
+//
+// One launch = one epoch over the tensor AND the coupled matrices.
+//
+// Work split: every lane of every warp owns a contiguous chunk of the
+// (randomly permuted) tensor COO and a contiguous chunk of the merged
+// matrix COO.  Warps run free (no block barrier inside the sweep); each
+// iteration a lane updates one tensor entry and the matrix entries that are
+// due so that matrix updates stay interleaved with tensor updates over the
+// whole epoch (as in the reference's merged shuffled schedule,
+// src/trainer.cpp:114-128).
+//
+// Per tensor entry (OPT = Algorithm 3 reuse; NAIVE =
+// Algorithm 2): the core G sits in shared memory and every
+// G[a,b,c] read (a broadcast LDS) feeds two FP32 FMAs -- t_ab += G u3[c] and
+// g3[c] += G u1[a]u2[b] -- then the J^2 terms W1, g2, x_hat.
+//
+// Core gradient dG = sum_e -r_e u1 (x) u2 (x) u3: per warp a 32-entry GEMM
+// on the tensor cores, D[c][ab] += U3^T[c][e] * Q[e][ab] with
+// Q[e][ab] = (-r u1)_e[a] u2_e[b], mma.sync m16n8k8 TF32 with the 3xTF32
+// split (hi*hi + hi*lo + lo*hi, ~fp32 accurate), accumulated into a
+// warp-private shared-memory copy and pushed to the global core with vector
+// REDs every `flush_every` iterations (the reference's designated-worker
+// core step, src/trainer.cpp:211-219, becomes a damped batched step).
+//
+// Parameter rows:
+//  * cold rows: relaxed Hogwild directly on global memory (the reference's
+//    relaxed.hpp contract; lost updates and stale reads allowed);
+//  * hot rows (small modes, Zipf heads, small coupled factors): a per-block
+//    shared-memory replica updated with shared atomics; the block pushes
+//    alpha * (replica - base) to global and re-bases every flush window,
+//    alpha = min(1, kappa / (eta * lambda_hat * n_hat)) with lambda_hat the
+//    mean curvature |c|^2 of the row's recent updates and n_hat the expected
+//    number of concurrent updates of that row GPU-wide in one window.  With
+//    no contention alpha = 1 (plain SGD); with heavy contention the merged
+//    step is the largest stable step of the batched least-squares problem.
+#pragma once
+
+#include "common.cuh"
+
+namespace cmtfb {
+
+constexpr int kV2MaxMats = 8;
+
+struct HotDesc {
+  const int32_t* slot;     // row -> slot, -1 cold; nullptr = no hot rows
+  const uint32_t* row_of;  // slot -> row
+  const uint32_t* count;   // per row observation count (for n_hat)
+  uint32_t H;              // number of hot rows
+  uint32_t off;            // float offset of the replica in shared memory
+  uint32_t stat_off;       // float offset of the (lam, cnt) stats
+  float* base;             // [gridDim.x][H][JP] global per-block base copies
+  float nhat_scale;        // n_hat = count * nhat_scale
+};
+
+struct MatDesc3 {
+  int mode;
+  float* V;
+  const float* vreg;  // lambda_m * lambda / col count
+  float weight;
+  HotDesc hotV;
+};
+
+struct Hog3v2Args {
+  const uint4* rec;     // tensor records {i1, i2, i3, bits(x)}, random order
+  uint64_t nnz;
+  const uint4* mrec;    // matrix records {row, col, bits(y), matrix id}
+  uint64_t mnnz;
+  int n_mat;
+  MatDesc3 mats[kV2MaxMats];
+  float* U[3];
+  const float* reg[3];
+  HotDesc hot[3];
+  float* G;
+  float eta;
+  float core_reg;   // lambda / nnz
+  float kappa;      // damping constant
+  float nhat_core;  // expected GPU-wide entries between two flushes of a warp
+  int flush_every;  // iterations between flushes
+  int nonneg;
+};
+
+// ---------------------------------------------------------------------
+// small PTX helpers
+// ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = to_tf32(x);
+  lo = to_tf32(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_strong4(const float* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_weak4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void st_weak4(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+
+// Row access: hot rows live in the shared replica, cold rows in global.
+template <int JP>
+__device__ __forceinline__ void load_row(const float* U, uint32_t i, int slot,
+                                         const float* rep, float* u) {
+  if (slot >= 0) {
+#pragma unroll
+    for (int k = 0; k < JP; k += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(rep + slot * JP + k);
+      u[k] = q.x; u[k + 1] = q.y; u[k + 2] = q.z; u[k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < JP; k += 4) {
+      const float4 q = ld_weak4(U + (uint64_t)i * JP + k);
+      u[k] = q.x; u[k + 1] = q.y; u[k + 2] = q.z; u[k + 3] = q.w;
+    }
+  }
+}
+
+// Apply a row step u <- u - eta * grad (clamped if nonneg).  Hot rows: the
+// delta is added to the shared replica atomically and the curvature stat is
+// accumulated; cold rows: plain store of the new value.
+template <int J, int JP>
+__device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* rep,
+                                         float* stat, const float* u, const float* grad,
+                                         float eta, int nonneg, float curv) {
+  if (slot >= 0) {
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      float d = -eta * grad[k];
+      if (nonneg && u[k] + d < 0.f) d = -u[k];
+      atomicAdd(rep + slot * JP + k, d);
+    }
+    atomicAdd(stat + 2 * slot, curv);
+    atomicAdd(stat + 2 * slot + 1, 1.f);
+  } else {
+    float v[JP];
+#pragma unroll
+    for (int k = 0; k < JP; ++k) {
+      float x = k < J ? u[k] - eta * grad[k] : 0.f;
+      if (nonneg) x = fmaxf(x, 0.f);
+      v[k] = x;
+    }
+#pragma unroll
+    for (int k = 0; k < JP; k += 4)
+      st_weak4(U + (uint64_t)i * JP + k, make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+  }
+}
+
+// Push the block's progress on hot rows [r0, r1) to global and re-base.
+template <int J, int JP>
+__device__ void flush_hot(const HotDesc& h, float* U, float* rep, float* stat, float eta,
+                          float kappa, int r0, int r1, int lane) {
+  float* base_b = h.base + (uint64_t)blockIdx.x * h.H * JP;
+  for (int s = r0 + lane; s < r1; s += 32) {
+    const float cnt = atomicExch(stat + 2 * s + 1, 0.f);
+    const float lam = atomicExch(stat + 2 * s, 0.f);
+    const uint32_t row = __ldg(h.row_of + s);
+    float* g = U + (uint64_t)row * JP;
+    float alpha = 1.f;
+    if (cnt > 0.f) {
+      const float nhat = fmaxf(cnt, (float)__ldg(h.count + row) * h.nhat_scale);
+      const float q = eta * (lam / cnt) * nhat;
+      alpha = q > kappa ? kappa / q : 1.f;
+    }
+#pragma unroll
+    for (int k = 0; k < JP; k += 4) {
+      const float4 sv = *reinterpret_cast<const float4*>(rep + s * JP + k);
+      const float4 bv = ld_weak4(base_b + s * JP + k);
+      if (cnt > 0.f)
+        red_add_v4(g + k, make_float4(alpha * (sv.x - bv.x), alpha * (sv.y - bv.y),
+                                      alpha * (sv.z - bv.z), alpha * (sv.w - bv.w)));
+      const float4 gv = ld_strong4(g + k);
+      st_weak4(base_b + s * JP + k, gv);
+      atomicAdd(rep + s * JP + k + 0, gv.x - sv.x);
+      atomicAdd(rep + s * JP + k + 1, gv.y - sv.y);
+      atomicAdd(rep + s * JP + k + 2, gv.z - sv.z);
+      atomicAdd(rep + s * JP + k + 3, gv.w - sv.w);
+    }
+  }
+}
+
+// Initial replica load (also sets the per-block base).
+template <int JP>
+__device__ void load_hot(const HotDesc& h, const float* U, float* rep, float* stat) {
+  float* base_b = h.base + (uint64_t)blockIdx.x * h.H * JP;
+  for (uint32_t q = threadIdx.x; q < h.H * (JP / 4); q += blockDim.x) {
+    const uint32_t s = q / (JP / 4), k = (q % (JP / 4)) * 4;
+    const float4 v = ld_strong4(U + (uint64_t)__ldg(h.row_of + s) * JP + k);
+    *reinterpret_cast<float4*>(rep + s * JP + k) = v;
+    st_weak4(base_b + s * JP + k, v);
+  }
+  for (uint32_t s = threadIdx.x; s < 2 * h.H; s += blockDim.x) stat[s] = 0.f;
+}
+
+template <int J, bool OPT, int NW>
+struct V2Layout {
+  static constexpr int JP = round_up4(J);
+  static constexpr int AB = J * J;            // core rows (a,b)
+  // stage row width: >= 3*JP, multiple of 4, and == 8 or 24 mod 32 so the
+  // 4 entry rows a quad touches fall in distinct bank groups
+  static constexpr int sw_pick(int x) {
+    return ((x % 32) == 8 || (x % 32) == 24) ? x : sw_pick(x + 4);
+  }
+  static constexpr int SW = sw_pick(3 * JP);
+  static constexpr int NT = (AB + 7) / 8;     // ab tiles of 8 (mma N)
+  static constexpr int MT = (J + 15) / 16;    // c tiles of 16 (mma M)
+  static constexpr int G_FLOATS = AB * JP;    // shared core [ab][JP]
+  static constexpr int DG_FLOATS = AB * JP;   // per-warp core-grad accum
+  static constexpr int STAGE_FLOATS = 32 * SW;
+  static constexpr int FIXED_FLOATS = G_FLOATS + NW * (DG_FLOATS + STAGE_FLOATS);
+};
+
+template <int J, bool OPT, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+hog3v2_kernel(Hog3v2Args a) {
+  using L = V2Layout<J, OPT, NW>;
+  constexpr int JP = L::JP;
+  constexpr int AB = L::AB;
+  extern __shared__ __align__(16) float sm[];
+  float* Gs = sm;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* dGw = sm + L::G_FLOATS + w * (L::DG_FLOATS + L::STAGE_FLOATS);
+  float* stg = dGw + L::DG_FLOATS;
+  const int g8 = lane >> 2, t4 = lane & 3;
+
+  // ---- prologue: core copy, hot replicas ----
+  for (int q = threadIdx.x; q < AB * JP; q += blockDim.x) {
+    const int c = q % JP, ab = q / JP;
+    Gs[q] = c < J ? __ldcg(a.G + ab * J + c) : 0.f;
+  }
+  for (int q = lane; q < L::DG_FLOATS; q += 32) dGw[q] = 0.f;
+#pragma unroll
+  for (int n = 0; n < 3; ++n)
+    if (a.hot[n].H) load_hot<JP>(a.hot[n], a.U[n], sm + a.hot[n].off, sm + a.hot[n].stat_off);
+  for (int m = 0; m < a.n_mat; ++m)
+    if (a.mats[m].hotV.H)
+      load_hot<JP>(a.mats[m].hotV, a.mats[m].V, sm + a.mats[m].hotV.off,
+                   sm + a.mats[m].hotV.stat_off);
+  __syncthreads();
+
+  const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
+  const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
+  const uint64_t lo = a.nnz * gl / Wt, hi = a.nnz * (gl + 1) / Wt;
+  const uint64_t iters = (a.nnz + Wt - 1) / Wt;
+  const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
+  uint64_t mpos = mlo;
+  float kw = 0.f;      // entries since the warp's last core flush (lane-local)
+  float lamG = 0.f;    // sum |phi|^2 since the last flush (lane-local)
+
+  const float* rep[3];
+  float* stat[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    rep[n] = sm + a.hot[n].off;
+    stat[n] = sm + a.hot[n].stat_off;
+  }
+
+  uint4 nrec = make_uint4(0, 0, 0, 0);
+  if (lo < hi) nrec = __ldg(a.rec + lo);
+
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e = lo + it;
+    const bool active = e < hi;
+    const uint4 rc = nrec;
+    if (e + 1 < hi) nrec = __ldg(a.rec + e + 1);
+    float r = 0.f;
+    float u1[JP], u2[JP], u3[JP];
+    if (active) {
+      int sl[3];
+      const uint32_t ix[3] = {rc.x, rc.y, rc.z};
+#pragma unroll
+      for (int n = 0; n < 3; ++n) sl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + ix[n]) : -1;
+      load_row<JP>(a.U[0], rc.x, sl[0], rep[0], u1);
+      load_row<JP>(a.U[1], rc.y, sl[1], rep[1], u2);
+      load_row<JP>(a.U[2], rc.z, sl[2], rep[2], u3);
+      const float reg1 = __ldg(a.reg[0] + rc.x), reg2 = __ldg(a.reg[1] + rc.y),
+                  reg3 = __ldg(a.reg[2] + rc.z);
+      float w1[J], g2[J], g3[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) { w1[k] = 0.f; g2[k] = 0.f; g3[k] = 0.f; }
+      float xh = 0.f;
+      if (OPT) {
+#pragma unroll 1
+        for (int ia = 0; ia < J; ++ia) {
+          // u1[ia] with a runtime index: select through the unrolled row
+          float ua = 0.f;
+#pragma unroll
+          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
+          const float* grow = Gs + ia * J * JP;
+          float wsum = 0.f;
+#pragma unroll
+          for (int ib = 0; ib < J; ++ib) {
+            float gv[JP];
+#pragma unroll
+            for (int c = 0; c < JP; c += 4) {
+              const float4 q = *reinterpret_cast<const float4*>(grow + ib * JP + c);
+              gv[c] = q.x; gv[c + 1] = q.y; gv[c + 2] = q.z; gv[c + 3] = q.w;
+            }
+            float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < J; ++c) {
+              if (c & 1) t1 = fmaf(gv[c], u3[c], t1);
+              else t0 = fmaf(gv[c], u3[c], t0);
+            }
+            const float p = ua * u2[ib];
+#pragma unroll
+            for (int c = 0; c < J; ++c) g3[c] = fmaf(gv[c], p, g3[c]);
+            const float tab = t0 + t1;
+            wsum = fmaf(tab, u2[ib], wsum);
+            g2[ib] = fmaf(tab, ua, g2[ib]);
+          }
+#pragma unroll
+          for (int k = 0; k < J; ++k) w1[k] = (k == ia) ? wsum : w1[k];
+          xh = fmaf(wsum, ua, xh);
+        }
+      } else {
+        // Algorithm 2: separate walks (predict, then each contract_all_but)
+#pragma unroll 1
+        for (int ia = 0; ia < J; ++ia) {
+          float ua = 0.f;
+#pragma unroll
+          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
+          const float* grow = Gs + ia * J * JP;
+#pragma unroll
+          for (int ib = 0; ib < J; ++ib) {
+            float tab = 0.f;
+#pragma unroll
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
+            xh = fmaf(tab * u2[ib], ua, xh);
+          }
+        }
+        asm volatile("" ::: "memory");
+#pragma unroll 1
+        for (int ia = 0; ia < J; ++ia) {
+          const float* grow = Gs + ia * J * JP;
+          float wsum = 0.f;
+#pragma unroll
+          for (int ib = 0; ib < J; ++ib) {
+            float tab = 0.f;
+#pragma unroll
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
+            wsum = fmaf(tab, u2[ib], wsum);
+          }
+#pragma unroll
+          for (int k = 0; k < J; ++k) w1[k] = (k == ia) ? wsum : w1[k];
+        }
+        asm volatile("" ::: "memory");
+#pragma unroll 1
+        for (int ia = 0; ia < J; ++ia) {
+          float ua = 0.f;
+#pragma unroll
+          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
+          const float* grow = Gs + ia * J * JP;
+#pragma unroll
+          for (int ib = 0; ib < J; ++ib) {
+            float tab = 0.f;
+#pragma unroll
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
+            g2[ib] = fmaf(tab, ua, g2[ib]);
+          }
+        }
+        asm volatile("" ::: "memory");
+#pragma unroll 1
+        for (int ia = 0; ia < J; ++ia) {
+          float ua = 0.f;
+#pragma unroll
+          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
+          const float* grow = Gs + ia * J * JP;
+#pragma unroll
+          for (int ib = 0; ib < J; ++ib) {
+            const float p = ua * u2[ib];
+#pragma unroll
+            for (int c = 0; c < J; ++c) g3[c] = fmaf(grow[ib * JP + c], p, g3[c]);
+          }
+        }
+      }
+      r = __uint_as_float(rc.w) - xh;
+      // core-gradient curvature |phi|^2 = prod_n |u_n|^2
+      float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < J; ++k) {
+        n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[k], u2[k], n2); n3 = fmaf(u3[k], u3[k], n3);
+        c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[k], g2[k], c2); c3 = fmaf(g3[k], g3[k], c3);
+      }
+      lamG += n1 * n2 * n3;
+      kw += 1.f;
+      // stage (-r u1, u2, u3) at pre-update values
+      float* st = stg + lane * L::SW;
+#pragma unroll
+      for (int k = 0; k < JP; k += 4) {
+        *reinterpret_cast<float4*>(st + k) =
+            make_float4(-r * u1[k], -r * u1[k + 1], -r * u1[k + 2], -r * u1[k + 3]);
+        *reinterpret_cast<float4*>(st + JP + k) = make_float4(u2[k], u2[k + 1], u2[k + 2], u2[k + 3]);
+        *reinterpret_cast<float4*>(st + 2 * JP + k) =
+            make_float4(u3[k], u3[k + 1], u3[k + 2], u3[k + 3]);
+      }
+      // row steps: grad = -r c + reg u
+      float gr[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1 * u1[k]);
+      step_row<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0], u1, gr, a.eta,
+                      a.nonneg, c1);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], reg2 * u2[k]);
+      step_row<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1], u2, gr, a.eta,
+                      a.nonneg, c2);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], reg3 * u3[k]);
+      step_row<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2], u3, gr, a.eta,
+                      a.nonneg, c3);
+    } else {
+      float* st = stg + lane * L::SW;
+#pragma unroll
+      for (int k = 0; k < L::SW; k += 4)
+        *reinterpret_cast<float4*>(st + k) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+
+    // ---- core gradient of the warp's 32 entries on the tensor cores ----
+    // D[c][ab] += sum_e U3^T[c][e] * Q[e][ab]   (M = c, N = ab, K = e)
+#pragma unroll
+    for (int mt = 0; mt < L::MT; ++mt) {
+      uint32_t ah[4][4], al[4][4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int e0 = ks * 8 + t4, e1 = e0 + 4;
+        const int c0 = mt * 16 + g8, c1 = c0 + 8;
+        const float x0 = c0 < J ? stg[e0 * L::SW + 2 * JP + c0] : 0.f;
+        const float x1 = c1 < J ? stg[e0 * L::SW + 2 * JP + c1] : 0.f;
+        const float x2 = c0 < J ? stg[e1 * L::SW + 2 * JP + c0] : 0.f;
+        const float x3 = c1 < J ? stg[e1 * L::SW + 2 * JP + c1] : 0.f;
+        split_tf32(x0, ah[ks][0], al[ks][0]);
+        split_tf32(x1, ah[ks][1], al[ks][1]);
+        split_tf32(x2, ah[ks][2], al[ks][2]);
+        split_tf32(x3, ah[ks][3], al[ks][3]);
+      }
+#pragma unroll 1
+      for (int nt = 0; nt < L::NT; ++nt) {
+        const int ab = nt * 8 + g8;
+        const int ia = ab / J, ib = ab - (ab / J) * J;
+        const bool ok = ab < AB;
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int e0 = ks * 8 + t4, e1 = e0 + 4;
+          const float q0 = ok ? stg[e0 * L::SW + ia] * stg[e0 * L::SW + JP + ib] : 0.f;
+          const float q1 = ok ? stg[e1 * L::SW + ia] * stg[e1 * L::SW + JP + ib] : 0.f;
+          uint32_t bh[2], bl[2];
+          split_tf32(q0, bh[0], bl[0]);
+          split_tf32(q1, bh[1], bl[1]);
+          mma_tf32(d, ah[ks], bh);
+          mma_tf32(d, ah[ks], bl);
+          mma_tf32(d, al[ks], bh);
+        }
+        // d: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
+        const int abo = nt * 8 + 2 * t4;
+        const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
+        if (abo < AB) {
+          if (cr0 < J) dGw[abo * JP + cr0] += d[0];
+          if (cr1 < J) dGw[abo * JP + cr1] += d[2];
+        }
+        if (abo + 1 < AB) {
+          if (cr0 < J) dGw[(abo + 1) * JP + cr0] += d[1];
+          if (cr1 < J) dGw[(abo + 1) * JP + cr1] += d[3];
+        }
+      }
+    }
+
+    // ---- matrix entries due by this iteration (interleaved) ----
+    {
+      const uint64_t due = mlo + (mhi - mlo) * (it + 1) / iters;
+      while (mpos < due) {
+        const uint4 mr = __ldg(a.mrec + mpos);
+        ++mpos;
+        const MatDesc3& M = a.mats[mr.w];
+        const int mode = M.mode;
+        const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
+        const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
+        float uu[JP], vv[JP];
+        float* repU = sm + a.hot[mode].off;
+        float* repV = sm + M.hotV.off;
+        load_row<JP>(a.U[mode], mr.x, su, repU, uu);
+        load_row<JP>(M.V, mr.y, sv, repV, vv);
+        float yh = 0.f, nu = 0.f, nv = 0.f;
+#pragma unroll
+        for (int k = 0; k < J; ++k) {
+          yh = fmaf(uu[k], vv[k], yh);
+          nu = fmaf(uu[k], uu[k], nu);
+          nv = fmaf(vv[k], vv[k], nv);
+        }
+        const float rr = __uint_as_float(mr.z) - yh;
+        const float vr = __ldg(M.vreg + mr.y);
+        float du[J], dv[J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) {  // src/gradients.cpp:241-247
+          du[k] = -M.weight * rr * vv[k];
+          dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
+        }
+        step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
+                        a.nonneg, M.weight * nv);
+        step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
+                        M.weight * nu);
+      }
+    }
+
+    // ---- periodic flushes (staggered across warps) ----
+    if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {
+      // core: damped batched step from this warp's accumulated gradient
+      const float kws = warp_sum(kw);
+      const float lgs = warp_sum(lamG);
+      if (kws > 0.f) {
+        const float q = a.eta * (lgs / kws) * a.nhat_core;
+        const float alpha = q > a.kappa ? a.kappa / q : 1.f;
+        const float s = -a.eta * alpha;
+        for (int ab = lane; ab < AB; ab += 32) {
+#pragma unroll
+          for (int c = 0; c < JP; c += 4) {
+            float4 dv = *reinterpret_cast<float4*>(dGw + ab * JP + c);
+            const float4 gv = *reinterpret_cast<const float4*>(Gs + ab * JP + c);
+            dv.x = s * fmaf(kws * a.core_reg, gv.x, dv.x);
+            dv.y = s * fmaf(kws * a.core_reg, gv.y, dv.y);
+            dv.z = s * fmaf(kws * a.core_reg, gv.z, dv.z);
+            dv.w = s * fmaf(kws * a.core_reg, gv.w, dv.w);
+            *reinterpret_cast<float4*>(dGw + ab * JP + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            // global core is unpadded [ab][J]: scalar REDs for the J valid columns
+            if (c + 0 < J) atomicAdd(a.G + ab * J + c + 0, dv.x);
+            if (c + 1 < J) atomicAdd(a.G + ab * J + c + 1, dv.y);
+            if (c + 2 < J) atomicAdd(a.G + ab * J + c + 2, dv.z);
+            if (c + 3 < J) atomicAdd(a.G + ab * J + c + 3, dv.w);
+          }
+        }
+      }
+      kw = 0.f;
+      lamG = 0.f;
+      __syncwarp();
+      // refresh this warp's share of the shared core
+      for (int q = w * 32 + lane; q < AB * J; q += NW * 32) {
+        float v = __ldcg(a.G + q);
+        if (a.nonneg) v = fmaxf(v, 0.f);
+        Gs[(q / J) * JP + (q % J)] = v;
+      }
+      // hot rows: this warp's share
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const HotDesc& h = a.hot[n];
+        if (h.H) {
+          const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+          flush_hot<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1, lane);
+        }
+      }
+      for (int m = 0; m < a.n_mat; ++m) {
+        const HotDesc& h = a.mats[m].hotV;
+        if (h.H) {
+          const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+          flush_hot<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
+                           lane);
+        }
+      }
+    }
+  }
+  // remaining matrix entries (rounding) and final hot flush of everything
+  while (mpos < mhi) {
+    const uint4 mr = __ldg(a.mrec + mpos);
+    ++mpos;
+    const MatDesc3& M = a.mats[mr.w];
+    const int mode = M.mode;
+    const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
+    const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
+    float uu[JP], vv[JP];
+    float* repU = sm + a.hot[mode].off;
+    float* repV = sm + M.hotV.off;
+    load_row<JP>(a.U[mode], mr.x, su, repU, uu);
+    load_row<JP>(M.V, mr.y, sv, repV, vv);
+    float yh = 0.f, nu = 0.f, nv = 0.f;
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      yh = fmaf(uu[k], vv[k], yh);
+      nu = fmaf(uu[k], uu[k], nu);
+      nv = fmaf(vv[k], vv[k], nv);
+    }
+    const float rr = __uint_as_float(mr.z) - yh;
+    const float vr = __ldg(M.vreg + mr.y);
+    float du[J], dv[J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      du[k] = -M.weight * rr * vv[k];
+      dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
+    }
+    step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
+                    a.nonneg, M.weight * nv);
+    step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
+                    M.weight * nu);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const HotDesc& h = a.hot[n];
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1, lane);
+    }
+  }
+  for (int m = 0; m < a.n_mat; ++m) {
+    const HotDesc& h = a.mats[m].hotV;
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
+                       lane);
+    }
+  }
+}
+
+}  // namespace cmtfb

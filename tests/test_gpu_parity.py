@@ -201,7 +201,7 @@ def test_hogwild_rmse_within_1pct_of_oracle(kernel, generic):
     for _ in range(epochs):
         api.run_epoch(st)
     info = st.kernel_info()
-    assert info["kernel"] == ("generic" if generic else "order3")
+    assert info["kernel"] == "generic" if generic else info["kernel"].startswith("order3")
     gpu_test = api.test_rmse(st, test)
     gpu_train = api.epoch_stats(st, 0.01).train_rmse
     assert abs(gpu_test - ref_test) <= 0.01 * ref_test, (gpu_test, ref_test, info)
