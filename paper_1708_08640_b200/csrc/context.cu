@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <limits>
 #include <random>
 #include <string>
@@ -94,6 +95,7 @@ struct cmtf_gpu_ctx {
   HotHost hot[kMaxOrder];
   HotHost hotV[kMaxMats];
   int v2_blocks = 0;
+  int v2_nw = 12;
   size_t v2_smem = 0;
 
   // timing
@@ -564,7 +566,7 @@ int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M, float eta) {
 // ---------------------------------------------------------------------
 // v2 epoch kernel (order 3, equal ranks): preparation and launch
 // ---------------------------------------------------------------------
-constexpr int kV2Warps = 8;
+constexpr int kV2Warps = 8;  // default; 12 when registers and shared memory allow
 
 bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
   if (ctx->cfg.kernel_version == 1) return false;
@@ -589,32 +591,52 @@ __global__ void gather_uint4_kernel(const uint4* src, const uint32_t* ids, uint6
     dst[s] = src[ids[s]];
 }
 
-template <int J>
+template <int J, int NW>
 size_t v2_fixed_bytes() {
-  return sizeof(float) * (size_t)V2Layout<J, true, kV2Warps>::FIXED_FLOATS;
+  return sizeof(float) * (size_t)V2Layout<J, true, NW>::FIXED_FLOATS;
 }
 
-size_t v2_fixed_bytes_rt(int J) {
-  switch (J) {
-    case 4: return v2_fixed_bytes<4>();
-    case 5: return v2_fixed_bytes<5>();
-    case 8: return v2_fixed_bytes<8>();
-    default: return v2_fixed_bytes<10>();
+size_t v2_fixed_bytes_rt(int J, int NW) {
+  if (NW == 12) {
+    switch (J) {
+      case 4: return v2_fixed_bytes<4, 12>();
+      case 5: return v2_fixed_bytes<5, 12>();
+      case 8: return v2_fixed_bytes<8, 12>();
+      default: return v2_fixed_bytes<10, 12>();
+    }
   }
+  switch (J) {
+    case 4: return v2_fixed_bytes<4, 8>();
+    case 5: return v2_fixed_bytes<5, 8>();
+    case 8: return v2_fixed_bytes<8, 8>();
+    default: return v2_fixed_bytes<10, 8>();
+  }
+}
+
+int v2_warps(const cmtf_gpu_ctx* ctx) {
+  const char* e = std::getenv("CMTF_V2_WARPS");
+  if (e) return std::atoi(e) == 8 ? 8 : 12;
+  (void)ctx;
+  return 12;
 }
 
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const uint32_t JP = (uint32_t)round_up4(J);
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
+  const int NW = v2_warps(ctx);
+  ctx->v2_nw = NW;
   int blocks = ctx->num_sms;
-  if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (kV2Warps * 32));
+  if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (NW * 32));
   else {
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (16ull * kV2Warps * 32));
+    // auto: at least ~64 entries per worker per epoch (at most 1/64 of the
+    // data in flight), so small problems stay close to sequential SGD while
+    // large ones fill every SM
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (64ull * NW * 32));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->v2_blocks = blocks;
-  const double W = (double)blocks * kV2Warps * 32;
+  const double W = (double)blocks * NW * 32;
 
   // merged matrix records (random order, seeded)
   ctx->mnnz = 0;
@@ -651,7 +673,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 2.0f : ctx->cfg.hot_tau;
-  const size_t fixed = v2_fixed_bytes_rt(J);
+  const size_t fixed = v2_fixed_bytes_rt(J, NW);
   const size_t limit = 227 * 1024 - 1024;
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   struct Cand {
@@ -723,14 +745,20 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   return CMTF_OK;
 }
 
-template <int J, bool OPT>
-int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  auto kern = hog3v2_kernel<J, OPT, kV2Warps>;
+template <int J, bool OPT, int NW>
+int launch_v2_nw(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
+  auto kern = hog3v2_kernel<J, OPT, NW>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)ctx->v2_smem));
-  kern<<<ctx->v2_blocks, kV2Warps * 32, ctx->v2_smem, ctx->stream>>>(args);
+  kern<<<ctx->v2_blocks, NW * 32, ctx->v2_smem, ctx->stream>>>(args);
   CU(cudaGetLastError());
   return CMTF_OK;
+}
+
+template <int J, bool OPT>
+int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
+  return ctx->v2_nw == 12 ? launch_v2_nw<J, OPT, 12>(ctx, args)
+                          : launch_v2_nw<J, OPT, 8>(ctx, args);
 }
 
 int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
@@ -742,7 +770,7 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
   a.mnnz = ctx->mnnz;
   a.n_mat = (int)ctx->mats.size();
   const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 8;
-  const double W = (double)ctx->v2_blocks * kV2Warps * 32;
+  const double W = (double)ctx->v2_blocks * ctx->v2_nw * 32;
   const float nhat_scale = (float)(W * F / (double)ctx->nnz);
   auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count) {
     HotDesc d{};

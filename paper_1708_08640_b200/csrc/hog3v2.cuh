@@ -88,9 +88,13 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+// 3xTF32 split by truncation: hi keeps the top 10 mantissa bits (exactly a
+// tf32), lo = x - hi is exact in fp32 and is passed as raw bits (the tensor
+// core reads the tf32 field, truncating lo's last bits): x - (hi + lo_tf32)
+// is below 2^-21 |x|.  Two instructions instead of two cvt.rna sequences.
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = to_tf32(x);
-  lo = to_tf32(x - __uint_as_float(hi));
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
   asm volatile(
@@ -146,14 +150,27 @@ __device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* 
                                          float* stat, const float* u, const float* grad,
                                          float eta, int nonneg, float curv) {
   if (slot >= 0) {
+    // Hogwild on the block's replica: plain RMW of the delta (shared float
+    // atomics are CAS loops on this part; lost updates are allowed, as in
+    // the reference's relaxed.hpp contract).  The curvature stat is a plain
+    // RMW too; the observation count is a native integer atomic.
+    float* rp = rep + slot * JP;
 #pragma unroll
-    for (int k = 0; k < J; ++k) {
-      float d = -eta * grad[k];
-      if (nonneg && u[k] + d < 0.f) d = -u[k];
-      atomicAdd(rep + slot * JP + k, d);
+    for (int k = 0; k < JP; k += 4) {
+      float4 cur = *reinterpret_cast<float4*>(rp + k);
+      float d0 = k + 0 < J ? -eta * grad[k + 0] : 0.f;
+      float d1 = k + 1 < J ? -eta * grad[k + 1] : 0.f;
+      float d2 = k + 2 < J ? -eta * grad[k + 2] : 0.f;
+      float d3 = k + 3 < J ? -eta * grad[k + 3] : 0.f;
+      cur.x += d0; cur.y += d1; cur.z += d2; cur.w += d3;
+      if (nonneg) {
+        cur.x = fmaxf(cur.x, 0.f); cur.y = fmaxf(cur.y, 0.f);
+        cur.z = fmaxf(cur.z, 0.f); cur.w = fmaxf(cur.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(rp + k) = cur;
     }
-    atomicAdd(stat + 2 * slot, curv);
-    atomicAdd(stat + 2 * slot + 1, 1.f);
+    stat[2 * slot] += curv;
+    atomicAdd(reinterpret_cast<int*>(stat) + 2 * slot + 1, 1);
   } else {
     float v[JP];
 #pragma unroll
@@ -174,7 +191,7 @@ __device__ void flush_hot(const HotDesc& h, float* U, float* rep, float* stat, f
                           float kappa, int r0, int r1, int lane) {
   float* base_b = h.base + (uint64_t)blockIdx.x * h.H * JP;
   for (int s = r0 + lane; s < r1; s += 32) {
-    const float cnt = atomicExch(stat + 2 * s + 1, 0.f);
+    const float cnt = (float)atomicExch(reinterpret_cast<int*>(stat) + 2 * s + 1, 0);
     const float lam = atomicExch(stat + 2 * s, 0.f);
     const uint32_t row = __ldg(h.row_of + s);
     float* g = U + (uint64_t)row * JP;
@@ -193,10 +210,10 @@ __device__ void flush_hot(const HotDesc& h, float* U, float* rep, float* stat, f
                                       alpha * (sv.z - bv.z), alpha * (sv.w - bv.w)));
       const float4 gv = ld_strong4(g + k);
       st_weak4(base_b + s * JP + k, gv);
-      atomicAdd(rep + s * JP + k + 0, gv.x - sv.x);
-      atomicAdd(rep + s * JP + k + 1, gv.y - sv.y);
-      atomicAdd(rep + s * JP + k + 2, gv.z - sv.z);
-      atomicAdd(rep + s * JP + k + 3, gv.w - sv.w);
+      // re-base, keeping local progress made since the snapshot
+      float4 cur = *reinterpret_cast<float4*>(rep + s * JP + k);
+      cur.x += gv.x - sv.x; cur.y += gv.y - sv.y; cur.z += gv.z - sv.z; cur.w += gv.w - sv.w;
+      *reinterpret_cast<float4*>(rep + s * JP + k) = cur;
     }
   }
 }
@@ -301,13 +318,16 @@ hog3v2_kernel(Hog3v2Args a) {
 #pragma unroll
       for (int k = 0; k < J; ++k) { w1[k] = 0.f; g2[k] = 0.f; g3[k] = 0.f; }
       float xh = 0.f;
+      // u1 and W1 live in this lane's staging row during the sweep so the
+      // a-loop can stay rolled (small code, no register selects)
+      float* myst = stg + lane * L::SW;
+#pragma unroll
+      for (int k = 0; k < JP; k += 4)
+        *reinterpret_cast<float4*>(myst + k) = make_float4(u1[k], u1[k + 1], u1[k + 2], u1[k + 3]);
       if (OPT) {
 #pragma unroll 1
         for (int ia = 0; ia < J; ++ia) {
-          // u1[ia] with a runtime index: select through the unrolled row
-          float ua = 0.f;
-#pragma unroll
-          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
+          const float ua = myst[ia];
           const float* grow = Gs + ia * J * JP;
           float wsum = 0.f;
 #pragma unroll
@@ -331,10 +351,11 @@ hog3v2_kernel(Hog3v2Args a) {
             wsum = fmaf(tab, u2[ib], wsum);
             g2[ib] = fmaf(tab, ua, g2[ib]);
           }
-#pragma unroll
-          for (int k = 0; k < J; ++k) w1[k] = (k == ia) ? wsum : w1[k];
+          myst[JP + ia] = wsum;
           xh = fmaf(wsum, ua, xh);
         }
+#pragma unroll
+        for (int k = 0; k < J; ++k) w1[k] = myst[JP + k];
       } else {
         // Algorithm 2: separate walks (predict, then each contract_all_but)
 #pragma unroll 1

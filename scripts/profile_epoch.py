@@ -5,7 +5,7 @@ from paper_1708_08640_b200 import api, synth
 p = argparse.ArgumentParser()
 p.add_argument("--scale", type=float, default=0.1)
 p.add_argument("--epochs", type=int, default=3)
-p.add_argument("--order", default="sorted")
+p.add_argument("--order", default="random")
 p.add_argument("--uniform", action="store_true")
 p.add_argument("--kernel", default="opt")
 p.add_argument("--nohot", action="store_true")
