@@ -76,7 +76,7 @@ typedef struct cmtf_gpu_config {
   float hot_tau;         /* rows whose expected concurrent updates
                             (count * workers / nnz) reach hot_tau get a
                             per-block shared-memory replica; 0 = default
-                            (2.0), < 0 disables                         */
+                            (0.5), < 0 disables                         */
   float kappa;           /* damping of batched hot-row / core steps;
                             0 = default (0.5)                           */
   int32_t flush_every;   /* sweep iterations between replica/core merges;

@@ -629,10 +629,10 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   int blocks = ctx->num_sms;
   if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (NW * 32));
   else {
-    // auto: at least ~64 entries per worker per epoch (at most 1/64 of the
-    // data in flight), so small problems stay close to sequential SGD while
-    // large ones fill every SM
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (64ull * NW * 32));
+    // auto: at least ~128 entries per worker per epoch (at most 1/128 of
+    // the data in flight), so small problems stay close to sequential SGD
+    // while large ones fill every SM
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (128ull * NW * 32));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->v2_blocks = blocks;
@@ -672,7 +672,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
 
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
-  float tau = ctx->cfg.hot_tau == 0.f ? 2.0f : ctx->cfg.hot_tau;
+  float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
   const size_t fixed = v2_fixed_bytes_rt(J, NW);
   const size_t limit = 227 * 1024 - 1024;
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
@@ -705,7 +705,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   }
   std::stable_sort(cand.begin(), cand.end(),
                    [](const Cand& x, const Cand& y) { return x.count > y.count; });
-  const size_t per_row = JP + 2;
+  const size_t per_row = JP + 3;
   const size_t slack = 4 * (ctx->order + ctx->mats.size());  // alignment padding
   size_t take = std::min(cand.size(), budget_floats > slack ? (budget_floats - slack) / per_row : 0);
   std::vector<std::vector<uint32_t>> rows_of(ctx->order), vrows_of(ctx->mats.size());
@@ -734,7 +734,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     h.off = off;  // float4-aligned (off and H*JP are multiples of 4)
     off += h.H * JP;
     h.stat_off = off;
-    off += (2 * h.H + 3) & ~3u;
+    off += (3 * h.H + 3) & ~3u;
     return CMTF_OK;
   };
   for (int n = 0; n < ctx->order; ++n) TRY(build(ctx->hot[n], rows_of[n], ctx->dims[n]));

@@ -48,7 +48,7 @@ struct HotDesc {
   const uint32_t* count;   // per row observation count (for n_hat)
   uint32_t H;              // number of hot rows
   uint32_t off;            // float offset of the replica in shared memory
-  uint32_t stat_off;       // float offset of the (lam, cnt) stats
+  uint32_t stat_off;       // float offset of the (lam, cnt, n_hat) stats
   float* base;             // [gridDim.x][H][JP] global per-block base copies
   float nhat_scale;        // n_hat = count * nhat_scale
 };
@@ -169,8 +169,8 @@ __device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* 
       }
       *reinterpret_cast<float4*>(rp + k) = cur;
     }
-    stat[2 * slot] += curv;
-    atomicAdd(reinterpret_cast<int*>(stat) + 2 * slot + 1, 1);
+    stat[3 * slot] += curv;
+    atomicAdd(reinterpret_cast<int*>(stat) + 3 * slot + 1, 1);
   } else {
     float v[JP];
 #pragma unroll
@@ -186,34 +186,44 @@ __device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* 
 }
 
 // Push the block's progress on hot rows [r0, r1) to global and re-base.
+// stat row layout: {sum |c|^2, observation count (int), n_hat}.  All loads
+// of a row are independent and issued together; the new base is the global
+// value read plus our own pushed delta (no load-after-RED round trip).
 template <int J, int JP>
 __device__ void flush_hot(const HotDesc& h, float* U, float* rep, float* stat, float eta,
                           float kappa, int r0, int r1, int lane) {
   float* base_b = h.base + (uint64_t)blockIdx.x * h.H * JP;
   for (int s = r0 + lane; s < r1; s += 32) {
-    const float cnt = (float)atomicExch(reinterpret_cast<int*>(stat) + 2 * s + 1, 0);
-    const float lam = atomicExch(stat + 2 * s, 0.f);
     const uint32_t row = __ldg(h.row_of + s);
     float* g = U + (uint64_t)row * JP;
-    float alpha = 1.f;
+    float4 gv[JP / 4], bv[JP / 4], sv[JP / 4];
+#pragma unroll
+    for (int k = 0; k < JP / 4; ++k) {
+      gv[k] = ld_strong4(g + 4 * k);
+      bv[k] = ld_weak4(base_b + s * JP + 4 * k);
+      sv[k] = *reinterpret_cast<const float4*>(rep + s * JP + 4 * k);
+    }
+    const float cnt = (float)atomicExch(reinterpret_cast<int*>(stat) + 3 * s + 1, 0);
+    const float lam = stat[3 * s];
+    stat[3 * s] = 0.f;
+    float alpha = 0.f;
     if (cnt > 0.f) {
-      const float nhat = fmaxf(cnt, (float)__ldg(h.count + row) * h.nhat_scale);
+      const float nhat = fmaxf(cnt, stat[3 * s + 2]);
       const float q = eta * (lam / cnt) * nhat;
       alpha = q > kappa ? kappa / q : 1.f;
     }
 #pragma unroll
-    for (int k = 0; k < JP; k += 4) {
-      const float4 sv = *reinterpret_cast<const float4*>(rep + s * JP + k);
-      const float4 bv = ld_weak4(base_b + s * JP + k);
-      if (cnt > 0.f)
-        red_add_v4(g + k, make_float4(alpha * (sv.x - bv.x), alpha * (sv.y - bv.y),
-                                      alpha * (sv.z - bv.z), alpha * (sv.w - bv.w)));
-      const float4 gv = ld_strong4(g + k);
-      st_weak4(base_b + s * JP + k, gv);
+    for (int k = 0; k < JP / 4; ++k) {
+      float4 dl = make_float4(alpha * (sv[k].x - bv[k].x), alpha * (sv[k].y - bv[k].y),
+                              alpha * (sv[k].z - bv[k].z), alpha * (sv[k].w - bv[k].w));
+      if (cnt > 0.f) red_add_v4(g + 4 * k, dl);
+      const float4 nb = make_float4(gv[k].x + dl.x, gv[k].y + dl.y, gv[k].z + dl.z, gv[k].w + dl.w);
+      st_weak4(base_b + s * JP + 4 * k, nb);
       // re-base, keeping local progress made since the snapshot
-      float4 cur = *reinterpret_cast<float4*>(rep + s * JP + k);
-      cur.x += gv.x - sv.x; cur.y += gv.y - sv.y; cur.z += gv.z - sv.z; cur.w += gv.w - sv.w;
-      *reinterpret_cast<float4*>(rep + s * JP + k) = cur;
+      float4 cur = *reinterpret_cast<float4*>(rep + s * JP + 4 * k);
+      cur.x += nb.x - sv[k].x; cur.y += nb.y - sv[k].y;
+      cur.z += nb.z - sv[k].z; cur.w += nb.w - sv[k].w;
+      *reinterpret_cast<float4*>(rep + s * JP + 4 * k) = cur;
     }
   }
 }
@@ -228,7 +238,11 @@ __device__ void load_hot(const HotDesc& h, const float* U, float* rep, float* st
     *reinterpret_cast<float4*>(rep + s * JP + k) = v;
     st_weak4(base_b + s * JP + k, v);
   }
-  for (uint32_t s = threadIdx.x; s < 2 * h.H; s += blockDim.x) stat[s] = 0.f;
+  for (uint32_t s = threadIdx.x; s < h.H; s += blockDim.x) {
+    stat[3 * s] = 0.f;
+    stat[3 * s + 1] = 0.f;
+    stat[3 * s + 2] = (float)__ldg(h.count + __ldg(h.row_of + s)) * h.nhat_scale;
+  }
 }
 
 template <int J, bool OPT, int NW>
@@ -294,21 +308,37 @@ hog3v2_kernel(Hog3v2Args a) {
     stat[n] = sm + a.hot[n].stat_off;
   }
 
-  uint4 nrec = make_uint4(0, 0, 0, 0);
-  if (lo < hi) nrec = __ldg(a.rec + lo);
+  // software pipeline: record of entry e+2 in flight, slots of e+1 looked
+  // up and its cold rows prefetched into L1 while entry e is computed
+  uint4 rc = make_uint4(0, 0, 0, 0), rc1 = rc;
+  if (lo < hi) rc = __ldg(a.rec + lo);
+  if (lo + 1 < hi) rc1 = __ldg(a.rec + lo + 1);
+  int sl[3] = {-1, -1, -1};
+  if (lo < hi) {
+    const uint32_t ix[3] = {rc.x, rc.y, rc.z};
+#pragma unroll
+    for (int n = 0; n < 3; ++n) sl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + ix[n]) : -1;
+  }
 
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e = lo + it;
     const bool active = e < hi;
-    const uint4 rc = nrec;
-    if (e + 1 < hi) nrec = __ldg(a.rec + e + 1);
+    uint4 rc2 = make_uint4(0, 0, 0, 0);
+    if (e + 2 < hi) rc2 = __ldg(a.rec + e + 2);
+    int nsl[3] = {-1, -1, -1};
+    if (e + 1 < hi) {
+      const uint32_t nx[3] = {rc1.x, rc1.y, rc1.z};
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + nx[n]) : -1;
+        const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + JP * 4 - 4));
+      }
+    }
     float r = 0.f;
     float u1[JP], u2[JP], u3[JP];
     if (active) {
-      int sl[3];
-      const uint32_t ix[3] = {rc.x, rc.y, rc.z};
-#pragma unroll
-      for (int n = 0; n < 3; ++n) sl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + ix[n]) : -1;
       load_row<JP>(a.U[0], rc.x, sl[0], rep[0], u1);
       load_row<JP>(a.U[1], rc.y, sl[1], rep[1], u2);
       load_row<JP>(a.U[2], rc.z, sl[2], rep[2], u3);
@@ -478,33 +508,58 @@ hog3v2_kernel(Hog3v2Args a) {
         split_tf32(x3, ah[ks][3], al[ks][3]);
       }
 #pragma unroll 1
-      for (int nt = 0; nt < L::NT; ++nt) {
-        const int ab = nt * 8 + g8;
-        const int ia = ab / J, ib = ab - (ab / J) * J;
-        const bool ok = ab < AB;
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int nt0 = 0; nt0 < L::NT; nt0 += 2) {
+        // two n-tiles per step, three independent accumulators each
+        // (hi*hi, hi*lo, lo*hi) so the HMMA chains are 4 deep, not 12
+        float d[2][3][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[j][p][q] = 0.f;
+        int iaj[2], ibj[2];
+        bool okj[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int ab = (nt0 + j) * 8 + g8;
+          okj[j] = (nt0 + j) < L::NT && ab < AB;
+          iaj[j] = ab / J;
+          ibj[j] = ab - iaj[j] * J;
+        }
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const int e0 = ks * 8 + t4, e1 = e0 + 4;
-          const float q0 = ok ? stg[e0 * L::SW + ia] * stg[e0 * L::SW + JP + ib] : 0.f;
-          const float q1 = ok ? stg[e1 * L::SW + ia] * stg[e1 * L::SW + JP + ib] : 0.f;
-          uint32_t bh[2], bl[2];
-          split_tf32(q0, bh[0], bl[0]);
-          split_tf32(q1, bh[1], bl[1]);
-          mma_tf32(d, ah[ks], bh);
-          mma_tf32(d, ah[ks], bl);
-          mma_tf32(d, al[ks], bh);
+          const float* s0 = stg + (ks * 8 + t4) * L::SW;
+          const float* s1 = s0 + 4 * L::SW;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float q0 = okj[j] ? s0[iaj[j]] * s0[JP + ibj[j]] : 0.f;
+            const float q1 = okj[j] ? s1[iaj[j]] * s1[JP + ibj[j]] : 0.f;
+            uint32_t bh[2], bl[2];
+            split_tf32(q0, bh[0], bl[0]);
+            split_tf32(q1, bh[1], bl[1]);
+            mma_tf32(d[j][0], ah[ks], bh);
+            mma_tf32(d[j][1], ah[ks], bl);
+            mma_tf32(d[j][2], al[ks], bh);
+          }
         }
-        // d: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
-        const int abo = nt * 8 + 2 * t4;
-        const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
-        if (abo < AB) {
-          if (cr0 < J) dGw[abo * JP + cr0] += d[0];
-          if (cr1 < J) dGw[abo * JP + cr1] += d[2];
-        }
-        if (abo + 1 < AB) {
-          if (cr0 < J) dGw[(abo + 1) * JP + cr0] += d[1];
-          if (cr1 < J) dGw[(abo + 1) * JP + cr1] += d[3];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (nt0 + j >= L::NT) break;
+          float dd[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dd[q] = d[j][0][q] + d[j][1][q] + d[j][2][q];
+          // dd: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
+          const int abo = (nt0 + j) * 8 + 2 * t4;
+          const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
+          if (abo < AB) {
+            if (cr0 < J) dGw[abo * JP + cr0] += dd[0];
+            if (cr1 < J) dGw[abo * JP + cr1] += dd[2];
+          }
+          if (abo + 1 < AB) {
+            if (cr0 < J) dGw[(abo + 1) * JP + cr0] += dd[1];
+            if (cr1 < J) dGw[(abo + 1) * JP + cr1] += dd[3];
+          }
         }
       }
     }
@@ -545,6 +600,11 @@ hog3v2_kernel(Hog3v2Args a) {
                         M.weight * nu);
       }
     }
+
+    rc = rc1;
+    rc1 = rc2;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) sl[n] = nsl[n];
 
     // ---- periodic flushes (staggered across warps) ----
     if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {

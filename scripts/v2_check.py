@@ -34,6 +34,8 @@ def timing(scale, settings, epochs=3, uniform=False):
                           "train_rmse": q.train_rmse, "test_rmse": api.test_rmse(st, test)}), flush=True)
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
+if mode == "grid":
+    conv([dict(hog_threads=h, hot_tau=t) for h in (384, 1152, 5376) for t in (0.05, 0.5, 2.0)])
 if mode in ("all", "conv"):
     conv([dict(hog_threads=256), dict(hog_threads=1024), dict(), dict(hot_tau=-1),
           dict(kernel_version=1, hog_threads=256)])

@@ -119,11 +119,22 @@ def test_entry_grads_at_init_and_midtraining(kernel):
             x = float(np.float32(b.tensor.values[e]))
             g_ref, c_ref, r_ref = O.compute_gradient(kernel == "opt", x, m.core, rows, 0.01, cn,
                                                      b.tensor.nnz)
-            xs = np.max(np.abs(m.core)) * np.prod([np.abs(r_).sum() for r_ in rows])
+            # scale-aware fp32 bound: r = x - x_hat cancels, so its rounding is
+            # relative to max(|x|, |x_hat|), and every gradient term -r*c_n
+            # inherits it: scale_n = max(|x|,|x_hat|) * |c_n|_max + reg*|u_n|.
+            gmax = np.max(np.abs(m.core))
+            l1 = [np.abs(r_).sum() for r_ in rows]
+            xs = gmax * np.prod(l1)
             scale_close([xh[k]], [x - r_ref], xs, 1e-5)
-            sc = abs(r_ref) * xs + 0.01 * max(np.abs(r_).max() for r_ in rows) + 1e-7
-            scale_close(grow[k], g_ref, sc, 1e-5)
-            scale_close(gcore[k], c_ref, sc, 1e-5)
+            big = max(abs(x), xs)
+            off = 0
+            for n in range(3):
+                cn_max = gmax * np.prod([l1[q] for q in range(3) if q != n])
+                sc = big * cn_max + 0.01 * np.abs(rows[n]).max() + 1e-7
+                scale_close(grow[k][off:off + 5], g_ref[off:off + 5], sc, 1e-5)
+                off += 5
+            phi_max = np.prod([np.abs(r_).max() for r_ in rows])
+            scale_close(gcore[k], c_ref, big * phi_max + 1e-7, 1e-5)
 
 
 def test_epoch_stats_and_test_rmse_match_oracle():
