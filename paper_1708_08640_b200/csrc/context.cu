@@ -75,6 +75,19 @@ struct cmtf_gpu_ctx {
   uint64_t* d_sched = nullptr;
   uint64_t d_sched_cap = 0;
 
+  // upload scratch (grow-only)
+  uint32_t* s_idx = nullptr;
+  uint64_t s_idx_cap = 0;
+  double* s_vals = nullptr;
+  uint64_t s_vals_cap = 0;
+  uint32_t* s_rec = nullptr;
+  uint64_t s_rec_cap = 0;
+  uint32_t* s_keys = nullptr;
+  uint64_t s_keys_cap = 0;
+  uint32_t* s_ids = nullptr;
+  uint64_t s_ids_cap = 0;
+  uint64_t rec_cap = 0, pos_cap = 0;
+
   // scratch
   double* d_partial = nullptr;
   uint64_t partial_cap = 0;
@@ -83,10 +96,13 @@ struct cmtf_gpu_ctx {
   // v2 sweep state (built lazily after a bundle change)
   bool v2_dirty = true;
   uint4* mrec = nullptr;  // merged matrix records {row, col, bits(y), m}, random order
-  uint64_t mnnz = 0;
+  uint64_t mnnz = 0, mrec_cap = 0;
+  uint4* s_m4 = nullptr;
+  uint64_t s_m4_cap = 0;
   struct HotHost {
     int32_t* slot = nullptr;
     uint32_t* row_of = nullptr;
+    uint64_t slot_cap = 0, row_cap = 0;
     uint32_t H = 0;
     float* base = nullptr;
     uint64_t base_cap = 0;
@@ -174,6 +190,18 @@ int dalloc(cmtf_gpu_ctx* ctx, T** p, size_t n) {
   CU(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
   return CMTF_OK;
 }
+// Grow-only device buffer (re-uploads of a same-sized bundle reuse it).
+template <typename T>
+int ensure(cmtf_gpu_ctx* ctx, T** p, uint64_t* cap, uint64_t n) {
+  if (*p && *cap >= n) return CMTF_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  CU(cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T)));
+  *cap = n;
+  return CMTF_OK;
+}
+
 template <typename T>
 void dfree(T*& p) {
   if (p) cudaFree(p);
@@ -217,6 +245,19 @@ __global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals,
   }
 }
 
+// Seeded affine bijection p -> (a*p + b) mod n with gcd(a, n) = 1: a random
+// entry order without a sort (the reference reshuffles its schedule,
+// src/trainer.cpp:122-128; a fixed pseudo-random order is used here).
+__global__ void scatter_affine_kernel(const uint32_t* src, uint64_t n, int words,
+                                      uint64_t a, uint64_t b, uint32_t* dst, uint32_t* pos) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = (uint64_t)(((unsigned __int128)a * e + b) % n);
+    for (int w = 0; w < words; ++w) dst[p * words + w] = src[e * words + w];
+    pos[e] = (uint32_t)p;
+  }
+}
+
 __global__ void gather_records_kernel(const uint32_t* src, const uint32_t* ids,
                                       uint64_t n, int words, uint32_t* dst,
                                       uint32_t* pos) {
@@ -253,6 +294,26 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
     keys[e] = shuffled ? mix32((uint32_t)e, seed) : i;
     ids[e] = (uint32_t)e;
   }
+}
+
+uint64_t gcd64(uint64_t x, uint64_t y) {
+  while (y) {
+    const uint64_t t = x % y;
+    x = y;
+    y = t;
+  }
+  return x;
+}
+
+// multiplier ~ n / golden ratio, coprime with n; offset from the seed
+void affine_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* b) {
+  uint64_t m = (uint64_t)((double)n * 0.6180339887498949) | 1ull;
+  if (m >= n) m = n > 1 ? n - 1 : 1;
+  while (m > 1 && gcd64(m, n) != 1) --m;
+  *a = m ? m : 1;
+  uint64_t s = seed * 0x9e3779b97f4a7c15ULL + 0x632be59bd9b4e019ULL;
+  s ^= s >> 29;
+  *b = n ? s % n : 0;
 }
 
 unsigned grid_for(uint64_t n, unsigned bt = 256) {
@@ -575,13 +636,10 @@ bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
 }
 
 __global__ void merge_matrix_kernel(const uint32_t* rec, uint64_t n, uint32_t m, uint64_t base,
-                                    uint32_t seed, uint4* out, uint32_t* keys, uint32_t* ids) {
+                                    uint4* out) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
-       e += (uint64_t)gridDim.x * blockDim.x) {
+       e += (uint64_t)gridDim.x * blockDim.x)
     out[base + e] = make_uint4(rec[3 * e], rec[3 * e + 1], rec[3 * e + 2], m);
-    keys[base + e] = mix32((uint32_t)(base + e), seed);
-    ids[base + e] = (uint32_t)(base + e);
-  }
 }
 
 __global__ void gather_uint4_kernel(const uint4* src, const uint32_t* ids, uint64_t n,
@@ -638,36 +696,28 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   ctx->v2_blocks = blocks;
   const double W = (double)blocks * NW * 32;
 
-  // merged matrix records (random order, seeded)
+  // merged matrix records (random order, seeded affine permutation)
   ctx->mnnz = 0;
   for (auto& M : ctx->mats) ctx->mnnz += M.nnz;
-  dfree(ctx->mrec);
   if (ctx->mnnz) {
-    uint4* tmp = nullptr;
-    uint32_t *keys = nullptr, *ids = nullptr, *sorted = nullptr;
-    TRY(dalloc(ctx, &tmp, ctx->mnnz));
-    TRY(dalloc(ctx, &keys, ctx->mnnz));
-    TRY(dalloc(ctx, &ids, ctx->mnnz));
+    TRY(ensure(ctx, &ctx->s_m4, &ctx->s_m4_cap, ctx->mnnz));
+    TRY(ensure(ctx, &ctx->mrec, &ctx->mrec_cap, ctx->mnnz));
+    TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, ctx->mnnz));
     uint64_t base = 0;
     for (size_t m = 0; m < ctx->mats.size(); ++m) {
       const auto& M = ctx->mats[m];
       if (M.nnz)
-        merge_matrix_kernel<<<grid_for(M.nnz), 256, 0, ctx->stream>>>(
-            M.rec, M.nnz, (uint32_t)m, base, (uint32_t)ctx->cfg.seed + 0x27d4eb2fu, tmp, keys,
-            ids);
+        merge_matrix_kernel<<<grid_for(M.nnz), 256, 0, ctx->stream>>>(M.rec, M.nnz,
+                                                                      (uint32_t)m, base,
+                                                                      ctx->s_m4);
       base += M.nnz;
     }
+    uint64_t pa, pb;
+    affine_params(ctx->mnnz, ctx->cfg.seed + 1, &pa, &pb);
+    scatter_affine_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const uint32_t*>(ctx->s_m4), ctx->mnnz, 4, pa, pb,
+        reinterpret_cast<uint32_t*>(ctx->mrec), ctx->s_ids);
     CU(cudaGetLastError());
-    TRY(sort_ids(ctx, keys, ids, ctx->mnnz, 0xffffffffu, &sorted));
-    TRY(dalloc(ctx, &ctx->mrec, ctx->mnnz));
-    gather_uint4_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(tmp, sorted, ctx->mnnz,
-                                                                       ctx->mrec);
-    CU(cudaGetLastError());
-    CU(cudaStreamSynchronize(ctx->stream));
-    cudaFree(tmp);
-    cudaFree(keys);
-    cudaFree(ids);
-    cudaFree(sorted);
   }
 
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
@@ -716,14 +766,12 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   uint32_t off = (uint32_t)(fixed / sizeof(float));
   auto build = [&](cmtf_gpu_ctx::HotHost& h, const std::vector<uint32_t>& rows,
                    uint32_t nrows) -> int {
-    dfree(h.slot);
-    dfree(h.row_of);
     h.H = (uint32_t)rows.size();
     if (!h.H) return CMTF_OK;
     std::vector<int32_t> slot(nrows, -1);
     for (uint32_t s = 0; s < h.H; ++s) slot[rows[s]] = (int32_t)s;
-    TRY(dalloc(ctx, &h.slot, nrows));
-    TRY(dalloc(ctx, &h.row_of, h.H));
+    TRY(ensure(ctx, &h.slot, &h.slot_cap, nrows));
+    TRY(ensure(ctx, &h.row_of, &h.row_cap, h.H));
     CU(cudaMemcpy(h.slot, slot.data(), nrows * sizeof(int32_t), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(h.row_of, rows.data(), h.H * sizeof(uint32_t), cudaMemcpyHostToDevice));
     const uint64_t need = (uint64_t)blocks * h.H * JP;
@@ -859,7 +907,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
   int blocks = ctx->num_sms * per_sm;
   if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / 32 / (bt / 32));
   else {
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (16ull * (bt / 32)));
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (1024ull * (bt / 32)));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->hog_threads_used = blocks * (bt / 32);
@@ -1031,6 +1079,11 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   dfree(ctx->rec);
   dfree(ctx->pos);
+  dfree(ctx->s_idx);
+  dfree(ctx->s_vals);
+  dfree(ctx->s_rec);
+  dfree(ctx->s_keys);
+  dfree(ctx->s_ids);
   for (int n = 0; n < kMaxOrder; ++n) {
     dfree(ctx->count[n]);
     dfree(ctx->reg[n]);
@@ -1043,8 +1096,15 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
     dfree(m.vreg);
     dfree(m.V);
   }
-  for (auto& m : ctx->spare) dfree(m.V);
+  for (auto& m : ctx->spare) {
+    dfree(m.V);
+    dfree(m.rec);
+    dfree(m.pos);
+    dfree(m.count);
+    dfree(m.vreg);
+  }
   dfree(ctx->mrec);
+  dfree(ctx->s_m4);
   for (auto& h : ctx->hot) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   for (auto& h : ctx->hotV) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   dfree(ctx->G);
@@ -1088,21 +1148,23 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   ctx->sort_mode = sm;
 
-  uint32_t* d_idx = nullptr;
-  double* d_vals = nullptr;
-  uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
-  TRY(dalloc(ctx, &d_idx, nnz * N));
-  TRY(dalloc(ctx, &d_vals, nnz));
-  TRY(dalloc(ctx, &d_rec, nnz * (N + 1)));
-  TRY(dalloc(ctx, &d_keys, nnz));
-  TRY(dalloc(ctx, &d_ids, nnz));
+  TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * N));
+  TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
+  TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * (N + 1)));
+  TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
+  TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
+  uint32_t* d_idx = ctx->s_idx;
+  double* d_vals = ctx->s_vals;
+  uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
   CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyHostToDevice,
                      ctx->stream));
   CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
                      ctx->stream));
   for (int n = 0; n < N; ++n) {
-    TRY(dalloc(ctx, &ctx->count[n], dims[n]));
-    TRY(dalloc(ctx, &ctx->reg[n], dims[n]));
+    if (!same_shape || !ctx->count[n]) {
+      TRY(dalloc(ctx, &ctx->count[n], dims[n]));
+      TRY(dalloc(ctx, &ctx->reg[n], dims[n]));
+    }
     CU(cudaMemsetAsync(ctx->count[n], 0, dims[n] * sizeof(uint32_t), ctx->stream));
   }
   CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
@@ -1115,13 +1177,9 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   unsigned long long bad[2];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_idx);
-  cudaFree(d_vals);
   if (bad[0] != ~0ull || bad[1] != ~0ull) {
-    cudaFree(d_rec);
-    cudaFree(d_keys);
-    cudaFree(d_ids);
     dfree(ctx->rec);
+    ctx->rec_cap = 0;
     if (bad[0] != ~0ull) {
       const uint64_t e = bad[0];
       for (int n = 0; n < N; ++n)
@@ -1132,22 +1190,26 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
     }
     return set_err(ctx, CMTF_EVALIDATION, "tensor value is not finite");
   }
+  TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
+  TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
   uint32_t* sorted_ids = nullptr;
-  TRY(sort_ids(ctx, d_keys, d_ids, nnz, shuffled ? 0xffffffffu : dims[sm], &sorted_ids));
-  cudaFree(d_keys);
-  cudaFree(d_ids);
-  TRY(dalloc(ctx, &ctx->rec, nnz * (N + 1)));
-  TRY(dalloc(ctx, &ctx->pos, nnz));
-  gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-      d_rec, sorted_ids, nnz, N + 1, ctx->rec, ctx->pos);
+  if (shuffled) {
+    uint64_t pa, pb;
+    affine_params(nnz, ctx->cfg.seed, &pa, &pb);
+    scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, pa, pb,
+                                                                  ctx->rec, ctx->pos);
+  } else {
+    TRY(sort_ids(ctx, d_keys, d_ids, nnz, dims[sm], &sorted_ids));
+    gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+        d_rec, sorted_ids, nnz, N + 1, ctx->rec, ctx->pos);
+  }
   CU(cudaGetLastError());
   for (int n = 0; n < N; ++n)
     reg_kernel<<<grid_for(dims[n]), 256, 0, ctx->stream>>>(
         ctx->count[n], dims[n], (float)ctx->cfg.lambda_reg, ctx->reg[n]);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_rec);
-  cudaFree(sorted_ids);
+  if (sorted_ids) cudaFree(sorted_ids);
   // model buffers (allocated with the bundle's shapes; kept on re-upload of a
   // same-shaped bundle, as run_epoch(state, bundle) keeps the state's model)
   if (!same_shape || !ctx->G) {
@@ -1161,15 +1223,16 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
 
 int cmtf_gpu_clear_matrices(cmtf_gpu_ctx* ctx) {
   if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
-  for (auto& v : ctx->spare) dfree(v.V);
-  ctx->spare.clear();
-  for (auto& m : ctx->mats) {
-    dfree(m.rec);
-    dfree(m.pos);
-    dfree(m.count);
-    dfree(m.vreg);
-    ctx->spare.push_back(m);  // coupled factor kept for a same-shaped re-add
+  for (auto& v : ctx->spare) {
+    dfree(v.V);
+    dfree(v.rec);
+    dfree(v.pos);
+    dfree(v.count);
+    dfree(v.vreg);
   }
+  ctx->spare.clear();
+  // every buffer (and the coupled factor) is kept for a same-shaped re-add
+  for (auto& m : ctx->mats) ctx->spare.push_back(m);
   ctx->mats.clear();
   return CMTF_OK;
 }
@@ -1194,34 +1257,35 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
   if (nnz >= 0xffffffffull)
     return set_err(ctx, CMTF_EUNSUPPORTED, "matrix nnz >= 2^32 per device");
   DevMatrix M;
+  const size_t slot = ctx->mats.size();
+  DevMatrix* sp = slot < ctx->spare.size() ? &ctx->spare[slot] : nullptr;
+  const bool reuse = sp && sp->V && sp->mode == mode0 && sp->cols == cols && sp->nnz >= nnz;
+  if (reuse) {
+    M = *sp;  // buffers and the coupled factor of the state
+    *sp = DevMatrix();
+  } else {
+    TRY(dalloc(ctx, &M.count, cols));
+    TRY(dalloc(ctx, &M.vreg, cols));
+    TRY(dalloc(ctx, &M.V, (uint64_t)cols * ctx->JP(mode0)));
+    TRY(dalloc(ctx, &M.rec, nnz * 3));
+    TRY(dalloc(ctx, &M.pos, nnz));
+    ctx->have_model = false;
+  }
   M.mode = mode0;
   M.rows = rows;
   M.cols = cols;
   M.nnz = nnz;
   M.weight = weight;
-  TRY(dalloc(ctx, &M.count, cols));
-  TRY(dalloc(ctx, &M.vreg, cols));
   CU(cudaMemsetAsync(M.count, 0, cols * sizeof(uint32_t), ctx->stream));
-  const size_t slot = ctx->mats.size();
-  if (slot < ctx->spare.size() && ctx->spare[slot].V && ctx->spare[slot].mode == mode0 &&
-      ctx->spare[slot].cols == cols) {
-    M.V = ctx->spare[slot].V;  // keep the coupled factor of the state
-    ctx->spare[slot].V = nullptr;
-  } else {
-    TRY(dalloc(ctx, &M.V, (uint64_t)cols * ctx->JP(mode0)));
-    ctx->have_model = false;
-  }
-  TRY(dalloc(ctx, &M.rec, nnz * 3));
-  TRY(dalloc(ctx, &M.pos, nnz));
   if (nnz > 0) {
-    uint32_t* d_idx = nullptr;
-    double* d_vals = nullptr;
-    uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
-    TRY(dalloc(ctx, &d_idx, nnz * 2));
-    TRY(dalloc(ctx, &d_vals, nnz));
-    TRY(dalloc(ctx, &d_rec, nnz * 3));
-    TRY(dalloc(ctx, &d_keys, nnz));
-    TRY(dalloc(ctx, &d_ids, nnz));
+    TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * 2));
+    TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
+    TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * 3));
+    TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
+    TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
+    uint32_t* d_idx = ctx->s_idx;
+    double* d_vals = ctx->s_vals;
+    uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
     CU(cudaMemcpyAsync(d_idx, idx, nnz * 2 * sizeof(uint32_t), cudaMemcpyHostToDevice,
                        ctx->stream));
     CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
@@ -1236,12 +1300,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     unsigned long long bad[2];
     CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_idx);
-    cudaFree(d_vals);
     if (bad[0] != ~0ull || bad[1] != ~0ull) {
-      cudaFree(d_rec);
-      cudaFree(d_keys);
-      cudaFree(d_ids);
       dfree(M.count);
       dfree(M.vreg);
       dfree(M.V);
@@ -1253,15 +1312,19 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
     }
     uint32_t* sorted_ids = nullptr;
-    TRY(sort_ids(ctx, d_keys, d_ids, nnz, shuffled ? 0xffffffffu : rows, &sorted_ids));
-    cudaFree(d_keys);
-    cudaFree(d_ids);
-    gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-        d_rec, sorted_ids, nnz, 3, M.rec, M.pos);
+    if (shuffled) {
+      uint64_t pa, pb;
+      affine_params(nnz, ctx->cfg.seed + 7 + ctx->mats.size(), &pa, &pb);
+      scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, 3, pa, pb,
+                                                                    M.rec, M.pos);
+    } else {
+      TRY(sort_ids(ctx, d_keys, d_ids, nnz, rows, &sorted_ids));
+      gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+          d_rec, sorted_ids, nnz, 3, M.rec, M.pos);
+    }
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_rec);
-    cudaFree(sorted_ids);
+    if (sorted_ids) cudaFree(sorted_ids);
   }
   reg_kernel<<<grid_for(cols), 256, 0, ctx->stream>>>(
       M.count, cols, (float)(weight * ctx->cfg.lambda_reg), M.vreg);
