@@ -137,8 +137,20 @@ def generate(spec: PlantedSpec):
         if ms.symmetric:
             if ms.cols != rows:
                 raise ValueError("symmetric matrix must be square")
-            half = distinct_coords(ms.nnz // 2, [rows, rows], [ms.row_law, ms.col_law], rng)
-            half = half[half[:, 0] != half[:, 1]]
+            # unordered pairs i < j, distinct, then mirrored: no duplicates
+            half = np.zeros((0, 2), dtype=np.int64)
+            need = ms.nnz // 2
+            for _ in range(50):
+                if half.shape[0] >= need:
+                    break
+                c = distinct_coords(2 * (need - half.shape[0]) + 64, [rows, rows],
+                                    [ms.row_law, ms.col_law], rng)
+                c = c[c[:, 0] != c[:, 1]]
+                c = np.sort(c, axis=1)
+                allc = np.concatenate([half, c])
+                _, first = np.unique(allc[:, 0] * rows + allc[:, 1], return_index=True)
+                half = allc[np.sort(first)]
+            half = half[:need]
             w = factors[ms.mode]
             y = np.einsum("nj,nj->n", factors[ms.mode][half[:, 0]], w[half[:, 1]])
             if ms.noise:
