@@ -308,3 +308,22 @@ def test_empty_matrix_is_allowed():
     st = api.make_state(TrainConfig(ranks=[2, 2, 2], seed=17, eta0=0.01), b)
     api.run_epoch(st)
     assert np.isfinite(api.epoch_stats(st, 0.1).objective)
+
+
+def test_config2_rmse_within_1pct_of_reference():
+    """BASELINE configs[1] shape (Zipf 1.2 modes, clipped planted values,
+    symmetric + 200-column coupled matrices) at 10% scale: 10 Hogwild epochs on
+    the GPU vs the reference's own run (tests/golden/config2_s01_reference.json,
+    produced by scripts/oracle_config2.py with oracle/_ref, 6 threads)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "config2_s01_reference.json")))
+    b, test, _ = synth.generate(synth.config2(0.1))
+    st = api.make_state(TrainConfig(ranks=[10, 10, 10], eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
+    for _ in range(10):
+        api.run_epoch(st)
+    tr = api.epoch_stats(st, 0.01).train_rmse
+    te = api.test_rmse(st, test)
+    assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
+    assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
