@@ -111,7 +111,8 @@ struct cmtf_gpu_ctx {
   HotHost hot[kMaxOrder];
   HotHost hotV[kMaxMats];
   int v2_blocks = 0;
-  int v2_nw = 12;
+  int v2_nw = 8;
+  int v2_e = 2;
   size_t v2_smem = 0;
 
   // timing
@@ -649,52 +650,56 @@ __global__ void gather_uint4_kernel(const uint4* src, const uint32_t* ids, uint6
     dst[s] = src[ids[s]];
 }
 
-template <int J, int NW>
+template <int J, int NW, int E>
 size_t v2_fixed_bytes() {
-  return sizeof(float) * (size_t)V2Layout<J, true, NW>::FIXED_FLOATS;
+  return sizeof(float) * (size_t)V2Layout<J, true, NW, E>::FIXED_FLOATS;
 }
 
-size_t v2_fixed_bytes_rt(int J, int NW) {
-  if (NW == 12) {
-    switch (J) {
-      case 4: return v2_fixed_bytes<4, 12>();
-      case 5: return v2_fixed_bytes<5, 12>();
-      case 8: return v2_fixed_bytes<8, 12>();
-      default: return v2_fixed_bytes<10, 12>();
-    }
-  }
-  switch (J) {
-    case 4: return v2_fixed_bytes<4, 8>();
-    case 5: return v2_fixed_bytes<5, 8>();
-    case 8: return v2_fixed_bytes<8, 8>();
-    default: return v2_fixed_bytes<10, 8>();
-  }
-}
+// (warps per block, entries per lane) of the v2 sweep
+struct V2Shape {
+  int nw, e;
+};
 
-int v2_warps(const cmtf_gpu_ctx* ctx) {
-  const char* e = std::getenv("CMTF_V2_WARPS");
-  if (e) return std::atoi(e) == 8 ? 8 : 12;
+V2Shape v2_shape(const cmtf_gpu_ctx* ctx) {
   (void)ctx;
-  return 12;
+  V2Shape s{8, 2};
+  if (const char* v = std::getenv("CMTF_V2_SHAPE")) {  // "12x1" or "8x2" (experiments)
+    if (std::string(v) == "12x1") s = {12, 1};
+    if (std::string(v) == "8x2") s = {8, 2};
+  }
+  return s;
+}
+
+size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
+#define FB(JV)                                                                  \
+  case JV:                                                                      \
+    return sh.nw == 12 ? v2_fixed_bytes<JV, 12, 1>() : v2_fixed_bytes<JV, 8, 2>();
+  switch (J) {
+    FB(4) FB(5) FB(8) FB(10)
+  }
+#undef FB
+  return 0;
 }
 
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const uint32_t JP = (uint32_t)round_up4(J);
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
-  const int NW = v2_warps(ctx);
+  const V2Shape sh = v2_shape(ctx);
+  const int NW = sh.nw;
   ctx->v2_nw = NW;
+  ctx->v2_e = sh.e;
   int blocks = ctx->num_sms;
   if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (NW * 32));
   else {
-    // auto: at least ~128 entries per worker per epoch (at most 1/128 of
-    // the data in flight), so small problems stay close to sequential SGD
-    // while large ones fill every SM
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (128ull * NW * 32));
+    // auto: at least ~112 entries per worker slot per epoch (at most ~1/112
+    // of the data in flight), so small problems stay close to sequential
+    // SGD while large ones fill every SM
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (112ull * NW * 32 * sh.e));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->v2_blocks = blocks;
-  const double W = (double)blocks * NW * 32;
+  const double W = (double)blocks * NW * 32 * sh.e;  // entries in flight
 
   // merged matrix records (random order, seeded affine permutation)
   ctx->mnnz = 0;
@@ -723,7 +728,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
-  const size_t fixed = v2_fixed_bytes_rt(J, NW);
+  const size_t fixed = v2_fixed_bytes_rt(J, sh);
   const size_t limit = 227 * 1024 - 1024;
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   struct Cand {
@@ -793,9 +798,9 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   return CMTF_OK;
 }
 
-template <int J, bool OPT, int NW>
+template <int J, bool OPT, int NW, int E>
 int launch_v2_nw(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  auto kern = hog3v2_kernel<J, OPT, NW>;
+  auto kern = hog3v2_kernel<J, OPT, NW, E>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)ctx->v2_smem));
   kern<<<ctx->v2_blocks, NW * 32, ctx->v2_smem, ctx->stream>>>(args);
@@ -805,8 +810,8 @@ int launch_v2_nw(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
 
 template <int J, bool OPT>
 int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  return ctx->v2_nw == 12 ? launch_v2_nw<J, OPT, 12>(ctx, args)
-                          : launch_v2_nw<J, OPT, 8>(ctx, args);
+  return ctx->v2_nw == 12 ? launch_v2_nw<J, OPT, 12, 1>(ctx, args)
+                          : launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
 int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
@@ -819,7 +824,9 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
   a.n_mat = (int)ctx->mats.size();
   const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 8;
   const double W = (double)ctx->v2_blocks * ctx->v2_nw * 32;
-  const float nhat_scale = (float)(W * F / (double)ctx->nnz);
+  // entries processed GPU-wide between two flushes of one warp: W * F * E
+  const double win = W * F * ctx->v2_e;
+  const float nhat_scale = (float)(win / (double)ctx->nnz);
   auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count) {
     HotDesc d{};
     d.slot = h.H ? h.slot : nullptr;
@@ -849,7 +856,7 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
   a.eta = eta;
   a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
   a.kappa = ctx->cfg.kappa > 0.f ? ctx->cfg.kappa : 0.5f;
-  a.nhat_core = (float)(W * F);
+  a.nhat_core = (float)win;
   a.flush_every = F;
   a.nonneg = ctx->cfg.nonnegative;
   ctx->kernel_which = 3;

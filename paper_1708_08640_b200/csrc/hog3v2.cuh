@@ -245,7 +245,7 @@ __device__ void load_hot(const HotDesc& h, const float* U, float* rep, float* st
   }
 }
 
-template <int J, bool OPT, int NW>
+template <int J, bool OPT, int NW, int E>
 struct V2Layout {
   static constexpr int JP = round_up4(J);
   static constexpr int AB = J * J;            // core rows (a,b)
@@ -259,21 +259,155 @@ struct V2Layout {
   static constexpr int MT = (J + 15) / 16;    // c tiles of 16 (mma M)
   static constexpr int G_FLOATS = AB * JP;    // shared core [ab][JP]
   static constexpr int DG_FLOATS = AB * JP;   // per-warp core-grad accum
-  static constexpr int STAGE_FLOATS = 32 * SW;
+  static constexpr int STAGE_FLOATS = 32 * E * SW;
   static constexpr int FIXED_FLOATS = G_FLOATS + NW * (DG_FLOATS + STAGE_FLOATS);
 };
 
-template <int J, bool OPT, int NW>
+// Tensor-core core gradient of 32 staged entries (rows stg[0..32) of width
+// SW holding (-r u1, u2, u3)): dGw[ab][c] += sum_e u3_e[c] (-r u1)_e[a] u2_e[b].
+template <int J, int JP, int SW, int AB, int NT, int MT>
+__device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int g8, int t4) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    uint32_t ah[4][4], al[4][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int e0 = ks * 8 + t4, e1 = e0 + 4;
+      const int c0 = mt * 16 + g8, c1 = c0 + 8;
+      const float x0 = c0 < J ? stg[e0 * SW + 2 * JP + c0] : 0.f;
+      const float x1 = c1 < J ? stg[e0 * SW + 2 * JP + c1] : 0.f;
+      const float x2 = c0 < J ? stg[e1 * SW + 2 * JP + c0] : 0.f;
+      const float x3 = c1 < J ? stg[e1 * SW + 2 * JP + c1] : 0.f;
+      split_tf32(x0, ah[ks][0], al[ks][0]);
+      split_tf32(x1, ah[ks][1], al[ks][1]);
+      split_tf32(x2, ah[ks][2], al[ks][2]);
+      split_tf32(x3, ah[ks][3], al[ks][3]);
+    }
+#pragma unroll 1
+    for (int nt0 = 0; nt0 < NT; nt0 += 2) {
+      // two n-tiles per step, three independent accumulators each
+      // (hi*hi, hi*lo, lo*hi) so the HMMA chains are 4 deep, not 12
+      float d[2][3][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) d[j][p][q] = 0.f;
+      int iaj[2], ibj[2];
+      bool okj[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int ab = (nt0 + j) * 8 + g8;
+        okj[j] = (nt0 + j) < NT && ab < AB;
+        iaj[j] = ab / J;
+        ibj[j] = ab - iaj[j] * J;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const float* s0 = stg + (ks * 8 + t4) * SW;
+        const float* s1 = s0 + 4 * SW;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float q0 = okj[j] ? s0[iaj[j]] * s0[JP + ibj[j]] : 0.f;
+          const float q1 = okj[j] ? s1[iaj[j]] * s1[JP + ibj[j]] : 0.f;
+          uint32_t bh[2], bl[2];
+          split_tf32(q0, bh[0], bl[0]);
+          split_tf32(q1, bh[1], bl[1]);
+          mma_tf32(d[j][0], ah[ks], bh);
+          mma_tf32(d[j][1], ah[ks], bl);
+          mma_tf32(d[j][2], al[ks], bh);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (nt0 + j >= NT) break;
+        float dd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dd[q] = d[j][0][q] + d[j][1][q] + d[j][2][q];
+        // dd: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
+        const int abo = (nt0 + j) * 8 + 2 * t4;
+        const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
+        if (abo < AB) {
+          if (cr0 < J) dGw[abo * JP + cr0] += dd[0];
+          if (cr1 < J) dGw[abo * JP + cr1] += dd[2];
+        }
+        if (abo + 1 < AB) {
+          if (cr0 < J) dGw[(abo + 1) * JP + cr0] += dd[1];
+          if (cr1 < J) dGw[(abo + 1) * JP + cr1] += dd[3];
+        }
+      }
+    }
+  }
+}
+
+// One coupled-matrix entry (src/gradients.cpp:225-248; trainer.cpp:220-235).
+template <int J, int JP>
+__device__ __forceinline__ void matrix_entry(const Hog3v2Args& a, float* sm, const uint4 mr) {
+  const MatDesc3& M = a.mats[mr.w];
+  const int mode = M.mode;
+  const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
+  const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
+  float uu[JP], vv[JP];
+  float* repU = sm + a.hot[mode].off;
+  float* repV = sm + M.hotV.off;
+  load_row<JP>(a.U[mode], mr.x, su, repU, uu);
+  load_row<JP>(M.V, mr.y, sv, repV, vv);
+  float yh = 0.f, nu = 0.f, nv = 0.f;
+#pragma unroll
+  for (int k = 0; k < J; ++k) {
+    yh = fmaf(uu[k], vv[k], yh);
+    nu = fmaf(uu[k], uu[k], nu);
+    nv = fmaf(vv[k], vv[k], nv);
+  }
+  const float rr = __uint_as_float(mr.z) - yh;
+  const float vr = __ldg(M.vreg + mr.y);
+  float du[J], dv[J];
+#pragma unroll
+  for (int k = 0; k < J; ++k) {
+    du[k] = -M.weight * rr * vv[k];
+    dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
+  }
+  step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
+                  a.nonneg, M.weight * nv);
+  step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
+                  M.weight * nu);
+}
+
+template <int J, int JP, int NW>
+__device__ __forceinline__ void flush_all_hot(const Hog3v2Args& a, float* sm, int w, int lane) {
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const HotDesc& h = a.hot[n];
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1, lane);
+    }
+  }
+  for (int m = 0; m < a.n_mat; ++m) {
+    const HotDesc& h = a.mats[m].hotV;
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
+                       lane);
+    }
+  }
+}
+
+// E = entries per lane per iteration: every broadcast LDS of a core row feeds
+// 2E FMAs and each lane carries E independent FMA chains.
+template <int J, bool OPT, int NW, int E>
 __global__ void __launch_bounds__(NW * 32, 1)
 hog3v2_kernel(Hog3v2Args a) {
-  using L = V2Layout<J, OPT, NW>;
+  using L = V2Layout<J, OPT, NW, E>;
   constexpr int JP = L::JP;
   constexpr int AB = L::AB;
+  constexpr int SW = L::SW;
   extern __shared__ __align__(16) float sm[];
   float* Gs = sm;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* dGw = sm + L::G_FLOATS + w * (L::DG_FLOATS + L::STAGE_FLOATS);
-  float* stg = dGw + L::DG_FLOATS;
+  float* stg = dGw + L::DG_FLOATS;  // [E*32][SW]; entry j of this lane -> row j*32+lane
   const int g8 = lane >> 2, t4 = lane & 3;
 
   // ---- prologue: core copy, hot replicas ----
@@ -294,7 +428,8 @@ hog3v2_kernel(Hog3v2Args a) {
   const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
   const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
   const uint64_t lo = a.nnz * gl / Wt, hi = a.nnz * (gl + 1) / Wt;
-  const uint64_t iters = (a.nnz + Wt - 1) / Wt;
+  const uint64_t maxchunk = (a.nnz + Wt - 1) / Wt;
+  const uint64_t iters = (maxchunk + E - 1) / E;
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
   float kw = 0.f;      // entries since the warp's last core flush (lane-local)
@@ -308,303 +443,250 @@ hog3v2_kernel(Hog3v2Args a) {
     stat[n] = sm + a.hot[n].stat_off;
   }
 
-  // software pipeline: record of entry e+2 in flight, slots of e+1 looked
-  // up and its cold rows prefetched into L1 while entry e is computed
-  uint4 rc = make_uint4(0, 0, 0, 0), rc1 = rc;
-  if (lo < hi) rc = __ldg(a.rec + lo);
-  if (lo + 1 < hi) rc1 = __ldg(a.rec + lo + 1);
-  int sl[3] = {-1, -1, -1};
-  if (lo < hi) {
-    const uint32_t ix[3] = {rc.x, rc.y, rc.z};
+  // software pipeline: records of the next E entries in flight, their slots
+  // looked up and cold rows prefetched into L1 while this group is computed
+  uint4 rc[E], rc1[E];
+  int sl[E][3];
 #pragma unroll
-    for (int n = 0; n < 3; ++n) sl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + ix[n]) : -1;
+  for (int j = 0; j < E; ++j) {
+    const uint64_t e = lo + j, e1 = lo + E + j;
+    rc[j] = e < hi ? __ldg(a.rec + e) : make_uint4(0, 0, 0, 0);
+    rc1[j] = e1 < hi ? __ldg(a.rec + e1) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const uint32_t ix[3] = {rc[j].x, rc[j].y, rc[j].z};
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+      sl[j][n] = (lo + j < hi && a.hot[n].slot) ? __ldg(a.hot[n].slot + ix[n]) : -1;
   }
 
   for (uint64_t it = 0; it < iters; ++it) {
-    const uint64_t e = lo + it;
-    const bool active = e < hi;
-    uint4 rc2 = make_uint4(0, 0, 0, 0);
-    if (e + 2 < hi) rc2 = __ldg(a.rec + e + 2);
-    int nsl[3] = {-1, -1, -1};
-    if (e + 1 < hi) {
-      const uint32_t nx[3] = {rc1.x, rc1.y, rc1.z};
+    const uint64_t e0 = lo + it * E;
+    bool active[E];
+    uint4 rc2[E];
+    int nsl[E][3];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      active[j] = e0 + j < hi;
+      const uint64_t e2 = e0 + 2 * E + j;
+      rc2[j] = e2 < hi ? __ldg(a.rec + e2) : make_uint4(0, 0, 0, 0);
+      const bool nxt = e0 + E + j < hi;
+      const uint32_t nx[3] = {rc1[j].x, rc1[j].y, rc1[j].z};
 #pragma unroll
       for (int n = 0; n < 3; ++n) {
-        nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + nx[n]) : -1;
-        const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + JP * 4 - 4));
+        nsl[j][n] = (nxt && a.hot[n].slot) ? __ldg(a.hot[n].slot + nx[n]) : -1;
+        if (nxt) {
+          const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + JP * 4 - 4));
+        }
       }
     }
-    float r = 0.f;
-    float u1[JP], u2[JP], u3[JP];
-    if (active) {
-      load_row<JP>(a.U[0], rc.x, sl[0], rep[0], u1);
-      load_row<JP>(a.U[1], rc.y, sl[1], rep[1], u2);
-      load_row<JP>(a.U[2], rc.z, sl[2], rep[2], u3);
-      const float reg1 = __ldg(a.reg[0] + rc.x), reg2 = __ldg(a.reg[1] + rc.y),
-                  reg3 = __ldg(a.reg[2] + rc.z);
-      float w1[J], g2[J], g3[J];
+
+    // ---- gather rows; u1 goes to the lane's staging row (rolled a-loop) ----
+    float u2[E][JP], u3[E][JP], g2[E][J], g3[E][J], xh[E], reg1[E], reg2[E], reg3[E];
 #pragma unroll
-      for (int k = 0; k < J; ++k) { w1[k] = 0.f; g2[k] = 0.f; g3[k] = 0.f; }
-      float xh = 0.f;
-      // u1 and W1 live in this lane's staging row during the sweep so the
-      // a-loop can stay rolled (small code, no register selects)
-      float* myst = stg + lane * L::SW;
+    for (int j = 0; j < E; ++j) {
+      float u1[JP];
+      if (active[j]) {
+        load_row<JP>(a.U[0], rc[j].x, sl[j][0], rep[0], u1);
+        load_row<JP>(a.U[1], rc[j].y, sl[j][1], rep[1], u2[j]);
+        load_row<JP>(a.U[2], rc[j].z, sl[j][2], rep[2], u3[j]);
+        reg1[j] = __ldg(a.reg[0] + rc[j].x);
+        reg2[j] = __ldg(a.reg[1] + rc[j].y);
+        reg3[j] = __ldg(a.reg[2] + rc[j].z);
+      } else {
+#pragma unroll
+        for (int k = 0; k < JP; ++k) { u1[k] = 0.f; u2[j][k] = 0.f; u3[j][k] = 0.f; }
+        reg1[j] = reg2[j] = reg3[j] = 0.f;
+      }
+      float* myst = stg + (j * 32 + lane) * SW;
 #pragma unroll
       for (int k = 0; k < JP; k += 4)
         *reinterpret_cast<float4*>(myst + k) = make_float4(u1[k], u1[k + 1], u1[k + 2], u1[k + 3]);
-      if (OPT) {
+#pragma unroll
+      for (int k = 0; k < J; ++k) { g2[j][k] = 0.f; g3[j][k] = 0.f; }
+      xh[j] = 0.f;
+    }
+
+    // ---- contractions (FP32 CUDA cores, core rows broadcast from smem) ----
+    if (OPT) {
 #pragma unroll 1
-        for (int ia = 0; ia < J; ++ia) {
-          const float ua = myst[ia];
-          const float* grow = Gs + ia * J * JP;
-          float wsum = 0.f;
+      for (int ia = 0; ia < J; ++ia) {
+        const float* grow = Gs + ia * J * JP;
+        float ua[E], wsum[E];
 #pragma unroll
-          for (int ib = 0; ib < J; ++ib) {
-            float gv[JP];
+        for (int j = 0; j < E; ++j) {
+          ua[j] = stg[(j * 32 + lane) * SW + ia];
+          wsum[j] = 0.f;
+        }
 #pragma unroll
-            for (int c = 0; c < JP; c += 4) {
-              const float4 q = *reinterpret_cast<const float4*>(grow + ib * JP + c);
-              gv[c] = q.x; gv[c + 1] = q.y; gv[c + 2] = q.z; gv[c + 3] = q.w;
-            }
+        for (int ib = 0; ib < J; ++ib) {
+          float gv[JP];
+#pragma unroll
+          for (int c = 0; c < JP; c += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(grow + ib * JP + c);
+            gv[c] = q.x; gv[c + 1] = q.y; gv[c + 2] = q.z; gv[c + 3] = q.w;
+          }
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
             float t0 = 0.f, t1 = 0.f;
 #pragma unroll
             for (int c = 0; c < J; ++c) {
-              if (c & 1) t1 = fmaf(gv[c], u3[c], t1);
-              else t0 = fmaf(gv[c], u3[c], t0);
+              if (c & 1) t1 = fmaf(gv[c], u3[j][c], t1);
+              else t0 = fmaf(gv[c], u3[j][c], t0);
             }
-            const float p = ua * u2[ib];
+            const float p = ua[j] * u2[j][ib];
 #pragma unroll
-            for (int c = 0; c < J; ++c) g3[c] = fmaf(gv[c], p, g3[c]);
+            for (int c = 0; c < J; ++c) g3[j][c] = fmaf(gv[c], p, g3[j][c]);
             const float tab = t0 + t1;
-            wsum = fmaf(tab, u2[ib], wsum);
-            g2[ib] = fmaf(tab, ua, g2[ib]);
+            wsum[j] = fmaf(tab, u2[j][ib], wsum[j]);
+            g2[j][ib] = fmaf(tab, ua[j], g2[j][ib]);
           }
-          myst[JP + ia] = wsum;
-          xh = fmaf(wsum, ua, xh);
         }
 #pragma unroll
-        for (int k = 0; k < J; ++k) w1[k] = myst[JP + k];
-      } else {
-        // Algorithm 2: separate walks (predict, then each contract_all_but)
+        for (int j = 0; j < E; ++j) {
+          stg[(j * 32 + lane) * SW + JP + ia] = wsum[j];
+          xh[j] = fmaf(wsum[j], ua[j], xh[j]);
+        }
+      }
+    } else {
+      // Algorithm 2: separate walks (predict, then each contract_all_but)
 #pragma unroll 1
-        for (int ia = 0; ia < J; ++ia) {
-          float ua = 0.f;
+      for (int ia = 0; ia < J; ++ia) {
+        const float* grow = Gs + ia * J * JP;
 #pragma unroll
-          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
-          const float* grow = Gs + ia * J * JP;
+        for (int j = 0; j < E; ++j) {
+          const float ua = stg[(j * 32 + lane) * SW + ia];
 #pragma unroll
           for (int ib = 0; ib < J; ++ib) {
             float tab = 0.f;
 #pragma unroll
-            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
-            xh = fmaf(tab * u2[ib], ua, xh);
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[j][c], tab);
+            xh[j] = fmaf(tab * u2[j][ib], ua, xh[j]);
           }
         }
-        asm volatile("" ::: "memory");
+      }
+      asm volatile("" ::: "memory");
 #pragma unroll 1
-        for (int ia = 0; ia < J; ++ia) {
-          const float* grow = Gs + ia * J * JP;
+      for (int ia = 0; ia < J; ++ia) {
+        const float* grow = Gs + ia * J * JP;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
           float wsum = 0.f;
 #pragma unroll
           for (int ib = 0; ib < J; ++ib) {
             float tab = 0.f;
 #pragma unroll
-            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
-            wsum = fmaf(tab, u2[ib], wsum);
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[j][c], tab);
+            wsum = fmaf(tab, u2[j][ib], wsum);
           }
-#pragma unroll
-          for (int k = 0; k < J; ++k) w1[k] = (k == ia) ? wsum : w1[k];
+          stg[(j * 32 + lane) * SW + JP + ia] = wsum;
         }
-        asm volatile("" ::: "memory");
+      }
+      asm volatile("" ::: "memory");
 #pragma unroll 1
-        for (int ia = 0; ia < J; ++ia) {
-          float ua = 0.f;
+      for (int ia = 0; ia < J; ++ia) {
+        const float* grow = Gs + ia * J * JP;
 #pragma unroll
-          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
-          const float* grow = Gs + ia * J * JP;
+        for (int j = 0; j < E; ++j) {
+          const float ua = stg[(j * 32 + lane) * SW + ia];
 #pragma unroll
           for (int ib = 0; ib < J; ++ib) {
             float tab = 0.f;
 #pragma unroll
-            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[c], tab);
-            g2[ib] = fmaf(tab, ua, g2[ib]);
+            for (int c = 0; c < J; ++c) tab = fmaf(grow[ib * JP + c], u3[j][c], tab);
+            g2[j][ib] = fmaf(tab, ua, g2[j][ib]);
           }
         }
-        asm volatile("" ::: "memory");
+      }
+      asm volatile("" ::: "memory");
 #pragma unroll 1
-        for (int ia = 0; ia < J; ++ia) {
-          float ua = 0.f;
+      for (int ia = 0; ia < J; ++ia) {
+        const float* grow = Gs + ia * J * JP;
 #pragma unroll
-          for (int k = 0; k < J; ++k) ua = (k == ia) ? u1[k] : ua;
-          const float* grow = Gs + ia * J * JP;
+        for (int j = 0; j < E; ++j) {
+          const float ua = stg[(j * 32 + lane) * SW + ia];
 #pragma unroll
           for (int ib = 0; ib < J; ++ib) {
-            const float p = ua * u2[ib];
+            const float p = ua * u2[j][ib];
 #pragma unroll
-            for (int c = 0; c < J; ++c) g3[c] = fmaf(grow[ib * JP + c], p, g3[c]);
+            for (int c = 0; c < J; ++c) g3[j][c] = fmaf(grow[ib * JP + c], p, g3[j][c]);
           }
         }
       }
-      r = __uint_as_float(rc.w) - xh;
-      // core-gradient curvature |phi|^2 = prod_n |u_n|^2
-      float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+    }
+
+    // ---- residuals, row steps, staging for the core gradient ----
 #pragma unroll
-      for (int k = 0; k < J; ++k) {
-        n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[k], u2[k], n2); n3 = fmaf(u3[k], u3[k], n3);
-        c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[k], g2[k], c2); c3 = fmaf(g3[k], g3[k], c3);
+    for (int j = 0; j < E; ++j) {
+      float* myst = stg + (j * 32 + lane) * SW;
+      float u1[JP], w1[J];
+#pragma unroll
+      for (int k = 0; k < JP; ++k) u1[k] = myst[k];
+#pragma unroll
+      for (int k = 0; k < J; ++k) w1[k] = myst[JP + k];
+      const float r = active[j] ? __uint_as_float(rc[j].w) - xh[j] : 0.f;
+      if (active[j]) {
+        float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+        for (int k = 0; k < J; ++k) {
+          n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[j][k], u2[j][k], n2);
+          n3 = fmaf(u3[j][k], u3[j][k], n3);
+          c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[j][k], g2[j][k], c2);
+          c3 = fmaf(g3[j][k], g3[j][k], c3);
+        }
+        lamG += n1 * n2 * n3;
+        kw += 1.f;
+        float gr[J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1[j] * u1[k]);
+        step_row<J, JP>(a.U[0], rc[j].x, sl[j][0], const_cast<float*>(rep[0]), stat[0], u1, gr,
+                        a.eta, a.nonneg, c1);
+#pragma unroll
+        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[j][k], reg2[j] * u2[j][k]);
+        step_row<J, JP>(a.U[1], rc[j].y, sl[j][1], const_cast<float*>(rep[1]), stat[1], u2[j],
+                        gr, a.eta, a.nonneg, c2);
+#pragma unroll
+        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[j][k], reg3[j] * u3[j][k]);
+        step_row<J, JP>(a.U[2], rc[j].z, sl[j][2], const_cast<float*>(rep[2]), stat[2], u3[j],
+                        gr, a.eta, a.nonneg, c3);
       }
-      lamG += n1 * n2 * n3;
-      kw += 1.f;
-      // stage (-r u1, u2, u3) at pre-update values
-      float* st = stg + lane * L::SW;
+      // stage (-r u1, u2, u3) at pre-update values (zeros for idle lanes)
 #pragma unroll
       for (int k = 0; k < JP; k += 4) {
-        *reinterpret_cast<float4*>(st + k) =
+        *reinterpret_cast<float4*>(myst + k) =
             make_float4(-r * u1[k], -r * u1[k + 1], -r * u1[k + 2], -r * u1[k + 3]);
-        *reinterpret_cast<float4*>(st + JP + k) = make_float4(u2[k], u2[k + 1], u2[k + 2], u2[k + 3]);
-        *reinterpret_cast<float4*>(st + 2 * JP + k) =
-            make_float4(u3[k], u3[k + 1], u3[k + 2], u3[k + 3]);
+        *reinterpret_cast<float4*>(myst + JP + k) =
+            make_float4(u2[j][k], u2[j][k + 1], u2[j][k + 2], u2[j][k + 3]);
+        *reinterpret_cast<float4*>(myst + 2 * JP + k) =
+            make_float4(u3[j][k], u3[j][k + 1], u3[j][k + 2], u3[j][k + 3]);
       }
-      // row steps: grad = -r c + reg u
-      float gr[J];
-#pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1 * u1[k]);
-      step_row<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0], u1, gr, a.eta,
-                      a.nonneg, c1);
-#pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], reg2 * u2[k]);
-      step_row<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1], u2, gr, a.eta,
-                      a.nonneg, c2);
-#pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], reg3 * u3[k]);
-      step_row<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2], u3, gr, a.eta,
-                      a.nonneg, c3);
-    } else {
-      float* st = stg + lane * L::SW;
-#pragma unroll
-      for (int k = 0; k < L::SW; k += 4)
-        *reinterpret_cast<float4*>(st + k) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncwarp();
 
-    // ---- core gradient of the warp's 32 entries on the tensor cores ----
-    // D[c][ab] += sum_e U3^T[c][e] * Q[e][ab]   (M = c, N = ab, K = e)
+    // ---- core gradient of the warp's 32*E entries on the tensor cores ----
 #pragma unroll
-    for (int mt = 0; mt < L::MT; ++mt) {
-      uint32_t ah[4][4], al[4][4];
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int e0 = ks * 8 + t4, e1 = e0 + 4;
-        const int c0 = mt * 16 + g8, c1 = c0 + 8;
-        const float x0 = c0 < J ? stg[e0 * L::SW + 2 * JP + c0] : 0.f;
-        const float x1 = c1 < J ? stg[e0 * L::SW + 2 * JP + c1] : 0.f;
-        const float x2 = c0 < J ? stg[e1 * L::SW + 2 * JP + c0] : 0.f;
-        const float x3 = c1 < J ? stg[e1 * L::SW + 2 * JP + c1] : 0.f;
-        split_tf32(x0, ah[ks][0], al[ks][0]);
-        split_tf32(x1, ah[ks][1], al[ks][1]);
-        split_tf32(x2, ah[ks][2], al[ks][2]);
-        split_tf32(x3, ah[ks][3], al[ks][3]);
-      }
-#pragma unroll 1
-      for (int nt0 = 0; nt0 < L::NT; nt0 += 2) {
-        // two n-tiles per step, three independent accumulators each
-        // (hi*hi, hi*lo, lo*hi) so the HMMA chains are 4 deep, not 12
-        float d[2][3][4];
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[j][p][q] = 0.f;
-        int iaj[2], ibj[2];
-        bool okj[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int ab = (nt0 + j) * 8 + g8;
-          okj[j] = (nt0 + j) < L::NT && ab < AB;
-          iaj[j] = ab / J;
-          ibj[j] = ab - iaj[j] * J;
-        }
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const float* s0 = stg + (ks * 8 + t4) * L::SW;
-          const float* s1 = s0 + 4 * L::SW;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const float q0 = okj[j] ? s0[iaj[j]] * s0[JP + ibj[j]] : 0.f;
-            const float q1 = okj[j] ? s1[iaj[j]] * s1[JP + ibj[j]] : 0.f;
-            uint32_t bh[2], bl[2];
-            split_tf32(q0, bh[0], bl[0]);
-            split_tf32(q1, bh[1], bl[1]);
-            mma_tf32(d[j][0], ah[ks], bh);
-            mma_tf32(d[j][1], ah[ks], bl);
-            mma_tf32(d[j][2], al[ks], bh);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (nt0 + j >= L::NT) break;
-          float dd[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dd[q] = d[j][0][q] + d[j][1][q] + d[j][2][q];
-          // dd: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
-          const int abo = (nt0 + j) * 8 + 2 * t4;
-          const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
-          if (abo < AB) {
-            if (cr0 < J) dGw[abo * JP + cr0] += dd[0];
-            if (cr1 < J) dGw[abo * JP + cr1] += dd[2];
-          }
-          if (abo + 1 < AB) {
-            if (cr0 < J) dGw[(abo + 1) * JP + cr0] += dd[1];
-            if (cr1 < J) dGw[(abo + 1) * JP + cr1] += dd[3];
-          }
-        }
-      }
-    }
+    for (int j = 0; j < E; ++j)
+      core_grad_mma<J, JP, SW, AB, L::NT, L::MT>(stg + j * 32 * SW, dGw, g8, t4);
 
     // ---- matrix entries due by this iteration (interleaved) ----
     {
       const uint64_t due = mlo + (mhi - mlo) * (it + 1) / iters;
       while (mpos < due) {
-        const uint4 mr = __ldg(a.mrec + mpos);
+        matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mpos));
         ++mpos;
-        const MatDesc3& M = a.mats[mr.w];
-        const int mode = M.mode;
-        const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
-        const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
-        float uu[JP], vv[JP];
-        float* repU = sm + a.hot[mode].off;
-        float* repV = sm + M.hotV.off;
-        load_row<JP>(a.U[mode], mr.x, su, repU, uu);
-        load_row<JP>(M.V, mr.y, sv, repV, vv);
-        float yh = 0.f, nu = 0.f, nv = 0.f;
-#pragma unroll
-        for (int k = 0; k < J; ++k) {
-          yh = fmaf(uu[k], vv[k], yh);
-          nu = fmaf(uu[k], uu[k], nu);
-          nv = fmaf(vv[k], vv[k], nv);
-        }
-        const float rr = __uint_as_float(mr.z) - yh;
-        const float vr = __ldg(M.vreg + mr.y);
-        float du[J], dv[J];
-#pragma unroll
-        for (int k = 0; k < J; ++k) {  // src/gradients.cpp:241-247
-          du[k] = -M.weight * rr * vv[k];
-          dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
-        }
-        step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
-                        a.nonneg, M.weight * nv);
-        step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
-                        M.weight * nu);
       }
     }
 
-    rc = rc1;
-    rc1 = rc2;
 #pragma unroll
-    for (int n = 0; n < 3; ++n) sl[n] = nsl[n];
+    for (int j = 0; j < E; ++j) {
+      rc[j] = rc1[j];
+      rc1[j] = rc2[j];
+#pragma unroll
+      for (int n = 0; n < 3; ++n) sl[j][n] = nsl[j][n];
+    }
 
     // ---- periodic flushes (staggered across warps) ----
     if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {
@@ -642,75 +724,16 @@ hog3v2_kernel(Hog3v2Args a) {
         if (a.nonneg) v = fmaxf(v, 0.f);
         Gs[(q / J) * JP + (q % J)] = v;
       }
-      // hot rows: this warp's share
-#pragma unroll
-      for (int n = 0; n < 3; ++n) {
-        const HotDesc& h = a.hot[n];
-        if (h.H) {
-          const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
-          flush_hot<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1, lane);
-        }
-      }
-      for (int m = 0; m < a.n_mat; ++m) {
-        const HotDesc& h = a.mats[m].hotV;
-        if (h.H) {
-          const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
-          flush_hot<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
-                           lane);
-        }
-      }
+      flush_all_hot<J, JP, NW>(a, sm, w, lane);
     }
   }
-  // remaining matrix entries (rounding) and final hot flush of everything
+  // remaining matrix entries (rounding) and the final hot flush of everything
   while (mpos < mhi) {
-    const uint4 mr = __ldg(a.mrec + mpos);
+    matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mpos));
     ++mpos;
-    const MatDesc3& M = a.mats[mr.w];
-    const int mode = M.mode;
-    const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
-    const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
-    float uu[JP], vv[JP];
-    float* repU = sm + a.hot[mode].off;
-    float* repV = sm + M.hotV.off;
-    load_row<JP>(a.U[mode], mr.x, su, repU, uu);
-    load_row<JP>(M.V, mr.y, sv, repV, vv);
-    float yh = 0.f, nu = 0.f, nv = 0.f;
-#pragma unroll
-    for (int k = 0; k < J; ++k) {
-      yh = fmaf(uu[k], vv[k], yh);
-      nu = fmaf(uu[k], uu[k], nu);
-      nv = fmaf(vv[k], vv[k], nv);
-    }
-    const float rr = __uint_as_float(mr.z) - yh;
-    const float vr = __ldg(M.vreg + mr.y);
-    float du[J], dv[J];
-#pragma unroll
-    for (int k = 0; k < J; ++k) {
-      du[k] = -M.weight * rr * vv[k];
-      dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
-    }
-    step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
-                    a.nonneg, M.weight * nv);
-    step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
-                    M.weight * nu);
   }
   __syncthreads();
-#pragma unroll
-  for (int n = 0; n < 3; ++n) {
-    const HotDesc& h = a.hot[n];
-    if (h.H) {
-      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
-      flush_hot<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1, lane);
-    }
-  }
-  for (int m = 0; m < a.n_mat; ++m) {
-    const HotDesc& h = a.mats[m].hotV;
-    if (h.H) {
-      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
-      flush_hot<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
-                       lane);
-    }
-  }
+  flush_all_hot<J, JP, NW>(a, sm, w, lane);
 }
 
 }  // namespace cmtfb
