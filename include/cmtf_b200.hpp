@@ -116,6 +116,12 @@ struct EpochStats {
 class TrainState {
  public:
   TrainState(const TrainConfig& config, const DataBundle& bundle) : config_(config) {
+    // validate_config (src/trainer.cpp:62-66): the C ABI cannot see the
+    // tensor's order, so the rank count is checked here
+    if (config.ranks.size() != bundle.tensor.dims.size())
+      throw ValidationError("rank list has " + std::to_string(config.ranks.size()) +
+                            " entries for a tensor of order " +
+                            std::to_string(bundle.tensor.dims.size()));
     cmtf_gpu_config c;
     cmtf_gpu_config_default(&c);
     c.order = static_cast<int32_t>(config.ranks.size());

@@ -195,6 +195,9 @@ class TrainState:
     """Owns a device context holding the bundle and the model."""
 
     def __init__(self, config: TrainConfig, bundle: DataBundle):
+        if len(config.ranks) != bundle.tensor.order:  # src/trainer.cpp:62-66
+            raise ValidationError(f"rank list has {len(config.ranks)} entries for a tensor "
+                                  f"of order {bundle.tensor.order}")
         L = _abi.lib()
         self._L = L
         self.config = config
