@@ -82,6 +82,11 @@ typedef struct cmtf_gpu_config {
   int32_t flush_every;   /* sweep iterations between replica/core merges;
                             0 = default (8)                             */
   int32_t kernel_version;/* 0 = auto (v2 where specialised), 1 = v1     */
+  int32_t core_flush_every; /* sweep iterations between block-level core
+                            pushes; 0 = default (1)                     */
+  float kappa_core;      /* damping of the batched core step; the curvature
+                            estimate is the trace E|phi|^2, an upper
+                            bound of the top eigenvalue; 0 = default 2.0 */
 } cmtf_gpu_config;
 
 typedef struct cmtf_gpu_ctx cmtf_gpu_ctx;

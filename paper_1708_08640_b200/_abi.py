@@ -46,6 +46,8 @@ class cmtf_gpu_config(C.Structure):
         ("kappa", C.c_float),
         ("flush_every", C.c_int32),
         ("kernel_version", C.c_int32),
+        ("core_flush_every", C.c_int32),
+        ("kappa_core", C.c_float),
     ]
 
 

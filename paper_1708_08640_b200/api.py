@@ -145,6 +145,8 @@ class TrainConfig:
     kappa: float = 0.0  # 0 = default 0.5
     flush_every: int = 0  # 0 = default 8
     kernel_version: int = 0  # 0 = auto (v2), 1 = v1
+    core_flush_every: int = 0  # 0 = default 1
+    kappa_core: float = 0.0  # 0 = default 2.0
 
     def to_c(self):
         c = _abi.cmtf_gpu_config()
@@ -167,6 +169,8 @@ class TrainConfig:
         c.order_policy = 1 if self.order_policy == "random" else 0
         c.hot_tau, c.kappa = self.hot_tau, self.kappa
         c.flush_every, c.kernel_version = self.flush_every, self.kernel_version
+        c.core_flush_every = self.core_flush_every
+        c.kappa_core = self.kappa_core
         return c, ranks
 
 

@@ -666,6 +666,7 @@ V2Shape v2_shape(const cmtf_gpu_ctx* ctx) {
   if (const char* v = std::getenv("CMTF_V2_SHAPE")) {  // "12x1" or "8x2" (experiments)
     if (std::string(v) == "12x1") s = {12, 1};
     if (std::string(v) == "8x2") s = {8, 2};
+    if (std::string(v) == "12x2") s = {12, 2};
   }
   return s;
 }
@@ -673,7 +674,8 @@ V2Shape v2_shape(const cmtf_gpu_ctx* ctx) {
 size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
 #define FB(JV)                                                                  \
   case JV:                                                                      \
-    return sh.nw == 12 ? v2_fixed_bytes<JV, 12, 1>() : v2_fixed_bytes<JV, 8, 2>();
+    return sh.nw == 12 ? (sh.e == 2 ? v2_fixed_bytes<JV, 12, 2>() : v2_fixed_bytes<JV, 12, 1>()) \
+                       : v2_fixed_bytes<JV, 8, 2>();
   switch (J) {
     FB(4) FB(5) FB(8) FB(10)
   }
@@ -810,8 +812,10 @@ int launch_v2_nw(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
 
 template <int J, bool OPT>
 int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  return ctx->v2_nw == 12 ? launch_v2_nw<J, OPT, 12, 1>(ctx, args)
-                          : launch_v2_nw<J, OPT, 8, 2>(ctx, args);
+  if (ctx->v2_nw == 12)
+    return ctx->v2_e == 2 ? launch_v2_nw<J, OPT, 12, 2>(ctx, args)
+                          : launch_v2_nw<J, OPT, 12, 1>(ctx, args);
+  return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
 int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
@@ -856,8 +860,11 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
   a.eta = eta;
   a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
   a.kappa = ctx->cfg.kappa > 0.f ? ctx->cfg.kappa : 0.5f;
-  a.nhat_core = (float)win;
+  a.kappa_core = ctx->cfg.kappa_core > 0.f ? ctx->cfg.kappa_core : 2.0f;
+  const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every : 1;
+  a.nhat_core = (float)(W * FG * ctx->v2_e);
   a.flush_every = F;
+  a.core_every = FG;
   a.nonneg = ctx->cfg.nonnegative;
   ctx->kernel_which = 3;
   ctx->hog_threads_used = (int)W;

@@ -74,9 +74,11 @@ struct Hog3v2Args {
   float* G;
   float eta;
   float core_reg;   // lambda / nnz
-  float kappa;      // damping constant
-  float nhat_core;  // expected GPU-wide entries between two flushes of a warp
-  int flush_every;  // iterations between flushes
+  float kappa;      // damping constant (hot rows)
+  float kappa_core; // damping constant (core)
+  float nhat_core;  // expected GPU-wide entries between two core pushes of a warp
+  int flush_every;  // iterations between hot-row flushes
+  int core_every;   // iterations between core pushes
   int nonneg;
 };
 
@@ -688,44 +690,53 @@ hog3v2_kernel(Hog3v2Args a) {
       for (int n = 0; n < 3; ++n) sl[j][n] = nsl[j][n];
     }
 
-    // ---- periodic flushes (staggered across warps) ----
-    if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {
-      // core: damped batched step from this warp's accumulated gradient
+    // ---- periodic core push / refresh (block-level, every core_every) ----
+    // The warps' private accumulators are summed inside the block so only
+    // one damped push per block reaches the global core (same-address
+    // atomics serialise in L2; 8x fewer of them than per-warp pushes).
+    if ((it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters) {
+      __shared__ float red_kw[NW], red_lam[NW];
       const float kws = warp_sum(kw);
       const float lgs = warp_sum(lamG);
-      if (kws > 0.f) {
-        const float q = a.eta * (lgs / kws) * a.nhat_core;
-        const float alpha = q > a.kappa ? a.kappa / q : 1.f;
-        const float s = -a.eta * alpha;
-        for (int ab = lane; ab < AB; ab += 32) {
-#pragma unroll
-          for (int c = 0; c < JP; c += 4) {
-            float4 dv = *reinterpret_cast<float4*>(dGw + ab * JP + c);
-            const float4 gv = *reinterpret_cast<const float4*>(Gs + ab * JP + c);
-            dv.x = s * fmaf(kws * a.core_reg, gv.x, dv.x);
-            dv.y = s * fmaf(kws * a.core_reg, gv.y, dv.y);
-            dv.z = s * fmaf(kws * a.core_reg, gv.z, dv.z);
-            dv.w = s * fmaf(kws * a.core_reg, gv.w, dv.w);
-            *reinterpret_cast<float4*>(dGw + ab * JP + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-            // global core is unpadded [ab][J]: scalar REDs for the J valid columns
-            if (c + 0 < J) atomicAdd(a.G + ab * J + c + 0, dv.x);
-            if (c + 1 < J) atomicAdd(a.G + ab * J + c + 1, dv.y);
-            if (c + 2 < J) atomicAdd(a.G + ab * J + c + 2, dv.z);
-            if (c + 3 < J) atomicAdd(a.G + ab * J + c + 3, dv.w);
-          }
-        }
+      if (lane == 0) {
+        red_kw[w] = kws;
+        red_lam[w] = lgs;
       }
       kw = 0.f;
       lamG = 0.f;
-      __syncwarp();
-      // refresh this warp's share of the shared core
-      for (int q = w * 32 + lane; q < AB * J; q += NW * 32) {
-        float v = __ldcg(a.G + q);
-        if (a.nonneg) v = fmaxf(v, 0.f);
-        Gs[(q / J) * JP + (q % J)] = v;
+      __syncthreads();
+      float kb = 0.f, lb = 0.f;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        kb += red_kw[q];
+        lb += red_lam[q];
       }
-      flush_all_hot<J, JP, NW>(a, sm, w, lane);
+      if (kb > 0.f) {
+        const float q = a.eta * (lb / kb) * a.nhat_core;
+        const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
+        const float s = -a.eta * alpha;
+        float* dG0 = sm + L::G_FLOATS;
+        for (int e = threadIdx.x; e < AB * J; e += NW * 32) {
+          const int ab = e / J, c = e - (e / J) * J;
+          const int o = ab * JP + c;
+          float sum = 0.f;
+#pragma unroll
+          for (int q = 0; q < NW; ++q) {
+            float* dq = dG0 + q * (L::DG_FLOATS + L::STAGE_FLOATS) + o;
+            sum += *dq;
+            *dq = 0.f;
+          }
+          const float delta = s * fmaf(kb * a.core_reg, Gs[o], sum);
+          float v = atomicAdd(a.G + e, delta) + delta;
+          if (a.nonneg) v = fmaxf(v, 0.f);
+          Gs[o] = v;
+        }
+      }
+      __syncthreads();
     }
+    // ---- periodic hot-row merges (staggered across warps) ----
+    if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
+      flush_all_hot<J, JP, NW>(a, sm, w, lane);
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
   while (mpos < mhi) {
