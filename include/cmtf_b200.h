@@ -72,7 +72,8 @@ typedef struct cmtf_gpu_config {
   int32_t order_policy;  /* entry order of the Hogwild sweep: 0 = sorted
                             by sort_mode (row caching), 1 = a seeded random
                             permutation (the reference's shuffled
-                            schedule, src/trainer.cpp:122-128)          */
+                            schedule, src/trainer.cpp:122-128), 2 = the
+                            caller's order (DSGD strata)                */
   float hot_tau;         /* rows whose expected concurrent updates
                             (count * workers / nnz) reach hot_tau get a
                             per-block shared-memory replica; 0 = default
@@ -181,6 +182,41 @@ int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double *y,
                                     const uint32_t *col_count, double *du,
                                     double *dv, double *residual,
                                     int32_t device);
+
+/* ---- DSGD (multi-GPU) support: SURVEY.md 8(e) ----------------------
+ * A rank uploads its local bundle grouped by stratum (order_policy 2 keeps
+ * the caller's order) and runs each sub-epoch over record ranges.        */
+
+/* One Hogwild sweep over tensor records [t_lo, t_hi) and, for each coupled
+ * matrix m, records [m_lo[m], m_hi[m]) (caller order).  No epoch
+ * bookkeeping; m_lo/m_hi may be NULL (no matrix entries). */
+int cmtf_gpu_sweep_range(cmtf_gpu_ctx *ctx, uint64_t t_lo, uint64_t t_hi,
+                         const uint64_t *m_lo, const uint64_t *m_hi);
+/* epoch += 1, eta decay, non-finite scan (the tail of run_epoch). */
+int cmtf_gpu_end_epoch(cmtf_gpu_ctx *ctx);
+/* Declare the replicated parameters and the number of ranks updating them
+ * concurrently (their batched steps are damped for world * local
+ * concurrency).  mode_mask / mat_mask: bit n = factor n / coupled factor n. */
+int cmtf_gpu_set_shared(cmtf_gpu_ctx *ctx, int32_t world, uint32_t mode_mask,
+                        uint32_t mat_mask, uint64_t nnz_global);
+/* Override observation counts with the GLOBAL counts (a rank's local bundle
+ * sees only its own entries): which = mode n (0..N-1) or 100 + m for the
+ * column counts of coupled matrix m.  Recomputes lambda/count. */
+int cmtf_gpu_set_counts(cmtf_gpu_ctx *ctx, int32_t which, const uint32_t *counts,
+                        uint32_t n);
+/* NCCL communicator over the ranks (unique id from rank 0, 128 bytes). */
+int cmtf_gpu_comm_unique_id(void *id_out);
+int cmtf_gpu_comm_init(cmtf_gpu_ctx *ctx, int32_t nranks, int32_t rank,
+                       const void *unique_id);
+/* Sum the deltas (current - base) of the selected parameters over the
+ * ranks with ncclAllReduce and re-base: afterwards every rank holds
+ * base + sum of all ranks' deltas.  core != 0 includes the core. */
+int cmtf_gpu_sync(cmtf_gpu_ctx *ctx, uint32_t mode_mask, uint32_t mat_mask,
+                  int32_t core);
+/* The same reduction for n contexts living on ONE device (single-GPU
+ * emulation of the ranks, used by tests). */
+int cmtf_gpu_sync_local(cmtf_gpu_ctx *const *ctxs, int32_t n, uint32_t mode_mask,
+                        uint32_t mat_mask, int32_t core);
 
 /* Timing and introspection for the harness.  Events bracket the last
  * run_epoch on the launching stream.  kernel_ms[0..3] = tensor sweep,

@@ -430,20 +430,43 @@ void orc_shuffle(uint64_t *s, uint64_t n, uint64_t seed, int32_t epoch) {
 /* of the reference's Hogwild execution.  Returns 0, or 2 on a          */
 /* non-finite parameter (src/trainer.cpp:312-315).                      */
 /* ------------------------------------------------------------------ */
+int orc_run_epoch_counts(const orc_bundle *b, orc_model *m, uint64_t *schedule,
+                         int32_t epoch, uint64_t seed, double eta, double lambda,
+                         int32_t kernel_opt, int32_t workers, int32_t nonneg,
+                         int32_t do_shuffle, const uint32_t *given_counts,
+                         uint64_t nnz_global, uint64_t n_sched);
+
 int orc_run_epoch(const orc_bundle *b, orc_model *m, uint64_t *schedule,
                   int32_t epoch, uint64_t seed, double eta, double lambda,
                   int32_t kernel_opt, int32_t workers, int32_t nonneg,
                   int32_t do_shuffle) {
+  return orc_run_epoch_counts(b, m, schedule, epoch, seed, eta, lambda, kernel_opt,
+                              workers, nonneg, do_shuffle, NULL, 0, 0);
+}
+
+/* As orc_run_epoch, with externally supplied (global) counts and the global
+ * training nnz for the core regulariser -- the per-stratum sweep of the
+ * DSGD test oracle. */
+int orc_run_epoch_counts(const orc_bundle *b, orc_model *m, uint64_t *schedule,
+                         int32_t epoch, uint64_t seed, double eta, double lambda,
+                         int32_t kernel_opt, int32_t workers, int32_t nonneg,
+                         int32_t do_shuffle, const uint32_t *given_counts,
+                         uint64_t nnz_global, uint64_t n_sched) {
   const int order = b->order;
   uint64_t total = b->nnz;
   for (int c = 0; c < b->n_mat; ++c) total += b->mat_nnz[c];
+  if (n_sched) total = n_sched; /* a sub-schedule (one DSGD stratum) */
   if (do_shuffle) orc_shuffle(schedule, total, seed, epoch);
 
   uint64_t cnt_total = 0;
   for (int n = 0; n < order; ++n) cnt_total += b->dims[n];
   for (int c = 0; c < b->n_mat; ++c) cnt_total += b->mat_cols[c];
   uint32_t *counts = (uint32_t *)malloc(sizeof(uint32_t) * cnt_total);
-  orc_count_modes(b, counts);
+  if (given_counts)
+    memcpy(counts, given_counts, sizeof(uint32_t) * cnt_total);
+  else
+    orc_count_modes(b, counts);
+  const uint64_t nnz_core = nnz_global ? nnz_global : b->nnz;
   const uint32_t *tcount[ORC_MAX_ORDER];
   const uint32_t *mcount[64];
   {
@@ -481,7 +504,7 @@ int orc_run_epoch(const orc_bundle *b, orc_model *m, uint64_t *schedule,
         }
         double r;
         orc_compute_gradient(kernel_opt, b->vals[id], order, b->ranks, b->cp,
-                             m->core, rows, lambda, cn, b->nnz, designated,
+                             m->core, rows, lambda, cn, nnz_core, designated,
                              grow, gcore, &r);
         const double *gp = grow;
         for (int n = 0; n < order; ++n) {

@@ -511,3 +511,17 @@ def ref_generate(dims, n_entries, ranks, noise, seed, with_matrix=True, matrix_r
     mats = [dict(mode=coupled_mode, rows=int(dims[coupled_mode]), cols=int(mc[m]),
                  indices=mi[m], values=mv[m], weight=matrix_weight) for m in range(nm.value)]
     return idx, vals, mats
+
+
+def run_epoch_counts(bundle, model: OracleModel, schedule, eta, lambda_reg, counts_concat,
+                     nnz_global, kernel_opt=True):
+    """One serial sweep over `schedule` with given GLOBAL counts (DSGD stratum)."""
+    b, k1 = _bundle_struct(bundle, model.ranks)
+    ms, k2 = model.struct()
+    cc = np.ascontiguousarray(counts_concat, dtype=np.uint32)
+    orc().orc_run_epoch_counts.restype = C.c_int
+    return orc().orc_run_epoch_counts(
+        C.byref(b), C.byref(ms), _p(schedule, C.c_uint64), C.c_int32(0), C.c_uint64(0),
+        C.c_double(eta), C.c_double(lambda_reg), C.c_int32(int(kernel_opt)), C.c_int32(1),
+        C.c_int32(0), C.c_int32(0), _p(cc, C.c_uint32), C.c_uint64(nnz_global),
+        C.c_uint64(len(schedule)))

@@ -87,6 +87,15 @@ SIGNATURES = [
     ("cmtf_gpu_matrix_entry_gradients", C.c_int,
      [C.c_uint64, C.c_uint32, f64p, f64p, f64p, C.c_double, C.c_double, u32p, f64p,
       f64p, f64p, C.c_int32]),
+    ("cmtf_gpu_sweep_range", C.c_int, [P, C.c_uint64, C.c_uint64, u64p, u64p]),
+    ("cmtf_gpu_end_epoch", C.c_int, [P]),
+    ("cmtf_gpu_set_shared", C.c_int, [P, C.c_int32, C.c_uint32, C.c_uint32, C.c_uint64]),
+    ("cmtf_gpu_set_counts", C.c_int, [P, C.c_int32, u32p, C.c_uint32]),
+    ("cmtf_gpu_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("cmtf_gpu_comm_init", C.c_int, [P, C.c_int32, C.c_int32, C.c_void_p]),
+    ("cmtf_gpu_sync", C.c_int, [P, C.c_uint32, C.c_uint32, C.c_int32]),
+    ("cmtf_gpu_sync_local", C.c_int, [C.POINTER(P), C.c_int32, C.c_uint32, C.c_uint32,
+                                      C.c_int32]),
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
 ]

@@ -140,7 +140,7 @@ class TrainConfig:
     hog_threads: int = 0
     sort_mode: int = -1
     force_generic: bool = False
-    order_policy: str = "random"  # "random" | "sorted"
+    order_policy: str = "random"  # "random" | "sorted" | "caller"
     hot_tau: float = 0.0  # 0 = default 2.0, < 0 disables hot-row replicas
     kappa: float = 0.0  # 0 = default 0.5
     flush_every: int = 0  # 0 = default 8
@@ -166,7 +166,7 @@ class TrainConfig:
         c.hog_threads = self.hog_threads
         c.sort_mode = self.sort_mode
         c.force_generic = int(self.force_generic)
-        c.order_policy = 1 if self.order_policy == "random" else 0
+        c.order_policy = {"random": 1, "caller": 2}.get(self.order_policy, 0)
         c.hot_tau, c.kappa = self.hot_tau, self.kappa
         c.flush_every, c.kernel_version = self.flush_every, self.kernel_version
         c.core_flush_every = self.core_flush_every

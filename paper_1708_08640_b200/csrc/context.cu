@@ -4,6 +4,7 @@
 // trainer (/root/reference/proj/core/src/trainer.cpp) and is native C++;
 // every O(nnz) step runs on the device.
 #include <cub/device/device_radix_sort.cuh>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -114,6 +115,18 @@ struct cmtf_gpu_ctx {
   int v2_nw = 8;
   int v2_e = 2;
   size_t v2_smem = 0;
+
+  // DSGD: replicated parameters, global sizes, communicator
+  uint64_t nnz_global = 0;  // 0 = local nnz
+  int world = 1;
+  uint32_t shared_modes = 0, shared_mats = 0;
+  std::vector<uint64_t> mat_base;  // offset of matrix m in the merged stream
+  float* baseU[kMaxOrder] = {};
+  float* baseV[kMaxMats] = {};
+  float* baseG = nullptr;
+  float* sync_buf = nullptr;
+  uint64_t sync_cap = 0;
+  ncclComm_t comm = nullptr;
 
   // timing
   cudaEvent_t ev[6] = {};
@@ -344,6 +357,10 @@ int sort_ids(cmtf_gpu_ctx* ctx, uint32_t* keys, uint32_t* ids, uint64_t n,
   cudaFree(keys_out);
   *sorted_ids_out = ids_out;
   return CMTF_OK;
+}
+
+uint64_t nnz_all_of(const cmtf_gpu_ctx* ctx) {
+  return ctx->nnz_global ? ctx->nnz_global : ctx->nnz;
 }
 
 ModeTables mode_tables(const cmtf_gpu_ctx* ctx) {
@@ -597,8 +614,12 @@ int scan_nonfinite(cmtf_gpu_ctx* ctx, std::string* offender) {
   return CMTF_OK;
 }
 
-int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M, float eta) {
-  if (M.nnz == 0) return CMTF_OK;
+int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M0, float eta, uint64_t lo, uint64_t hi) {
+  DevMatrix M = M0;
+  if (hi > M0.nnz) hi = M0.nnz;
+  if (hi <= lo) return CMTF_OK;
+  M.rec = M0.rec + 3 * lo;
+  M.nnz = hi - lo;
   const int JP = (int)ctx->JP(M.mode);
   const int bt = 256;
   uint64_t threads = std::min<uint64_t>((uint64_t)ctx->num_sms * 2048,
@@ -711,16 +732,19 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     TRY(ensure(ctx, &ctx->mrec, &ctx->mrec_cap, ctx->mnnz));
     TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, ctx->mnnz));
     uint64_t base = 0;
+    ctx->mat_base.assign(ctx->mats.size() + 1, 0);
     for (size_t m = 0; m < ctx->mats.size(); ++m) {
       const auto& M = ctx->mats[m];
+      ctx->mat_base[m] = base;
       if (M.nnz)
         merge_matrix_kernel<<<grid_for(M.nnz), 256, 0, ctx->stream>>>(M.rec, M.nnz,
                                                                       (uint32_t)m, base,
                                                                       ctx->s_m4);
       base += M.nnz;
     }
-    uint64_t pa, pb;
-    affine_params(ctx->mnnz, ctx->cfg.seed + 1, &pa, &pb);
+    ctx->mat_base[ctx->mats.size()] = base;
+    uint64_t pa = 1, pb = 0;  // caller order keeps the concatenation
+    if (ctx->cfg.order_policy != 2) affine_params(ctx->mnnz, ctx->cfg.seed + 1, &pa, &pb);
     scatter_affine_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(
         reinterpret_cast<const uint32_t*>(ctx->s_m4), ctx->mnnz, 4, pa, pb,
         reinterpret_cast<uint32_t*>(ctx->mrec), ctx->s_ids);
@@ -818,20 +842,37 @@ int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
   return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
-int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
+// One v2 sweep over tensor records [t_lo, t_hi) and matrix records
+// [m_lo[m], m_hi[m]) (NULL ranges = every matrix entry).
+int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
+             const uint64_t* m_lo, const uint64_t* m_hi) {
   if (ctx->v2_dirty) TRY(prepare_v2(ctx, J));
   Hog3v2Args a{};
-  a.rec = reinterpret_cast<const uint4*>(ctx->rec);
-  a.nnz = ctx->nnz;
+  a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
+  a.nnz = t_hi - t_lo;
   a.mrec = ctx->mrec;
-  a.mnnz = ctx->mnnz;
   a.n_mat = (int)ctx->mats.size();
+  if (m_lo && m_hi) {
+    a.n_mr = (int)ctx->mats.size();
+    a.mnnz = 0;
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      a.mr_lo[m] = ctx->mat_base[m] + m_lo[m];
+      a.mr_n[m] = m_hi[m] - m_lo[m];
+      a.mnnz += a.mr_n[m];
+    }
+  } else {
+    a.n_mr = 1;
+    a.mr_lo[0] = 0;
+    a.mr_n[0] = ctx->mnnz;
+    a.mnnz = ctx->mnnz;
+  }
+  if (a.nnz == 0 && a.mnnz == 0) return CMTF_OK;
   const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 8;
   const double W = (double)ctx->v2_blocks * ctx->v2_nw * 32;
   // entries processed GPU-wide between two flushes of one warp: W * F * E
   const double win = W * F * ctx->v2_e;
-  const float nhat_scale = (float)(win / (double)ctx->nnz);
-  auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count) {
+  const float nhat_scale = (float)(win / (double)std::max<uint64_t>(1, ctx->nnz));
+  auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count, bool shared) {
     HotDesc d{};
     d.slot = h.H ? h.slot : nullptr;
     d.row_of = h.row_of;
@@ -840,13 +881,14 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
     d.off = h.off;
     d.stat_off = h.stat_off;
     d.base = h.base;
-    d.nhat_scale = nhat_scale;
+    // replicated parameters are updated by `world` ranks at once
+    d.nhat_scale = nhat_scale * (shared ? (float)ctx->world : 1.f);
     return d;
   };
   for (int n = 0; n < 3; ++n) {
     a.U[n] = ctx->U[n];
     a.reg[n] = ctx->reg[n];
-    a.hot[n] = hd(ctx->hot[n], ctx->count[n]);
+    a.hot[n] = hd(ctx->hot[n], ctx->count[n], (ctx->shared_modes >> n) & 1u);
   }
   for (size_t m = 0; m < ctx->mats.size(); ++m) {
     const auto& M = ctx->mats[m];
@@ -854,15 +896,16 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
     a.mats[m].V = M.V;
     a.mats[m].vreg = M.vreg;
     a.mats[m].weight = (float)M.weight;
-    a.mats[m].hotV = hd(ctx->hotV[m], M.count);
+    a.mats[m].hotV = hd(ctx->hotV[m], M.count, (ctx->shared_mats >> m) & 1u);
   }
   a.G = ctx->G;
   a.eta = eta;
-  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  const uint64_t nnz_all = ctx->nnz_global ? ctx->nnz_global : ctx->nnz;
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all);
   a.kappa = ctx->cfg.kappa > 0.f ? ctx->cfg.kappa : 0.5f;
   a.kappa_core = ctx->cfg.kappa_core > 0.f ? ctx->cfg.kappa_core : 2.0f;
   const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every : 1;
-  a.nhat_core = (float)(W * FG * ctx->v2_e);
+  a.nhat_core = (float)(W * FG * ctx->v2_e * ctx->world);
   a.flush_every = F;
   a.core_every = FG;
   a.nonneg = ctx->cfg.nonnegative;
@@ -879,13 +922,14 @@ int v2_epoch(cmtf_gpu_ctx* ctx, int J, float eta) {
   return set_err(ctx, CMTF_EUNSUPPORTED, "no v2 kernel for J=%d", J);
 }
 
-int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
+int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi) {
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
   int J = 0;
+  if (t_hi <= t_lo) return CMTF_OK;
   if (fast3_supported(ctx, &J)) {
     Hog3Args a{};
-    a.rec = reinterpret_cast<const uint4*>(ctx->rec);
-    a.nnz = ctx->nnz;
+    a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
+    a.nnz = t_hi - t_lo;
     for (int n = 0; n < 3; ++n) {
       a.U[n] = ctx->U[n];
       a.reg[n] = ctx->reg[n];
@@ -893,7 +937,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
     a.G = ctx->G;
     a.eta = eta;
     a.eta_core = eta;
-    a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+    a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
     a.nonneg = ctx->cfg.nonnegative;
     ctx->kernel_which = 1;
     return launch_hog3(ctx, J, a, opt, ctx->cfg.order_policy == 1 ? 0 : ctx->sort_mode,
@@ -903,11 +947,11 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
   HogArgs a{};
   a.cs = core_shape(ctx);
   a.G = ctx->G;
-  a.rec = ctx->rec;
-  a.nnz = ctx->nnz;
+  a.rec = ctx->rec + t_lo * (ctx->order + 1);
+  a.nnz = t_hi - t_lo;
   a.mt = mode_tables(ctx);
   a.eta = eta;
-  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
   a.nonneg = ctx->cfg.nonnegative;
   const int bt = 256;
   const size_t smem =
@@ -921,7 +965,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta) {
   int blocks = ctx->num_sms * per_sm;
   if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / 32 / (bt / 32));
   else {
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (1024ull * (bt / 32)));
+    const uint64_t cap = std::max<uint64_t>(1, a.nnz / (1024ull * (bt / 32)));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->hog_threads_used = blocks * (bt / 32);
@@ -967,7 +1011,7 @@ int serial_epoch(cmtf_gpu_ctx* ctx, float eta) {
   a.n_sched = total;
   a.eta = eta;
   a.eta_core = eta;  // P = 1: core step eta (src/trainer.cpp:211-219)
-  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
   a.nonneg = ctx->cfg.nonnegative;
   const int bt = 256;
   const size_t smem = sizeof(float) * (a.cs.size + 2 * a.cs.off[a.cs.order] + 32);
@@ -1119,6 +1163,11 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   }
   dfree(ctx->mrec);
   dfree(ctx->s_m4);
+  for (auto& b : ctx->baseU) dfree(b);
+  for (auto& b : ctx->baseV) dfree(b);
+  dfree(ctx->baseG);
+  dfree(ctx->sync_buf);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (auto& h : ctx->hot) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   for (auto& h : ctx->hotV) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   dfree(ctx->G);
@@ -1207,7 +1256,10 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
   TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
   uint32_t* sorted_ids = nullptr;
-  if (shuffled) {
+  if (ctx->cfg.order_policy == 2) {  // caller order (DSGD strata)
+    scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, 1, 0,
+                                                                  ctx->rec, ctx->pos);
+  } else if (shuffled) {
     uint64_t pa, pb;
     affine_params(nnz, ctx->cfg.seed, &pa, &pb);
     scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, pa, pb,
@@ -1326,7 +1378,10 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
     }
     uint32_t* sorted_ids = nullptr;
-    if (shuffled) {
+    if (ctx->cfg.order_policy == 2) {
+      scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, 3, 1, 0, M.rec,
+                                                                    M.pos);
+    } else if (shuffled) {
       uint64_t pa, pb;
       affine_params(nnz, ctx->cfg.seed + 7 + ctx->mats.size(), &pa, &pb);
       scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, 3, pa, pb,
@@ -1448,35 +1503,44 @@ int cmtf_gpu_set_state(cmtf_gpu_ctx* ctx, int32_t epoch, double eta) {
   return CMTF_OK;
 }
 
-int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
-  TRY(require_bundle(ctx));
-  CU(cudaSetDevice(ctx->device));
+}  // extern "C"
+
+namespace {
+
+// One sweep (no epoch bookkeeping) over a tensor range and matrix ranges.
+int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
+          const uint64_t* m_hi) {
   const float eta = (float)ctx->eta;
-  ctx->last_launches = 0;
-  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (ctx->cfg.exec_mode == CMTF_EXEC_SERIAL) {
     TRY(serial_epoch(ctx, eta));
     ctx->last_launches += 1;
     CU(cudaEventRecord(ctx->ev[1], ctx->stream));
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-  } else {
-    int J = 0;
-    if (v2_supported(ctx, &J)) {
-      TRY(v2_epoch(ctx, J, eta));  // tensor + interleaved matrix entries
-      ctx->last_launches += 1;
-      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-      CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-    } else {
-      TRY(hogwild_tensor_sweep(ctx, eta));
-      ctx->last_launches += 1;
-      CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-      for (auto& M : ctx->mats) {
-        TRY(matrix_sweep(ctx, M, eta));
-        ctx->last_launches += M.nnz ? 1 : 0;
-      }
-      CU(cudaEventRecord(ctx->ev[2], ctx->stream));
-    }
+    return CMTF_OK;
   }
+  int J = 0;
+  if (v2_supported(ctx, &J)) {
+    TRY(v2_sweep(ctx, J, eta, t_lo, t_hi, m_lo, m_hi));  // + interleaved matrices
+    ctx->last_launches += 1;
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    return CMTF_OK;
+  }
+  TRY(hogwild_tensor_sweep(ctx, eta, t_lo, t_hi));
+  ctx->last_launches += 1;
+  CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    const auto& M = ctx->mats[m];
+    const uint64_t lo = m_lo ? m_lo[m] : 0, hi = m_hi ? m_hi[m] : M.nnz;
+    TRY(matrix_sweep(ctx, M, eta, lo, hi));
+    ctx->last_launches += hi > lo ? 1 : 0;
+  }
+  CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  return CMTF_OK;
+}
+
+// Tail of run_epoch (src/trainer.cpp:309-315): decay, divergence check.
+int end_epoch(cmtf_gpu_ctx* ctx) {
   std::string offender;
   TRY(scan_nonfinite(ctx, &offender));
   CU(cudaEventRecord(ctx->ev[3], ctx->stream));
@@ -1490,7 +1554,6 @@ int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
   ctx->last_ms[2] = ms;
   cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
   ctx->last_ms[3] = ms;
-  // src/trainer.cpp:309-315
   ctx->epoch += 1;
   ctx->eta = ctx->cfg.eta0 / (1.0 + ctx->cfg.mu * ctx->epoch);
   if (!offender.empty())
@@ -1498,6 +1561,246 @@ int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
                    "non-finite parameter after epoch %d: %s; try a smaller initial "
                    "learning rate",
                    ctx->epoch, offender.c_str());
+  return CMTF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cmtf_gpu_run_epoch(cmtf_gpu_ctx* ctx) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  ctx->last_launches = 0;
+  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  TRY(sweep(ctx, 0, ctx->nnz, nullptr, nullptr));
+  return end_epoch(ctx);
+}
+
+int cmtf_gpu_sweep_range(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
+                         const uint64_t* m_hi) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (t_hi > ctx->nnz || t_lo > t_hi)
+    return set_err(ctx, CMTF_EVALIDATION, "tensor range out of bounds");
+  if (m_lo && m_hi)
+    for (size_t m = 0; m < ctx->mats.size(); ++m)
+      if (m_hi[m] > ctx->mats[m].nnz || m_lo[m] > m_hi[m])
+        return set_err(ctx, CMTF_EVALIDATION, "matrix range out of bounds");
+  if (ctx->cfg.exec_mode == CMTF_EXEC_SERIAL)
+    return set_err(ctx, CMTF_EUNSUPPORTED, "range sweeps are Hogwild-only");
+  if (ctx->cfg.order_policy != 2 && m_lo)
+    return set_err(ctx, CMTF_EVALIDATION, "matrix ranges need order_policy 2 (caller order)");
+  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  return sweep(ctx, t_lo, t_hi, m_lo, m_hi);
+}
+
+int cmtf_gpu_end_epoch(cmtf_gpu_ctx* ctx) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  return end_epoch(ctx);
+}
+
+}  // extern "C"
+
+// ---- DSGD support -------------------------------------------------------
+namespace {
+
+int snapshot_bases(cmtf_gpu_ctx* ctx) {
+  auto snap = [&](float** base, const float* cur, uint64_t n) -> int {
+    if (!*base) CU(cudaMalloc(reinterpret_cast<void**>(base), n * sizeof(float)));
+    CU(cudaMemcpyAsync(*base, cur, n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    return CMTF_OK;
+  };
+  for (int n = 0; n < ctx->order; ++n)
+    TRY(snap(&ctx->baseU[n], ctx->U[n], (uint64_t)ctx->dims[n] * ctx->JP(n)));
+  for (size_t m = 0; m < ctx->mats.size(); ++m)
+    TRY(snap(&ctx->baseV[m], ctx->mats[m].V, (uint64_t)ctx->mats[m].cols * ctx->JP(ctx->mats[m].mode)));
+  TRY(snap(&ctx->baseG, ctx->G, ctx->core_size()));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return CMTF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cmtf_gpu_set_shared(cmtf_gpu_ctx* ctx, int32_t world, uint32_t mode_mask, uint32_t mat_mask,
+                        uint64_t nnz_global) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (world < 1) return set_err(ctx, CMTF_EVALIDATION, "world must be >= 1");
+  ctx->world = world;
+  ctx->shared_modes = mode_mask;
+  ctx->shared_mats = mat_mask;
+  ctx->nnz_global = nnz_global;
+  ctx->v2_dirty = true;
+  return snapshot_bases(ctx);
+}
+
+int cmtf_gpu_set_counts(cmtf_gpu_ctx* ctx, int32_t which, const uint32_t* counts, uint32_t n) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  CU(cudaSetDevice(ctx->device));
+  uint32_t* dst = nullptr;
+  float* reg = nullptr;
+  float lam = (float)ctx->cfg.lambda_reg;
+  if (which >= 0 && which < ctx->order) {
+    if (n != ctx->dims[which]) return set_err(ctx, CMTF_EVALIDATION, "count length mismatch");
+    dst = ctx->count[which];
+    reg = ctx->reg[which];
+  } else if (which >= 100 && which - 100 < (int)ctx->mats.size()) {
+    auto& M = ctx->mats[which - 100];
+    if (n != M.cols) return set_err(ctx, CMTF_EVALIDATION, "count length mismatch");
+    dst = M.count;
+    reg = M.vreg;
+    lam = (float)(M.weight * ctx->cfg.lambda_reg);
+  } else {
+    return set_err(ctx, CMTF_EVALIDATION, "no such count array");
+  }
+  CU(cudaMemcpy(dst, counts, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  reg_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(dst, n, lam, reg);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->v2_dirty = true;  // hot sets follow the counts
+  return CMTF_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+__global__ void delta_kernel(const float* cur, const float* base, float* d, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    d[i] = cur[i] - base[i];
+}
+__global__ void accum_delta_kernel(const float* cur, const float* base, float* d, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    d[i] += cur[i] - base[i];
+}
+__global__ void rebase_kernel(float* cur, float* base, const float* d, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = base[i] + d[i];
+    cur[i] = v;
+    base[i] = v;
+  }
+}
+
+struct SyncArr {
+  float* cur;
+  float* base;
+  uint64_t n;
+};
+
+std::vector<SyncArr> sync_arrays(cmtf_gpu_ctx* ctx, uint32_t mode_mask, uint32_t mat_mask,
+                                 int core) {
+  std::vector<SyncArr> v;
+  for (int n = 0; n < ctx->order; ++n)
+    if ((mode_mask >> n) & 1u)
+      v.push_back({ctx->U[n], ctx->baseU[n], (uint64_t)ctx->dims[n] * ctx->JP(n)});
+  for (size_t m = 0; m < ctx->mats.size(); ++m)
+    if ((mat_mask >> m) & 1u)
+      v.push_back({ctx->mats[m].V, ctx->baseV[m],
+                   (uint64_t)ctx->mats[m].cols * ctx->JP(ctx->mats[m].mode)});
+  if (core) v.push_back({ctx->G, ctx->baseG, ctx->core_size()});
+  return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cmtf_gpu_comm_unique_id(void* id_out) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess)
+    return set_err(nullptr, CMTF_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(id_out, &id, sizeof id);
+  return CMTF_OK;
+}
+
+int cmtf_gpu_comm_init(cmtf_gpu_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  CU(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  ctx->comm = nullptr;
+  ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+  if (r != ncclSuccess)
+    return set_err(ctx, CMTF_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_sync(cmtf_gpu_ctx* ctx, uint32_t mode_mask, uint32_t mat_mask, int32_t core) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (!ctx->baseG) return set_err(ctx, CMTF_EVALIDATION, "call cmtf_gpu_set_shared first");
+  auto arrs = sync_arrays(ctx, mode_mask, mat_mask, core);
+  uint64_t total = 0;
+  for (auto& s : arrs) total += s.n;
+  TRY(ensure(ctx, &ctx->sync_buf, &ctx->sync_cap, total));
+  uint64_t off = 0;
+  for (auto& s : arrs) {
+    delta_kernel<<<grid_for(s.n), 256, 0, ctx->stream>>>(s.cur, s.base, ctx->sync_buf + off, s.n);
+    off += s.n;
+  }
+  CU(cudaGetLastError());
+  if (ctx->comm && total) {
+    ncclResult_t r = ncclAllReduce(ctx->sync_buf, ctx->sync_buf, total, ncclFloat, ncclSum,
+                                   ctx->comm, ctx->stream);
+    if (r != ncclSuccess)
+      return set_err(ctx, CMTF_ENCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+  }
+  off = 0;
+  for (auto& s : arrs) {
+    rebase_kernel<<<grid_for(s.n), 256, 0, ctx->stream>>>(s.cur, s.base, ctx->sync_buf + off, s.n);
+    off += s.n;
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_sync_local(cmtf_gpu_ctx* const* ctxs, int32_t n, uint32_t mode_mask,
+                        uint32_t mat_mask, int32_t core) {
+  cmtf_gpu_ctx* ctx = n > 0 ? ctxs[0] : nullptr;
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "no contexts");
+  for (int i = 0; i < n; ++i) {
+    TRY(require_bundle(ctxs[i]));
+    if (ctxs[i]->device != ctx->device)
+      return set_err(ctx, CMTF_EVALIDATION, "sync_local needs one device");
+    if (!ctxs[i]->baseG) return set_err(ctx, CMTF_EVALIDATION, "call cmtf_gpu_set_shared first");
+    CU(cudaStreamSynchronize(ctxs[i]->stream));
+  }
+  CU(cudaSetDevice(ctx->device));
+  auto a0 = sync_arrays(ctx, mode_mask, mat_mask, core);
+  uint64_t total = 0;
+  for (auto& s : a0) total += s.n;
+  TRY(ensure(ctx, &ctx->sync_buf, &ctx->sync_cap, total));
+  CU(cudaMemsetAsync(ctx->sync_buf, 0, total * sizeof(float), ctx->stream));
+  for (int i = 0; i < n; ++i) {
+    auto ai = sync_arrays(ctxs[i], mode_mask, mat_mask, core);
+    uint64_t off = 0;
+    for (auto& s : ai) {
+      accum_delta_kernel<<<grid_for(s.n), 256, 0, ctx->stream>>>(s.cur, s.base,
+                                                                 ctx->sync_buf + off, s.n);
+      off += s.n;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    auto ai = sync_arrays(ctxs[i], mode_mask, mat_mask, core);
+    uint64_t off = 0;
+    for (auto& s : ai) {
+      rebase_kernel<<<grid_for(s.n), 256, 0, ctx->stream>>>(s.cur, s.base, ctx->sync_buf + off,
+                                                            s.n);
+      off += s.n;
+    }
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
   return CMTF_OK;
 }
 
@@ -1646,7 +1949,7 @@ int cmtf_gpu_entry_grads(cmtf_gpu_ctx* ctx, const uint64_t* ids, uint64_t n,
   a.ids = d_ids;
   a.mt = mode_tables(ctx);
   a.n = n;
-  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)ctx->nnz);
+  a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
   a.with_core = gcore != nullptr;
   a.xhat = d_x;
   a.resid = d_r;

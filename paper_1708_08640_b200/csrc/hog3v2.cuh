@@ -65,7 +65,10 @@ struct Hog3v2Args {
   const uint4* rec;     // tensor records {i1, i2, i3, bits(x)}, random order
   uint64_t nnz;
   const uint4* mrec;    // matrix records {row, col, bits(y), matrix id}
-  uint64_t mnnz;
+  uint64_t mnnz;        // total over the ranges below
+  int n_mr;             // matrix record ranges swept (virtual concatenation)
+  uint64_t mr_lo[kV2MaxMats];
+  uint64_t mr_n[kV2MaxMats];
   int n_mat;
   MatDesc3 mats[kV2MaxMats];
   float* U[3];
@@ -341,6 +344,15 @@ __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int 
       }
     }
   }
+}
+
+// virtual index over the swept matrix ranges -> physical record index
+__device__ __forceinline__ uint64_t mphys(const Hog3v2Args& a, uint64_t k) {
+  for (int r = 0; r < a.n_mr; ++r) {
+    if (k < a.mr_n[r]) return a.mr_lo[r] + k;
+    k -= a.mr_n[r];
+  }
+  return 0;
 }
 
 // One coupled-matrix entry (src/gradients.cpp:225-248; trainer.cpp:220-235).
@@ -677,7 +689,7 @@ hog3v2_kernel(Hog3v2Args a) {
     {
       const uint64_t due = mlo + (mhi - mlo) * (it + 1) / iters;
       while (mpos < due) {
-        matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mpos));
+        matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mphys(a, mpos)));
         ++mpos;
       }
     }
@@ -740,7 +752,7 @@ hog3v2_kernel(Hog3v2Args a) {
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
   while (mpos < mhi) {
-    matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mpos));
+    matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mphys(a, mpos)));
     ++mpos;
   }
   __syncthreads();
