@@ -49,6 +49,8 @@ def parse():
                    help="tensor entries in the bounded CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--dsgd", action="store_true",
+                   help="use the DSGD/NCCL path even with one rank (testing)")
     return p.parse_args()
 
 
@@ -86,43 +88,47 @@ def algorithmic(bundle, ranks):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons DURING the timed region: NVML polled
+    every 5 ms from a background thread (nvidia-smi -lms cannot sample a
+    tens-of-milliseconds window densely enough)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
-        self.samples, self.proc, self.index = [], None, index
+        self.index = index
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.samples.append([s.strip() for s in line.split(",")])
+            def loop():
+                while not self._stop.is_set():
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for name, bit in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                    time.sleep(0.005)
+
+            self._t = threading.Thread(target=loop, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        self._stop.set()
+        if self._t:
+            self._t.join(1)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "NVML, 5 ms polling"}
 
 
 def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None):
@@ -322,10 +328,117 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_dsgd(args):
+    """N > 1: DSGD strata over the ranks (one process per GPU), deltas of the
+    replicated parameters all-reduced with NCCL inside the library after every
+    sub-epoch.  Total work is the fixed workload (strong scaling)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1708_08640_b200 import api, dsgd
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"), rank=rank,
+                            world_size=world)
+    spec, bundle, test, ranks, lr, lam = make_workload(args)
+    cfg = api.TrainConfig(ranks=ranks, seed=0, eta0=lr, lambda_reg=lam, kernel=args.kernel,
+                          device=local)
+    part = dsgd.partition(bundle, world)
+    rs = dsgd.RankState(part, rank, cfg)
+    obj = [dsgd.new_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    dsgd.comm_init(rs, world, rank, obj[0])
+    L, h = rs.state._L, rs.state._h
+    nt, Bt, Ft, mats = algorithmic(bundle, ranks)
+    n_upd = nt + sum(n for n, _ in mats)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    for _ in range(args.warmup):
+        dsgd.run_epoch_nccl(rs)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    per = []
+    ms = C.c_double()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        rs.state._check(L.cmtf_gpu_mark(h, 0))
+        dsgd.run_epoch_nccl(rs)
+        rs.state._check(L.cmtf_gpu_mark(h, 1))
+        rs.state._check(L.cmtf_gpu_elapsed_ms(h, 0, 1, C.byref(ms)))
+        per.append(ms.value)
+    clk = clocks.stop()
+    t = torch.tensor([sum(per) / len(per)], device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    value = n_upd / (ms_step * 1e-3)
+    props = torch.cuda.get_device_properties(local)
+    peak = fp32_peak_tflops(props.multi_processor_count, 1965.0) * world
+    achieved = nt * Ft / (ms_step * 1e-3) / 1e12
+    n_sync = bin(rs.plan.sync_modes).count("1") + len(bundle.matrices) + 1
+    launches = args.steps * (world * (1 + 2 * n_sync) + 2 * bin(rs.plan.end_modes).count("1")
+                             + 1 + len(ranks) + len(bundle.matrices))
+    line = None
+    if rank == 0:
+        full = api.TrainState(api.TrainConfig(ranks=ranks, seed=0, eta0=lr, lambda_reg=lam,
+                                              device=local), bundle)
+        full.model = rs.state.model
+        line = {
+            "metric": "tensor+matrix nonzero SGD updates/sec per epoch", "value": value,
+            "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} (BASELINE configs[1]), scale {args.scale}",
+                       "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
+                       "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
+                       "parallelism": f"dsgd{world} (mode-1 x mode-2 strata, NCCL all-reduce "
+                                      "of replicated deltas per sub-epoch)",
+                       "l2": "flushed between epochs"},
+            "quality": {"train_rmse": api.epoch_stats(full, lam).train_rmse,
+                        "test_rmse": api.test_rmse(full, test), "epochs_done": rs.state.epoch},
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"nominal FP32 x {world} GPUs",
+                         "kernel": "whole DSGD epoch (sweeps + NCCL syncs)"},
+            "clocks": clk, "gpu_launches": launches,
+            "e2e": None,
+        }
+    # e2e: re-upload the rank's local bundle from host memory, run the epoch,
+    # read the stats back (wall clock, max over ranks)
+    ts = []
+    for _ in range(max(2, args.steps // 2)):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        rs.reupload(part)
+        dsgd.run_epoch_nccl(rs)
+        api.epoch_stats(rs.state, lam)
+        ts.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.median(ts)], device=f"cuda:{local}")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        lb = rs.plan.bundle
+        h2d = lb.tensor.indices.nbytes + lb.tensor.values.nbytes + sum(
+            m.indices.nbytes + m.values.nbytes for m in lb.matrices)
+        line["e2e"] = {"value": n_upd / float(te.item()), "unit": "updates/s",
+                       "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": 16 * world,
+                       "ms_per_step": 1e3 * float(te.item())}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[1] > 1 or args.dsgd:
+        run_dsgd(args)
     else:
         run_ours(args)
 

@@ -218,6 +218,11 @@ int cmtf_gpu_sync(cmtf_gpu_ctx *ctx, uint32_t mode_mask, uint32_t mat_mask,
 int cmtf_gpu_sync_local(cmtf_gpu_ctx *const *ctxs, int32_t n, uint32_t mode_mask,
                         uint32_t mat_mask, int32_t core);
 
+/* Device-side timing marks on the context's launching stream: record event
+ * `slot` (0..7); elapsed milliseconds between two recorded marks. */
+int cmtf_gpu_mark(cmtf_gpu_ctx *ctx, int32_t slot);
+int cmtf_gpu_elapsed_ms(cmtf_gpu_ctx *ctx, int32_t from, int32_t to, double *ms);
+
 /* Timing and introspection for the harness.  Events bracket the last
  * run_epoch on the launching stream.  kernel_ms[0..3] = tensor sweep,
  * matrix sweep(s), non-finite scan, total; launches = kernels launched. */

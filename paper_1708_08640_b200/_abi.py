@@ -96,6 +96,8 @@ SIGNATURES = [
     ("cmtf_gpu_sync", C.c_int, [P, C.c_uint32, C.c_uint32, C.c_int32]),
     ("cmtf_gpu_sync_local", C.c_int, [C.POINTER(P), C.c_int32, C.c_uint32, C.c_uint32,
                                       C.c_int32]),
+    ("cmtf_gpu_mark", C.c_int, [P, C.c_int32]),
+    ("cmtf_gpu_elapsed_ms", C.c_int, [P, C.c_int32, C.c_int32, f64p]),
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
 ]

@@ -130,6 +130,7 @@ struct cmtf_gpu_ctx {
 
   // timing
   cudaEvent_t ev[6] = {};
+  cudaEvent_t uev[8] = {};
   double last_ms[4] = {0, 0, 0, 0};
   int32_t last_launches = 0;
   int kernel_which = 0;
@@ -1124,6 +1125,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->uev) cudaEventCreate(&ev);
   if (cudaMalloc(&ctx->d_first, sizeof(unsigned long long) * (1 + kMaxOrder + kMaxMats)) !=
       cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "allocation failed"));
@@ -1175,6 +1177,8 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->d_partial);
   dfree(ctx->d_first);
   for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ctx->uev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -2116,6 +2120,25 @@ int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double* y,
   }
   for (uint64_t q = 0; q < n; ++q)
     if (residual) residual[q] = hr[q];
+  return CMTF_OK;
+}
+
+int cmtf_gpu_mark(cmtf_gpu_ctx* ctx, int32_t slot) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (slot < 0 || slot >= 8) return set_err(ctx, CMTF_EVALIDATION, "mark slot out of range");
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaEventRecord(ctx->uev[slot], ctx->stream));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_elapsed_ms(cmtf_gpu_ctx* ctx, int32_t from, int32_t to, double* ms) {
+  if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
+  if (from < 0 || from >= 8 || to < 0 || to >= 8)
+    return set_err(ctx, CMTF_EVALIDATION, "mark slot out of range");
+  CU(cudaEventSynchronize(ctx->uev[to]));
+  float f = 0.f;
+  CU(cudaEventElapsedTime(&f, ctx->uev[from], ctx->uev[to]));
+  *ms = f;
   return CMTF_OK;
 }
 

@@ -139,6 +139,13 @@ class RankState:
         cfg = TrainConfig(**{**config.__dict__, "order_policy": "caller"})
         self.plan = plan
         self.state = TrainState(cfg, plan.bundle)
+        self._set_counts(part)
+        self.state.initialize()  # same seed on every rank: identical replicas
+        L, h = self.state._L, self.state._h
+        self.state._check(L.cmtf_gpu_set_shared(h, plan.world, plan.shared_modes,
+                                                plan.mat_mask, part.nnz))
+
+    def _set_counts(self, part: Partition):
         L, h = self.state._L, self.state._h
         for n, c in enumerate(part.counts):
             c = np.ascontiguousarray(c)
@@ -146,9 +153,11 @@ class RankState:
         for m, c in enumerate(part.col_counts):
             c = np.ascontiguousarray(c)
             self.state._check(L.cmtf_gpu_set_counts(h, 100 + m, _ptr(c, C.c_uint32), c.shape[0]))
-        self.state.initialize()  # same seed on every rank: identical replicas
-        self.state._check(L.cmtf_gpu_set_shared(h, plan.world, plan.shared_modes,
-                                                plan.mat_mask, part.nnz))
+
+    def reupload(self, part: Partition):
+        """Upload the local bundle again from host memory (keeps the model)."""
+        self.state.upload(self.plan.bundle)
+        self._set_counts(part)
 
     def sweep(self, t: int):
         lo, hi = self.plan.t_ranges[t]

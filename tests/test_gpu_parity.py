@@ -327,3 +327,31 @@ def test_config2_rmse_within_1pct_of_reference():
     te = api.test_rmse(st, test)
     assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_dsgd_emulated_ranks_within_1pct(G):
+    """DSGD with G ranks emulated on one GPU -- the multi-GPU
+    algorithm minus the NCCL transport: strata sweeps + delta reductions of the
+    replicated parameters.  10 epochs on config 2 at 10% scale vs the
+    reference's own run."""
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_1708_08640_b200 import dsgd
+    ref = json.load(open(os.path.join(GOLDEN, "config2_s01_reference.json")))
+    b, test, _ = synth.generate(synth.config2(0.1))
+    cfg = TrainConfig(ranks=[10, 10, 10], seed=0, eta0=1e-3, mu=0.1, lambda_reg=0.01)
+    part = dsgd.partition(b, G)
+    ranks = [dsgd.RankState(part, p, cfg) for p in range(G)]
+    for _ in range(10):
+        dsgd.run_epoch_emulated(ranks)
+    models = [r.state.model for r in ranks]
+    for m in models[1:]:  # replicas agree after the end-of-epoch sync
+        np.testing.assert_allclose(m.core, models[0].core, rtol=0, atol=1e-6)
+    full = api.TrainState(cfg, b)
+    full.model = models[0]
+    tr = api.epoch_stats(full, 0.01).train_rmse
+    te = api.test_rmse(full, test)
+    assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
+    assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
