@@ -80,8 +80,8 @@ typedef struct cmtf_gpu_config {
                             (0.5), < 0 disables                         */
   float kappa;           /* damping of batched hot-row / core steps;
                             0 = default (0.5)                           */
-  int32_t flush_every;   /* sweep iterations between replica/core merges;
-                            0 = default (8)                             */
+  int32_t flush_every;   /* sweep iterations between hot-row replica
+                            merges; 0 = default (16)                    */
   int32_t kernel_version;/* 0 = auto (v2 where specialised), 1 = v1     */
   int32_t core_flush_every; /* sweep iterations between block-level core
                             pushes; 0 = default (1)                     */

@@ -868,7 +868,7 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     a.mnnz = ctx->mnnz;
   }
   if (a.nnz == 0 && a.mnnz == 0) return CMTF_OK;
-  const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 8;
+  const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 16;
   const double W = (double)ctx->v2_blocks * ctx->v2_nw * 32;
   // entries processed GPU-wide between two flushes of one warp: W * F * E
   const double win = W * F * ctx->v2_e;

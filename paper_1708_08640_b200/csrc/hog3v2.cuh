@@ -270,8 +270,15 @@ struct V2Layout {
 
 // Tensor-core core gradient of 32 staged entries (rows stg[0..32) of width
 // SW holding (-r u1, u2, u3)): dGw[ab][c] += sum_e u3_e[c] (-r u1)_e[a] u2_e[b].
+// SPLIT3 = 3xTF32 (hi*hi + hi*lo + lo*hi, ~fp32); otherwise the fp32 operand
+// registers are passed as tf32 (the tensor core reads the top 19 bits:
+// ~1e-3 relative per product on a block-summed gradient).
+#ifndef CMTF_CORE_SPLIT3
+#define CMTF_CORE_SPLIT3 0
+#endif
 template <int J, int JP, int SW, int AB, int NT, int MT>
 __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int g8, int t4) {
+  constexpr int NP = CMTF_CORE_SPLIT3 ? 3 : 1;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     uint32_t ah[4][4], al[4][4];
@@ -283,20 +290,27 @@ __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int 
       const float x1 = c1 < J ? stg[e0 * SW + 2 * JP + c1] : 0.f;
       const float x2 = c0 < J ? stg[e1 * SW + 2 * JP + c0] : 0.f;
       const float x3 = c1 < J ? stg[e1 * SW + 2 * JP + c1] : 0.f;
-      split_tf32(x0, ah[ks][0], al[ks][0]);
-      split_tf32(x1, ah[ks][1], al[ks][1]);
-      split_tf32(x2, ah[ks][2], al[ks][2]);
-      split_tf32(x3, ah[ks][3], al[ks][3]);
+      if (NP == 3) {
+        split_tf32(x0, ah[ks][0], al[ks][0]);
+        split_tf32(x1, ah[ks][1], al[ks][1]);
+        split_tf32(x2, ah[ks][2], al[ks][2]);
+        split_tf32(x3, ah[ks][3], al[ks][3]);
+      } else {
+        ah[ks][0] = __float_as_uint(x0);
+        ah[ks][1] = __float_as_uint(x1);
+        ah[ks][2] = __float_as_uint(x2);
+        ah[ks][3] = __float_as_uint(x3);
+      }
     }
 #pragma unroll 1
     for (int nt0 = 0; nt0 < NT; nt0 += 2) {
-      // two n-tiles per step, three independent accumulators each
-      // (hi*hi, hi*lo, lo*hi) so the HMMA chains are 4 deep, not 12
-      float d[2][3][4];
+      // two n-tiles per step; with the 3xTF32 split three independent
+      // accumulators each (hi*hi, hi*lo, lo*hi) so HMMA chains stay 4 deep
+      float d[2][NP][4];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < NP; ++p)
 #pragma unroll
           for (int q = 0; q < 4; ++q) d[j][p][q] = 0.f;
       int iaj[2], ibj[2];
@@ -317,11 +331,17 @@ __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int 
           const float q0 = okj[j] ? s0[iaj[j]] * s0[JP + ibj[j]] : 0.f;
           const float q1 = okj[j] ? s1[iaj[j]] * s1[JP + ibj[j]] : 0.f;
           uint32_t bh[2], bl[2];
-          split_tf32(q0, bh[0], bl[0]);
-          split_tf32(q1, bh[1], bl[1]);
-          mma_tf32(d[j][0], ah[ks], bh);
-          mma_tf32(d[j][1], ah[ks], bl);
-          mma_tf32(d[j][2], al[ks], bh);
+          if (NP == 3) {
+            split_tf32(q0, bh[0], bl[0]);
+            split_tf32(q1, bh[1], bl[1]);
+            mma_tf32(d[j][0], ah[ks], bh);
+            mma_tf32(d[j][NP > 1 ? 1 : 0], ah[ks], bl);
+            mma_tf32(d[j][NP > 2 ? 2 : 0], al[ks], bh);
+          } else {
+            bh[0] = __float_as_uint(q0);
+            bh[1] = __float_as_uint(q1);
+            mma_tf32(d[j][0], ah[ks], bh);
+          }
         }
       }
 #pragma unroll
@@ -329,7 +349,11 @@ __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int 
         if (nt0 + j >= NT) break;
         float dd[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dd[q] = d[j][0][q] + d[j][1][q] + d[j][2][q];
+        for (int q = 0; q < 4; ++q) {
+          dd[q] = d[j][0][q];
+#pragma unroll
+          for (int p = 1; p < NP; ++p) dd[q] += d[j][p][q];
+        }
         // dd: (c = mt*16+g8, ab' = nt*8+2t4 (+1)), (c+8, ...)
         const int abo = (nt0 + j) * 8 + 2 * t4;
         const int cr0 = mt * 16 + g8, cr1 = cr0 + 8;
@@ -545,16 +569,12 @@ hog3v2_kernel(Hog3v2Args a) {
           }
 #pragma unroll
           for (int j = 0; j < E; ++j) {
-            float t0 = 0.f, t1 = 0.f;
+            float tab = 0.f;
 #pragma unroll
-            for (int c = 0; c < J; ++c) {
-              if (c & 1) t1 = fmaf(gv[c], u3[j][c], t1);
-              else t0 = fmaf(gv[c], u3[j][c], t0);
-            }
+            for (int c = 0; c < J; ++c) tab = fmaf(gv[c], u3[j][c], tab);
             const float p = ua[j] * u2[j][ib];
 #pragma unroll
             for (int c = 0; c < J; ++c) g3[j][c] = fmaf(gv[c], p, g3[j][c]);
-            const float tab = t0 + t1;
             wsum[j] = fmaf(tab, u2[j][ib], wsum[j]);
             g2[j][ib] = fmaf(tab, ua[j], g2[j][ib]);
           }
@@ -746,8 +766,10 @@ hog3v2_kernel(Hog3v2Args a) {
       }
       __syncthreads();
     }
-    // ---- periodic hot-row merges (staggered across warps) ----
-    if ((it + 1 + (uint64_t)w) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
+    // ---- periodic hot-row merges: all warps in the same iteration, each a
+    // 1/NW share (the core push already aligns the warps; a staggered flush
+    // would make one warp late at every core-push barrier) ----
+    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
       flush_all_hot<J, JP, NW>(a, sm, w, lane);
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
