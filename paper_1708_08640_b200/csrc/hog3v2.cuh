@@ -470,6 +470,7 @@ hog3v2_kernel(Hog3v2Args a) {
   const uint64_t iters = (maxchunk + E - 1) / E;
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
+  uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
   float kw = 0.f;      // entries since the warp's last core flush (lane-local)
   float lamG = 0.f;    // sum |phi|^2 since the last flush (lane-local)
 
@@ -513,7 +514,9 @@ hog3v2_kernel(Hog3v2Args a) {
       const uint32_t nx[3] = {rc1[j].x, rc1[j].y, rc1[j].z};
 #pragma unroll
       for (int n = 0; n < 3; ++n) {
-        nsl[j][n] = (nxt && a.hot[n].slot) ? __ldg(a.hot[n].slot + nx[n]) : -1;
+        // no select on the loaded value (that would wait here); an invalid
+        // next entry is never used (`active` gates every use)
+        nsl[j][n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
         if (nxt) {
           const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
           asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -709,8 +712,10 @@ hog3v2_kernel(Hog3v2Args a) {
     {
       const uint64_t due = mlo + (mhi - mlo) * (it + 1) / iters;
       while (mpos < due) {
-        matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mphys(a, mpos)));
+        const uint4 mr = mrn;  // record prefetched one entry ahead
         ++mpos;
+        if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
+        matrix_entry<J, JP>(a, sm, mr);
       }
     }
 
@@ -774,8 +779,10 @@ hog3v2_kernel(Hog3v2Args a) {
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
   while (mpos < mhi) {
-    matrix_entry<J, JP>(a, sm, __ldg(a.mrec + mphys(a, mpos)));
+    const uint4 mr = mrn;
     ++mpos;
+    if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
+    matrix_entry<J, JP>(a, sm, mr);
   }
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);
