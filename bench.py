@@ -30,6 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP32_FMA_PER_SM_CLK = 128  # Blackwell SM: 4 x 32 FP32 lanes
+CONFIG_INDEX = {"config1": "BASELINE configs[0]", "config2": "BASELINE configs[1]",
+                "config3": "BASELINE configs[2]", "config4": "BASELINE configs[3]",
+                "config5": "BASELINE configs[4]"}
 
 
 def parse():
@@ -40,6 +43,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="config2")
     p.add_argument("--scale", type=float, default=1.0)
+    p.add_argument("--nnz", type=float, default=1e8, help="config5 tensor nonzeros")
+    p.add_argument("--rank", type=int, default=10, help="config5 rank")
     p.add_argument("--kernel", default="opt", choices=["opt", "naive"])
     p.add_argument("--hog-threads", type=int, default=0)
     p.add_argument("--order", default="random", choices=["sorted", "random"])
@@ -72,10 +77,31 @@ def make_workload(args):
     elif args.config == "config1":
         spec = synth.config1(literal=False)
         ranks, lr, lam = [5, 5, 5], 0.01, 0.01
+    elif args.config in ("config3", "config4", "config5"):
+        # device-side generation (1e8 - 1e9 nonzeros)
+        from paper_1708_08640_b200 import synth_gpu
+        if args.config == "config3":
+            spec = synth_gpu.config3(args.scale)
+        elif args.config == "config4":
+            spec = synth_gpu.config4(args.scale)
+        else:
+            spec = synth_gpu.config5(args.nnz, args.rank)
+        bundle, test = synth_gpu.generate(spec, device=f"cuda:{dist_env()[2]}")
+        return spec, bundle, test, list(spec.ranks), 1e-3, 0.01
     else:
         raise SystemExit(f"unknown config {args.config}")
     bundle, test, _ = synth.generate(spec)
     return spec, bundle, test, ranks, lr, lam
+
+
+def host_bundle(bundle, lo=0, hi=None):
+    """Host (numpy) view of a possibly device-resident bundle (prefix sample)."""
+    from paper_1708_08640_b200.api import DataBundle
+    if hasattr(bundle.tensor, "to_host"):
+        t = bundle.tensor.to_host(lo, hi)
+        frac = (t.nnz / bundle.tensor.nnz) if bundle.tensor.nnz else 1.0
+        return DataBundle(t, [m.to_host(0, int(m.nnz * frac)) for m in bundle.matrices])
+    return bundle
 
 
 def algorithmic(bundle, ranks):
@@ -137,6 +163,7 @@ def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None
     fraction of every coupled matrix."""
     from oracle import oracle as O
     from paper_1708_08640_b200.api import CoupledMatrix, DataBundle, SparseTensor
+    bundle = host_bundle(bundle, 0, min(sample, bundle.tensor.nnz))
     t = bundle.tensor
     frac = min(1.0, sample / t.nnz)
     st = SparseTensor(t.dims, t.indices[:sample], t.values[:sample])
@@ -174,7 +201,7 @@ def run_reference(args):
         "value": ups, "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * min(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE configs[1]) bounded sample",
+        "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}) bounded sample",
                    "sample_tensor_entries": min(args.cpu_sample, bundle.tensor.nnz),
                    "updates_per_step": n_upd, "ranks": ranks},
         "cpu_baseline": {"value": ups, "unit": "updates/s", "cores": cores,
@@ -244,7 +271,10 @@ def run_ours(args):
             "frac": achieved / peak_nominal, "traffic": None,
             "peak_source": f"nominal FP32: {sms} SMs x 128 FMA x 2 x 1965 MHz (no FP32 "
                            "entry in MEASURED_PEAKS.json)",
-            "kernel": "hog3_kernel (tensor sweep)", "kernel_ms": ten_ms,
+            "kernel": {"order3v2": "hog3v2_kernel (fused tensor+matrix epoch sweep)",
+                       "order3": "hog3_kernel (tensor sweep)",
+                       "generic": "hogwild_generic_kernel (tensor sweep)"}.get(info["kernel"]),
+            "kernel_ms": ten_ms,
             "flops_per_update": Ft, "bytes_per_update": Bt,
             "gather_gbs": bytes_t / (ten_ms * 1e-3) / 1e9,
             "frac_at_measured_clock": (achieved / fp32_peak_tflops(sms, clk["sm_mhz"])
@@ -264,7 +294,9 @@ def run_ours(args):
         "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE configs[1]), scale {args.scale}",
+        "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}), "
+                               f"scale {args.scale}" + (f", nnz {args.nnz:g}, rank {args.rank}"
+                                                         if args.config == "config5" else ""),
                    "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
                    "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
                    "hog_threads": info["hog_threads"], "tensor_kernel": info["kernel"],
@@ -287,14 +319,27 @@ def run_ours(args):
         from paper_1708_08640_b200.api import CoupledMatrix, DataBundle, SparseTensor
 
         def pinned(a):
+            if hasattr(a, "data_ptr"):  # device tensor: pinned host copy
+                return a.cpu().pin_memory()
             t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
             return t.numpy()
 
         t = bundle.tensor
-        pb = DataBundle(SparseTensor(t.dims, pinned(t.indices), pinned(t.values)),
-                        [CoupledMatrix(m.coupled_mode, m.rows, m.cols, pinned(m.indices),
-                                       pinned(m.values), m.weight) for m in bundle.matrices])
-        bundle = pb
+        if hasattr(t, "to_host"):
+            from paper_1708_08640_b200.synth_gpu import DeviceBundle, DeviceMatrix, DeviceTensor
+            pb = DeviceBundle(DeviceTensor(t.dims, pinned(t.indices), pinned(t.values)),
+                              [DeviceMatrix(m.coupled_mode, m.rows, m.cols, pinned(m.indices),
+                                            pinned(m.values), m.weight)
+                               for m in bundle.matrices])
+            h2d = pb.tensor.indices.nbytes + pb.tensor.values.nbytes + sum(
+                m.indices.nbytes + m.values.nbytes for m in pb.matrices)
+            bundle = pb
+        else:
+            pb = DataBundle(SparseTensor(t.dims, pinned(t.indices), pinned(t.values)),
+                            [CoupledMatrix(m.coupled_mode, m.rows, m.cols, pinned(m.indices),
+                                           pinned(m.values), m.weight)
+                             for m in bundle.matrices])
+            bundle = pb
         ts, parts = [], []
         for k in range(max(2, args.steps)):
             torch.cuda.synchronize()
@@ -394,7 +439,9 @@ def run_dsgd(args):
             "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} (BASELINE configs[1]), scale {args.scale}",
+            "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}), "
+                               f"scale {args.scale}" + (f", nnz {args.nnz:g}, rank {args.rank}"
+                                                         if args.config == "config5" else ""),
                        "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
                        "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
                        "parallelism": f"dsgd{world} (mode-1 x mode-2 strata, NCCL all-reduce "

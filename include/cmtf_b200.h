@@ -108,7 +108,8 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx *ctx);
  * count_mode_occurrences (src/sparse_data.cpp:344-362) are derived on the
  * device.  Range and finiteness are validated as check_entries
  * (src/sparse_data.cpp:19-64); duplicate detection is the caller's
- * (the reference rejects duplicates when the SparseTensor is constructed). */
+ * (the reference rejects duplicates when the SparseTensor is constructed).
+ * idx/vals may be host (pageable or pinned) or device pointers (UVA). */
 int cmtf_gpu_set_tensor(cmtf_gpu_ctx *ctx, const uint32_t *dims,
                         const uint32_t *idx, const double *vals, uint64_t nnz);
 int cmtf_gpu_add_matrix(cmtf_gpu_ctx *ctx, int32_t mode0, uint32_t rows,

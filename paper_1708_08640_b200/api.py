@@ -54,7 +54,11 @@ def _raise(rc: int, msg: str):
     raise cls(msg)
 
 
-def _ptr(a: np.ndarray, t):
+def _ptr(a, t):
+    """Pointer to a numpy array (host) or a contiguous torch tensor (host or
+    device; the C ABI resolves device pointers through UVA)."""
+    if hasattr(a, "data_ptr"):
+        return C.cast(C.c_void_p(a.data_ptr()), C.POINTER(t))
     return a.ctypes.data_as(C.POINTER(t))
 
 

@@ -1223,9 +1223,10 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   uint32_t* d_idx = ctx->s_idx;
   double* d_vals = ctx->s_vals;
   uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
-  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyHostToDevice,
+  // cudaMemcpyDefault: host (pageable or pinned) or device source (UVA)
+  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyDefault,
                      ctx->stream));
-  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault,
                      ctx->stream));
   for (int n = 0; n < N; ++n) {
     if (!same_shape || !ctx->count[n]) {
@@ -1356,9 +1357,9 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     uint32_t* d_idx = ctx->s_idx;
     double* d_vals = ctx->s_vals;
     uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
-    CU(cudaMemcpyAsync(d_idx, idx, nnz * 2 * sizeof(uint32_t), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(d_idx, idx, nnz * 2 * sizeof(uint32_t), cudaMemcpyDefault,
                        ctx->stream));
-    CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+    CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault,
                        ctx->stream));
     CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
     const int shuffled = ctx->cfg.order_policy == 1;
@@ -1851,9 +1852,10 @@ int cmtf_gpu_test_rmse(cmtf_gpu_ctx* ctx, const uint32_t* idx, const double* val
   TRY(dalloc(ctx, &d_rec, nnz * (N + 1)));
   TRY(dalloc(ctx, &d_keys, nnz));
   TRY(dalloc(ctx, &d_ids, nnz));
-  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyHostToDevice,
+  // cudaMemcpyDefault: host (pageable or pinned) or device source (UVA)
+  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyDefault,
                      ctx->stream));
-  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyHostToDevice,
+  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault,
                      ctx->stream));
   // counts of a test tensor must not touch the training counts: use scratch
   std::vector<uint32_t*> scratch(N, nullptr);
