@@ -78,8 +78,11 @@ typedef struct cmtf_gpu_config {
                             (count * workers / nnz) reach hot_tau get a
                             per-block shared-memory replica; 0 = default
                             (0.5), < 0 disables                         */
-  float kappa;           /* damping of batched hot-row / core steps;
-                            0 = default (0.5)                           */
+  float kappa;           /* damping of the merged hot-row replica steps:
+                            alpha = kappa / (kappa + q), q = (n_other /
+                            cnt) * (1 - exp(-eta * sum|c|^2)), n_other =
+                            the row's expected concurrent updates in other
+                            blocks; 0 = default (0.5)                   */
   int32_t flush_every;   /* sweep iterations between hot-row replica
                             merges; 0 = default (16)                    */
   int32_t kernel_version;/* 0 = auto (v2 where specialised), 1 = v1     */

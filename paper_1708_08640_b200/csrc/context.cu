@@ -4,7 +4,8 @@
 // trainer (/root/reference/proj/core/src/trainer.cpp) and is native C++;
 // every O(nnz) step runs on the device.
 #include <cub/device/device_radix_sort.cuh>
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is resolved at run time (nccl_api)
 
 #include <algorithm>
 #include <chrono>
@@ -23,10 +24,56 @@
 #include "generic.cuh"
 #include "hog3.cuh"
 #include "hog3v2.cuh"
+#include "hog4.cuh"
 
 using namespace cmtfb;
 
 namespace {
+
+// NCCL is resolved on first use (dlopen), never at load time: the process's
+// NCCL is whichever libnccl.so.2 is already mapped (PyTorch's bundled copy
+// when torch is imported first), else the CMTF_NCCL_LIB path, else the
+// system library.  Linking it would map the system NCCL at import and break
+// a later `import torch` that needs a newer NCCL.
+struct NcclApi {
+  bool tried = false;
+  std::string error;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) {
+    if (const char* p = std::getenv("CMTF_NCCL_LIB")) h = dlopen(p, RTLD_NOW);
+  }
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+  if (!h) {
+    api.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return api;
+  }
+  api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+  api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+  api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+  api.getErrorString =
+      reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+  if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.allReduce ||
+      !api.getErrorString) {
+    api.error = "libnccl.so.2 lacks a required symbol";
+    api.getUniqueId = nullptr;
+  }
+  return api;
+}
+
 
 thread_local std::string g_last_error;
 
@@ -491,7 +538,14 @@ int tensor_sse(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
   const uint64_t nb = (nnz + kEvalBlock - 1) / kEvalBlock;
   TRY(ensure_partials(ctx, nb));
   int J = 0;
-  if (fast3_supported(ctx, &J)) {
+  if (ctx->order == 4 && ctx->ranks[0] == 8 && ctx->ranks[1] == 8 && ctx->ranks[2] == 8 &&
+      ctx->ranks[3] == 8 && !ctx->cfg.force_generic) {
+    const size_t smem = sizeof(float) * 8 * 8 * 8 * 8;
+    eval4_kernel<<<(unsigned)nb, 256, smem, ctx->stream>>>(rec, nnz, ctx->U[0], ctx->U[1],
+                                                           ctx->U[2], ctx->U[3], ctx->G,
+                                                           ctx->d_partial);
+    CU(cudaGetLastError());
+  } else if (fast3_supported(ctx, &J)) {
     switch (J) {
       case 2: TRY(launch_eval3_t<2>(ctx, rec, nnz, ctx->d_partial)); break;
       case 4: TRY(launch_eval3_t<4>(ctx, rec, nnz, ctx->d_partial)); break;
@@ -708,8 +762,9 @@ size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const uint32_t JP = (uint32_t)round_up4(J);
+  const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
-  const V2Shape sh = v2_shape(ctx);
+  const V2Shape sh = four ? V2Shape{8, 1} : v2_shape(ctx);
   const int NW = sh.nw;
   ctx->v2_nw = NW;
   ctx->v2_e = sh.e;
@@ -717,9 +772,12 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   if (ctx->cfg.hog_threads > 0) blocks = std::max(1, ctx->cfg.hog_threads / (NW * 32));
   else {
     // auto: at least ~112 entries per worker slot per epoch (at most ~1/112
-    // of the data in flight), so small problems stay close to sequential
-    // SGD while large ones fill every SM
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (112ull * NW * 32 * sh.e));
+    // of the data in flight; 1/1024 for order 4, whose 8^4 core and four
+    // factor rows per entry make stale reads costlier: measured on
+    // synth.config4_small), so small problems stay close to sequential SGD
+    // while large ones fill every SM
+    const uint64_t per_slot = four ? 1024 : 112;
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (per_slot * NW * 32 * sh.e));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->v2_blocks = blocks;
@@ -755,7 +813,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
-  const size_t fixed = v2_fixed_bytes_rt(J, sh);
+  const size_t fixed = four ? sizeof(float) * (size_t)V4Layout<8, 8>::FIXED_FLOATS
+                            : v2_fixed_bytes_rt(J, sh);
   const size_t limit = 227 * 1024 - 1024;
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   struct Cand {
@@ -843,13 +902,12 @@ int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
   return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
-// One v2 sweep over tensor records [t_lo, t_hi) and matrix records
-// [m_lo[m], m_hi[m]) (NULL ranges = every matrix entry).
-int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
-             const uint64_t* m_lo, const uint64_t* m_hi) {
-  if (ctx->v2_dirty) TRY(prepare_v2(ctx, J));
-  Hog3v2Args a{};
-  a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
+// Fill the sweep arguments shared by hog3v2 and hog4 for tensor records
+// [t_lo, t_hi) and matrix records [m_lo[m], m_hi[m]) (NULL ranges = every
+// matrix entry).  Returns false when there is nothing to sweep.
+template <int NM, class Args>
+bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint64_t t_hi,
+                     const uint64_t* m_lo, const uint64_t* m_hi) {
   a.nnz = t_hi - t_lo;
   a.mrec = ctx->mrec;
   a.n_mat = (int)ctx->mats.size();
@@ -867,11 +925,12 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     a.mr_n[0] = ctx->mnnz;
     a.mnnz = ctx->mnnz;
   }
-  if (a.nnz == 0 && a.mnnz == 0) return CMTF_OK;
+  if (a.nnz == 0 && a.mnnz == 0) return false;
   const int F = ctx->cfg.flush_every > 0 ? ctx->cfg.flush_every : 16;
   const double W = (double)ctx->v2_blocks * ctx->v2_nw * 32;
   // entries processed GPU-wide between two flushes of one warp: W * F * E
-  const double win = W * F * ctx->v2_e;
+  // (an epoch shorter than one window: every row gets at most its count)
+  const double win = std::min(W * F * ctx->v2_e, (double)std::max<uint64_t>(1, ctx->nnz));
   const float nhat_scale = (float)(win / (double)std::max<uint64_t>(1, ctx->nnz));
   auto hd = [&](const cmtf_gpu_ctx::HotHost& h, const uint32_t* count, bool shared) {
     HotDesc d{};
@@ -886,7 +945,7 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     d.nhat_scale = nhat_scale * (shared ? (float)ctx->world : 1.f);
     return d;
   };
-  for (int n = 0; n < 3; ++n) {
+  for (int n = 0; n < NM; ++n) {
     a.U[n] = ctx->U[n];
     a.reg[n] = ctx->reg[n];
     a.hot[n] = hd(ctx->hot[n], ctx->count[n], (ctx->shared_modes >> n) & 1u);
@@ -910,8 +969,18 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   a.flush_every = F;
   a.core_every = FG;
   a.nonneg = ctx->cfg.nonnegative;
-  ctx->kernel_which = 3;
   ctx->hog_threads_used = (int)W;
+  return true;
+}
+
+// One v2 sweep (order 3) over a tensor range and matrix ranges.
+int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
+             const uint64_t* m_lo, const uint64_t* m_hi) {
+  if (ctx->v2_dirty) TRY(prepare_v2(ctx, J));
+  Hog3v2Args a{};
+  a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
+  if (!fill_sweep_args<3>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
+  ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
 #define V2_CASE(JV)                                                            \
   case JV:                                                                     \
@@ -921,6 +990,34 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   }
 #undef V2_CASE
   return set_err(ctx, CMTF_EUNSUPPORTED, "no v2 kernel for J=%d", J);
+}
+
+// order 4, all ranks 8 (BASELINE configs[3])
+bool v4_supported(const cmtf_gpu_ctx* ctx) {
+  if (ctx->order != 4 || ctx->cfg.force_generic || ctx->cfg.kernel_version == 1) return false;
+  for (int n = 0; n < 4; ++n)
+    if (ctx->ranks[n] != 8) return false;
+  return ctx->mats.size() <= (size_t)kV2MaxMats;
+}
+
+template <bool OPT>
+int launch_v4(cmtf_gpu_ctx* ctx, const Hog4Args& args) {
+  auto kern = hog4_kernel<8, OPT, 8>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->v2_smem));
+  kern<<<ctx->v2_blocks, 8 * 32, ctx->v2_smem, ctx->stream>>>(args);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+int v4_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
+             const uint64_t* m_hi) {
+  if (ctx->v2_dirty) TRY(prepare_v2(ctx, 8));
+  Hog4Args a{};
+  a.rec = ctx->rec + t_lo * 5;
+  if (!fill_sweep_args<4>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
+  ctx->kernel_which = 2;
+  return ctx->cfg.kernel == CMTF_KERNEL_OPT ? launch_v4<true>(ctx, a) : launch_v4<false>(ctx, a);
 }
 
 int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi) {
@@ -1169,7 +1266,7 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   for (auto& b : ctx->baseV) dfree(b);
   dfree(ctx->baseG);
   dfree(ctx->sync_buf);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm) nccl_api().commDestroy(ctx->comm);
   for (auto& h : ctx->hot) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   for (auto& h : ctx->hotV) { dfree(h.slot); dfree(h.row_of); dfree(h.base); }
   dfree(ctx->G);
@@ -1524,6 +1621,13 @@ int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
     return CMTF_OK;
   }
   int J = 0;
+  if (v4_supported(ctx)) {
+    TRY(v4_sweep(ctx, eta, t_lo, t_hi, m_lo, m_hi));  // + interleaved matrices
+    ctx->last_launches += 1;
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    return CMTF_OK;
+  }
   if (v2_supported(ctx, &J)) {
     TRY(v2_sweep(ctx, J, eta, t_lo, t_hi, m_lo, m_hi));  // + interleaved matrices
     ctx->last_launches += 1;
@@ -1718,10 +1822,12 @@ std::vector<SyncArr> sync_arrays(cmtf_gpu_ctx* ctx, uint32_t mode_mask, uint32_t
 extern "C" {
 
 int cmtf_gpu_comm_unique_id(void* id_out) {
+  NcclApi& N = nccl_api();
+  if (!N.getUniqueId) return set_err(nullptr, CMTF_ENCCL, "%s", N.error.c_str());
   ncclUniqueId id;
-  ncclResult_t r = ncclGetUniqueId(&id);
+  ncclResult_t r = N.getUniqueId(&id);
   if (r != ncclSuccess)
-    return set_err(nullptr, CMTF_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    return set_err(nullptr, CMTF_ENCCL, "ncclGetUniqueId: %s", N.getErrorString(r));
   std::memcpy(id_out, &id, sizeof id);
   return CMTF_OK;
 }
@@ -1729,13 +1835,15 @@ int cmtf_gpu_comm_unique_id(void* id_out) {
 int cmtf_gpu_comm_init(cmtf_gpu_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id) {
   if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
   CU(cudaSetDevice(ctx->device));
+  NcclApi& N = nccl_api();
+  if (!N.getUniqueId) return set_err(ctx, CMTF_ENCCL, "%s", N.error.c_str());
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof id);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm) N.commDestroy(ctx->comm);
   ctx->comm = nullptr;
-  ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+  ncclResult_t r = N.commInitRank(&ctx->comm, nranks, id, rank);
   if (r != ncclSuccess)
-    return set_err(ctx, CMTF_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    return set_err(ctx, CMTF_ENCCL, "ncclCommInitRank: %s", N.getErrorString(r));
   return CMTF_OK;
 }
 
@@ -1754,10 +1862,11 @@ int cmtf_gpu_sync(cmtf_gpu_ctx* ctx, uint32_t mode_mask, uint32_t mat_mask, int3
   }
   CU(cudaGetLastError());
   if (ctx->comm && total) {
-    ncclResult_t r = ncclAllReduce(ctx->sync_buf, ctx->sync_buf, total, ncclFloat, ncclSum,
-                                   ctx->comm, ctx->stream);
+    NcclApi& N = nccl_api();
+    ncclResult_t r = N.allReduce(ctx->sync_buf, ctx->sync_buf, total, ncclFloat, ncclSum,
+                                 ctx->comm, ctx->stream);
     if (r != ncclSuccess)
-      return set_err(ctx, CMTF_ENCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+      return set_err(ctx, CMTF_ENCCL, "ncclAllReduce: %s", N.getErrorString(r));
   }
   off = 0;
   for (auto& s : arrs) {

@@ -190,6 +190,91 @@ __device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* 
   }
 }
 
+#ifndef CMTF_WARP_AGG
+#define CMTF_WARP_AGG 0  // measured: +5% epoch time, DSGD unstable
+#endif
+// Tree sum of x[0..N) over the lanes of `peers` (the lanes sharing a key);
+// the lowest lane of every group ends with its group's sum.  All 32 lanes
+// call it; log2(largest group) rounds of N shuffles.
+template <int N>
+__device__ __forceinline__ void reduce_peers(unsigned peers, float* x, int lane) {
+  unsigned rel = __popc(peers & ((1u << lane) - 1u));  // my rank in the group
+  unsigned above = peers & (0xfffffffeu << lane);
+  while (__any_sync(0xffffffffu, above != 0u)) {
+    const int next = __ffs(above);  // next remaining group member above me
+    const int src = next ? next - 1 : lane;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const float t = __shfl_sync(0xffffffffu, x[k], src);
+      if (next) x[k] += t;
+    }
+    above &= __ballot_sync(0xffffffffu, !(rel & 1u));  // odd ranks are consumed
+    rel >>= 1;
+  }
+}
+
+// Warp-cooperative row step (all 32 lanes call; `act`: this lane steps a
+// row).  Cold rows: plain store (as step_row).  Hot rows: the lanes stepping
+// the same replica row in this instruction first sum their deltas and
+// curvature stats, and the group's lowest lane applies the sum, so no update
+// is lost to an intra-warp write collision on the replica.  `key` is the
+// replica row's shared-memory offset (unique across modes and matrices).
+template <int J, int JP>
+__device__ __forceinline__ void step_row_warp(float* U, uint32_t i, int slot, float* rep,
+                                              float* stat, int key_base, bool act,
+                                              const float* u, const float* grad, float eta,
+                                              int nonneg, float curv, int lane) {
+#if CMTF_WARP_AGG
+  if (act && slot < 0) step_row<J, JP>(U, i, -1, rep, stat, u, grad, eta, nonneg, curv);
+  const bool hot = act && slot >= 0;
+  if (!__any_sync(0xffffffffu, hot)) return;
+  const int key = hot ? key_base + slot * JP : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  float v[J + 1];
+#pragma unroll
+  for (int k = 0; k < J; ++k) v[k] = grad[k];
+  v[J] = curv;
+  reduce_peers<J + 1>(peers, v, lane);
+  if (hot && __ffs(peers) - 1 == lane) {
+    // n steps taken from one point: the summed step overshoots the n
+    // sequential steps it stands for once eta * sum|c|^2 is not small; scale
+    // it to the sequential gain along the curvature, 1 - (1 - x/n)^n over x
+    // (x = eta * sum|c|^2; exactly 1 for n = 1)
+    const int n = __popc(peers);
+    float sc = 1.f;
+    if (n > 1) {
+      const float x = eta * v[J];
+      const float b = fmaxf(0.f, 1.f - x / (float)n);
+      if (x > 1e-6f) sc = (1.f - __powf(b, (float)n)) / x;
+    }
+    const float es = -eta * sc;
+    float* rp = rep + slot * JP;
+#pragma unroll
+    for (int k = 0; k < JP; k += 4) {
+      float4 cur = *reinterpret_cast<float4*>(rp + k);
+      cur.x += k + 0 < J ? es * v[k + 0] : 0.f;
+      cur.y += k + 1 < J ? es * v[k + 1] : 0.f;
+      cur.z += k + 2 < J ? es * v[k + 2] : 0.f;
+      cur.w += k + 3 < J ? es * v[k + 3] : 0.f;
+      if (nonneg) {
+        cur.x = fmaxf(cur.x, 0.f); cur.y = fmaxf(cur.y, 0.f);
+        cur.z = fmaxf(cur.z, 0.f); cur.w = fmaxf(cur.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(rp + k) = cur;
+    }
+    stat[3 * slot] += v[J];
+    atomicAdd(reinterpret_cast<int*>(stat) + 3 * slot + 1, n);
+  }
+#else
+  (void)key_base;
+  (void)lane;
+  if (act) step_row<J, JP>(U, i, slot, rep, stat, u, grad, eta, nonneg, curv);
+#endif
+}
+
+#ifndef CMTF_SAT_GAIN
+#define CMTF_SAT_GAIN 1
+#endif
 // Push the block's progress on hot rows [r0, r1) to global and re-base.
 // stat row layout: {sum |c|^2, observation count (int), n_hat}.  All loads
 // of a row are independent and issued together; the new base is the global
@@ -213,9 +298,17 @@ __device__ void flush_hot(const HotDesc& h, float* U, float* rep, float* stat, f
     stat[3 * s] = 0.f;
     float alpha = 0.f;
     if (cnt > 0.f) {
-      const float nhat = fmaxf(cnt, stat[3 * s + 2]);
-      const float q = eta * (lam / cnt) * nhat;
-      alpha = q > kappa ? kappa / q : 1.f;
+      // This block's delta is cnt sequential steps of size ~eta * lam_hat:
+      // its gain along the row's curvature saturates at 1 (the block's local
+      // optimum).  The merge adds the deltas of the other blocks taken from
+      // the same base, n_other / cnt of them (n_other: expected updates of the
+      // row GPU-wide in one window minus this block's share), so the merged
+      // step is damped by 1 / (1 + q / kappa), q = (n_other / cnt) * gain:
+      // alpha = 1 without concurrency, ~kappa / q under heavy contention.
+      const float n_other = stat[3 * s + 2] * (1.f - 1.f / (float)gridDim.x);
+      const float gain = CMTF_SAT_GAIN ? -expm1f(-eta * lam) : eta * lam;
+      const float q = (n_other / cnt) * gain;
+      alpha = kappa / (kappa + q);
     }
 #pragma unroll
     for (int k = 0; k < JP / 4; ++k) {
@@ -371,7 +464,8 @@ __device__ __forceinline__ void core_grad_mma(const float* stg, float* dGw, int 
 }
 
 // virtual index over the swept matrix ranges -> physical record index
-__device__ __forceinline__ uint64_t mphys(const Hog3v2Args& a, uint64_t k) {
+template <class Args>
+__device__ __forceinline__ uint64_t mphys(const Args& a, uint64_t k) {
   for (int r = 0; r < a.n_mr; ++r) {
     if (k < a.mr_n[r]) return a.mr_lo[r] + k;
     k -= a.mr_n[r];
@@ -379,18 +473,25 @@ __device__ __forceinline__ uint64_t mphys(const Hog3v2Args& a, uint64_t k) {
   return 0;
 }
 
-// One coupled-matrix entry (src/gradients.cpp:225-248; trainer.cpp:220-235).
-template <int J, int JP>
-__device__ __forceinline__ void matrix_entry(const Hog3v2Args& a, float* sm, const uint4 mr) {
-  const MatDesc3& M = a.mats[mr.w];
+// One coupled-matrix entry per lane (src/gradients.cpp:225-248;
+// trainer.cpp:220-235); all 32 lanes call, `has` = this lane has an entry.
+template <int J, int JP, class Args>
+__device__ __forceinline__ void matrix_entry(const Args& a, float* sm, const uint4 mr, bool has,
+                                             int lane) {
+  const MatDesc3& M = a.mats[has ? mr.w : 0];
   const int mode = M.mode;
-  const int su = a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
-  const int sv = M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
+  const int su = has && a.hot[mode].slot ? __ldg(a.hot[mode].slot + mr.x) : -1;
+  const int sv = has && M.hotV.slot ? __ldg(M.hotV.slot + mr.y) : -1;
   float uu[JP], vv[JP];
   float* repU = sm + a.hot[mode].off;
   float* repV = sm + M.hotV.off;
-  load_row<JP>(a.U[mode], mr.x, su, repU, uu);
-  load_row<JP>(M.V, mr.y, sv, repV, vv);
+  if (has) {
+    load_row<JP>(a.U[mode], mr.x, su, repU, uu);
+    load_row<JP>(M.V, mr.y, sv, repV, vv);
+  } else {
+#pragma unroll
+    for (int k = 0; k < JP; ++k) uu[k] = vv[k] = 0.f;
+  }
   float yh = 0.f, nu = 0.f, nv = 0.f;
 #pragma unroll
   for (int k = 0; k < J; ++k) {
@@ -398,24 +499,40 @@ __device__ __forceinline__ void matrix_entry(const Hog3v2Args& a, float* sm, con
     nu = fmaf(uu[k], uu[k], nu);
     nv = fmaf(vv[k], vv[k], nv);
   }
-  const float rr = __uint_as_float(mr.z) - yh;
-  const float vr = __ldg(M.vreg + mr.y);
+  const float rr = has ? __uint_as_float(mr.z) - yh : 0.f;
+  const float vr = has ? __ldg(M.vreg + mr.y) : 0.f;
   float du[J], dv[J];
 #pragma unroll
   for (int k = 0; k < J; ++k) {
     du[k] = -M.weight * rr * vv[k];
     dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
   }
-  step_row<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off, uu, du, a.eta,
-                  a.nonneg, M.weight * nv);
-  step_row<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, vv, dv, a.eta, a.nonneg,
-                  M.weight * nu);
+  step_row_warp<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off,
+                       (int)a.hot[mode].off, has, uu, du, a.eta, a.nonneg, M.weight * nv, lane);
+  step_row_warp<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, (int)M.hotV.off, has, vv, dv,
+                       a.eta, a.nonneg, M.weight * nu, lane);
 }
 
-template <int J, int JP, int NW>
-__device__ __forceinline__ void flush_all_hot(const Hog3v2Args& a, float* sm, int w, int lane) {
+// Matrix entries of this lane up to `due`, in lockstep across the warp.
+template <int J, int JP, class Args>
+__device__ __forceinline__ void matrix_entries_until(const Args& a, float* sm, uint64_t& mpos,
+                                                     uint4& mrn, uint64_t due, uint64_t mhi,
+                                                     int lane) {
+  while (__any_sync(0xffffffffu, mpos < due)) {
+    const bool has = mpos < due;
+    const uint4 mr = mrn;  // record prefetched one entry ahead
+    if (has) {
+      ++mpos;
+      if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
+    }
+    matrix_entry<J, JP>(a, sm, mr, has, lane);
+  }
+}
+
+template <int J, int JP, int NW, int NM = 3, class Args>
+__device__ __forceinline__ void flush_all_hot(const Args& a, float* sm, int w, int lane) {
 #pragma unroll
-  for (int n = 0; n < 3; ++n) {
+  for (int n = 0; n < NM; ++n) {
     const HotDesc& h = a.hot[n];
     if (h.H) {
       const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
@@ -665,31 +782,32 @@ hog3v2_kernel(Hog3v2Args a) {
 #pragma unroll
       for (int k = 0; k < J; ++k) w1[k] = myst[JP + k];
       const float r = active[j] ? __uint_as_float(rc[j].w) - xh[j] : 0.f;
-      if (active[j]) {
-        float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+      float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
 #pragma unroll
-        for (int k = 0; k < J; ++k) {
-          n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[j][k], u2[j][k], n2);
-          n3 = fmaf(u3[j][k], u3[j][k], n3);
-          c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[j][k], g2[j][k], c2);
-          c3 = fmaf(g3[j][k], g3[j][k], c3);
-        }
+      for (int k = 0; k < J; ++k) {
+        n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[j][k], u2[j][k], n2);
+        n3 = fmaf(u3[j][k], u3[j][k], n3);
+        c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[j][k], g2[j][k], c2);
+        c3 = fmaf(g3[j][k], g3[j][k], c3);
+      }
+      if (active[j]) {
         lamG += n1 * n2 * n3;
         kw += 1.f;
-        float gr[J];
-#pragma unroll
-        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1[j] * u1[k]);
-        step_row<J, JP>(a.U[0], rc[j].x, sl[j][0], const_cast<float*>(rep[0]), stat[0], u1, gr,
-                        a.eta, a.nonneg, c1);
-#pragma unroll
-        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[j][k], reg2[j] * u2[j][k]);
-        step_row<J, JP>(a.U[1], rc[j].y, sl[j][1], const_cast<float*>(rep[1]), stat[1], u2[j],
-                        gr, a.eta, a.nonneg, c2);
-#pragma unroll
-        for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[j][k], reg3[j] * u3[j][k]);
-        step_row<J, JP>(a.U[2], rc[j].z, sl[j][2], const_cast<float*>(rep[2]), stat[2], u3[j],
-                        gr, a.eta, a.nonneg, c3);
       }
+      // row steps: every lane of the warp takes part (hot-row aggregation)
+      float gr[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1[j] * u1[k]);
+      step_row_warp<J, JP>(a.U[0], rc[j].x, sl[j][0], const_cast<float*>(rep[0]), stat[0],
+                           (int)a.hot[0].off, active[j], u1, gr, a.eta, a.nonneg, c1, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[j][k], reg2[j] * u2[j][k]);
+      step_row_warp<J, JP>(a.U[1], rc[j].y, sl[j][1], const_cast<float*>(rep[1]), stat[1],
+                           (int)a.hot[1].off, active[j], u2[j], gr, a.eta, a.nonneg, c2, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[j][k], reg3[j] * u3[j][k]);
+      step_row_warp<J, JP>(a.U[2], rc[j].z, sl[j][2], const_cast<float*>(rep[2]), stat[2],
+                           (int)a.hot[2].off, active[j], u3[j], gr, a.eta, a.nonneg, c3, lane);
       // stage (-r u1, u2, u3) at pre-update values (zeros for idle lanes)
 #pragma unroll
       for (int k = 0; k < JP; k += 4) {
@@ -709,15 +827,8 @@ hog3v2_kernel(Hog3v2Args a) {
       core_grad_mma<J, JP, SW, AB, L::NT, L::MT>(stg + j * 32 * SW, dGw, g8, t4);
 
     // ---- matrix entries due by this iteration (interleaved) ----
-    {
-      const uint64_t due = mlo + (mhi - mlo) * (it + 1) / iters;
-      while (mpos < due) {
-        const uint4 mr = mrn;  // record prefetched one entry ahead
-        ++mpos;
-        if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
-        matrix_entry<J, JP>(a, sm, mr);
-      }
-    }
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
+                                lane);
 
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -778,12 +889,7 @@ hog3v2_kernel(Hog3v2Args a) {
       flush_all_hot<J, JP, NW>(a, sm, w, lane);
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
-  while (mpos < mhi) {
-    const uint4 mr = mrn;
-    ++mpos;
-    if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
-    matrix_entry<J, JP>(a, sm, mr);
-  }
+  matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);
 }

@@ -1,0 +1,476 @@
+// hog4.cuh -- order-4 S^3CMTF epoch kernel for J = 8 (BASELINE configs[3]:
+// 4-way tensor, 8^4 core, two coupled matrices).
+//
+// Same execution model as hog3v2 (one launch per epoch, a contiguous chunk
+// of the randomly permuted COO per lane, interleaved matrix entries, hot-row
+// shared-memory replicas with damped merges, relaxed Hogwild on cold rows),
+// with the order-4 specifics:
+//
+// * sweep (Algorithm 3 reuse, src/gradients.cpp:150-206 restated): for every
+//   core row (a,b,c) one pair of broadcast LDS.128 of G[a,b,c,0:8] feeds
+//   t = G.u4 (8 FMA) and g4 += G * (u1[a]u2[b]u3[c]) (8 FMA); then
+//   s_ab += t u3[c], g3[c] += t u1[a]u2[b]; per (a,b): W1[a] += s_ab u2[b],
+//   g2[b] += s_ab u1[a].  The a-loop is rolled (u1 and W1 live in the lane's
+//   staging row) so the unrolled b,c,d body fits the instruction cache.
+// * core gradient dG[a,b,c,d] = sum_e -r_e u1[a]u2[b]u3[c]u4[d] on the
+//   tensor cores, block-wide: each lane stages (-r u1, u2, u3, u4), and after
+//   a block barrier warp w (NW = J = 8) computes the slab a = w over all 256
+//   staged entries: D[d][(b,c)] = sum_e u4_e[d] * Q_e[(b,c)] with
+//   Q_e[(b,c)] = (-r u1_e[w]) u2_e[b] u3_e[c], mma.sync m16n8k8 TF32 with
+//   the n-tile = b and the 8 columns = c.  The 16 live accumulators per lane
+//   stay in registers until the (damped, block-level) core push, which also
+//   refreshes the shared core slab a = w from the global core.
+#pragma once
+
+#include "hog3v2.cuh"
+
+namespace cmtfb {
+
+struct Hog4Args {
+  const uint32_t* rec;  // tensor records (i1, i2, i3, i4, bits(x)), random order
+  uint64_t nnz;
+  const uint4* mrec;    // matrix records {row, col, bits(y), matrix id}
+  uint64_t mnnz;
+  int n_mr;
+  uint64_t mr_lo[kV2MaxMats];
+  uint64_t mr_n[kV2MaxMats];
+  int n_mat;
+  MatDesc3 mats[kV2MaxMats];
+  float* U[4];
+  const float* reg[4];
+  HotDesc hot[4];
+  float* G;
+  float eta;
+  float core_reg;
+  float kappa;
+  float kappa_core;
+  float nhat_core;
+  int flush_every;
+  int core_every;
+  int nonneg;
+};
+
+template <int J, int NW>
+struct V4Layout {
+  static_assert(J == 8 && NW == 8, "hog4 is specialised for J = 8 (one core slab per warp)");
+  static constexpr int JP = J;
+  static constexpr int ABC = J * J * J;           // core rows (a,b,c), d fastest
+  static constexpr int SW = 40;                   // >= 4*JP, == 8 (mod 32)
+  static constexpr int G_FLOATS = ABC * JP;       // 16 KB
+  static constexpr int STAGE_FLOATS = NW * 32 * SW;
+  static constexpr int FIXED_FLOATS = G_FLOATS + STAGE_FLOATS;
+};
+
+template <int J, bool OPT, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+hog4_kernel(Hog4Args a) {
+  using L = V4Layout<J, NW>;
+  constexpr int JP = L::JP;
+  constexpr int ABC = L::ABC;
+  constexpr int SW = L::SW;
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float red_kw[NW], red_lam[NW];
+  float* Gs = sm;
+  float* stg = sm + L::G_FLOATS;  // [NW*32][SW]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  float* myst = stg + (w * 32 + lane) * SW;
+
+  for (int q = threadIdx.x; q < ABC * JP; q += blockDim.x) Gs[q] = __ldcg(a.G + q);
+#pragma unroll
+  for (int n = 0; n < 4; ++n)
+    if (a.hot[n].H) load_hot<JP>(a.hot[n], a.U[n], sm + a.hot[n].off, sm + a.hot[n].stat_off);
+  for (int m = 0; m < a.n_mat; ++m)
+    if (a.mats[m].hotV.H)
+      load_hot<JP>(a.mats[m].hotV, a.mats[m].V, sm + a.mats[m].hotV.off,
+                   sm + a.mats[m].hotV.stat_off);
+  __syncthreads();
+
+  const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
+  const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
+  const uint64_t lo = a.nnz * gl / Wt, hi = a.nnz * (gl + 1) / Wt;
+  const uint64_t iters = (a.nnz + Wt - 1) / Wt;
+  const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
+  uint64_t mpos = mlo;
+  uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+  float kw = 0.f, lamG = 0.f;
+  float acc[J][2];  // dG[a=w][b][c=2t4 (+1)][d=g8] since the last push
+#pragma unroll
+  for (int i = 0; i < J; ++i) acc[i][0] = acc[i][1] = 0.f;
+
+  const float* rep[4];
+  float* stat[4];
+#pragma unroll
+  for (int n = 0; n < 4; ++n) {
+    rep[n] = sm + a.hot[n].off;
+    stat[n] = sm + a.hot[n].stat_off;
+  }
+
+  // next entry's record and hot slots in flight while this one is computed
+  uint32_t nx[4] = {0, 0, 0, 0}, nxv = 0;
+  int nsl[4] = {-1, -1, -1, -1};
+  if (lo < hi) {
+#pragma unroll
+    for (int n = 0; n < 4; ++n) nx[n] = __ldg(a.rec + lo * 5 + n);
+    nxv = __ldg(a.rec + lo * 5 + 4);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + nx[n]) : -1;
+  }
+
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e = lo + it;
+    const bool active = e < hi;
+    uint32_t ix[4];
+    int sl[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      ix[n] = nx[n];
+      sl[n] = nsl[n];
+    }
+    const float x = __uint_as_float(nxv);
+    float u2[JP], u3[JP], u4[JP], reg[4];
+    {
+      float u1[JP];
+      if (active) {
+        load_row<JP>(a.U[0], ix[0], sl[0], rep[0], u1);
+        load_row<JP>(a.U[1], ix[1], sl[1], rep[1], u2);
+        load_row<JP>(a.U[2], ix[2], sl[2], rep[2], u3);
+        load_row<JP>(a.U[3], ix[3], sl[3], rep[3], u4);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) reg[n] = __ldg(a.reg[n] + ix[n]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < JP; ++k) u1[k] = u2[k] = u3[k] = u4[k] = 0.f;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) reg[n] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < JP; k += 4)
+        *reinterpret_cast<float4*>(myst + k) = make_float4(u1[k], u1[k + 1], u1[k + 2], u1[k + 3]);
+    }
+    // prefetch the next entry (record, hot slots, cold rows into L1)
+    if (e + 1 < hi) {
+#pragma unroll
+      for (int n = 0; n < 4; ++n) nx[n] = __ldg(a.rec + (e + 1) * 5 + n);
+      nxv = __ldg(a.rec + (e + 1) * 5 + 4);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + nx[n]) : -1;
+        const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+      }
+    }
+
+    float g2[J], g3[J], g4[J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) g2[k] = g3[k] = g4[k] = 0.f;
+    float xh = 0.f;
+    if (OPT) {
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {
+        const float ua = myst[ia];
+        const float* ga = Gs + ia * J * J * JP;
+        float wsum = 0.f;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib) {
+          const float pab = ua * u2[ib];
+          float sab = 0.f;
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            const float4 q0 = *reinterpret_cast<const float4*>(gr);
+            const float4 q1 = *reinterpret_cast<const float4*>(gr + 4);
+            const float gv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            float t = 0.f;
+#pragma unroll
+            for (int d = 0; d < J; ++d) t = fmaf(gv[d], u4[d], t);
+            const float pabc = pab * u3[ic];
+#pragma unroll
+            for (int d = 0; d < J; ++d) g4[d] = fmaf(gv[d], pabc, g4[d]);
+            sab = fmaf(t, u3[ic], sab);
+            g3[ic] = fmaf(t, pab, g3[ic]);
+          }
+          wsum = fmaf(sab, u2[ib], wsum);
+          g2[ib] = fmaf(sab, ua, g2[ib]);
+        }
+        myst[JP + ia] = wsum;
+        xh = fmaf(wsum, ua, xh);
+      }
+    } else {
+      // Algorithm 2: one walk for the prediction, then one per mode
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {
+        const float ua = myst[ia];
+        const float* ga = Gs + ia * J * J * JP;
+        float wsum = 0.f;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            float t = 0.f;
+#pragma unroll
+            for (int d = 0; d < J; ++d) t = fmaf(gr[d], u4[d], t);
+            wsum = fmaf(t, u2[ib] * u3[ic], wsum);
+          }
+        xh = fmaf(wsum, ua, xh);
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {  // mode 1
+        const float* ga = Gs + ia * J * J * JP;
+        float wsum = 0.f;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            float t = 0.f;
+#pragma unroll
+            for (int d = 0; d < J; ++d) t = fmaf(gr[d], u4[d], t);
+            wsum = fmaf(t, u2[ib] * u3[ic], wsum);
+          }
+        myst[JP + ia] = wsum;
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {  // mode 2
+        const float ua = myst[ia];
+        const float* ga = Gs + ia * J * J * JP;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            float t = 0.f;
+#pragma unroll
+            for (int d = 0; d < J; ++d) t = fmaf(gr[d], u4[d], t);
+            g2[ib] = fmaf(t, ua * u3[ic], g2[ib]);
+          }
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {  // mode 3
+        const float ua = myst[ia];
+        const float* ga = Gs + ia * J * J * JP;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            float t = 0.f;
+#pragma unroll
+            for (int d = 0; d < J; ++d) t = fmaf(gr[d], u4[d], t);
+            g3[ic] = fmaf(t, ua * u2[ib], g3[ic]);
+          }
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll 1
+      for (int ia = 0; ia < J; ++ia) {  // mode 4
+        const float ua = myst[ia];
+        const float* ga = Gs + ia * J * J * JP;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int ic = 0; ic < J; ++ic) {
+            const float* gr = ga + (ib * J + ic) * JP;
+            const float p = ua * u2[ib] * u3[ic];
+#pragma unroll
+            for (int d = 0; d < J; ++d) g4[d] = fmaf(gr[d], p, g4[d]);
+          }
+      }
+    }
+
+    // ---- residual, row steps, staging (-r u1, u2, u3, u4) ----
+    {
+      float u1[JP], w1[J];
+#pragma unroll
+      for (int k = 0; k < JP; ++k) u1[k] = myst[k];
+#pragma unroll
+      for (int k = 0; k < J; ++k) w1[k] = myst[JP + k];
+      const float r = active ? x - xh : 0.f;
+      float n1 = 0.f, n2 = 0.f, n3 = 0.f, n4 = 0.f;
+      float c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f;
+#pragma unroll
+      for (int k = 0; k < J; ++k) {
+        n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[k], u2[k], n2);
+        n3 = fmaf(u3[k], u3[k], n3); n4 = fmaf(u4[k], u4[k], n4);
+        c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[k], g2[k], c2);
+        c3 = fmaf(g3[k], g3[k], c3); c4 = fmaf(g4[k], g4[k], c4);
+      }
+      if (active) {
+        lamG += (n1 * n2) * (n3 * n4);
+        kw += 1.f;
+      }
+      // row steps: every lane of the warp takes part (hot-row aggregation)
+      float gr[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg[0] * u1[k]);
+      step_row_warp<J, JP>(a.U[0], ix[0], sl[0], const_cast<float*>(rep[0]), stat[0],
+                           (int)a.hot[0].off, active, u1, gr, a.eta, a.nonneg, c1, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], reg[1] * u2[k]);
+      step_row_warp<J, JP>(a.U[1], ix[1], sl[1], const_cast<float*>(rep[1]), stat[1],
+                           (int)a.hot[1].off, active, u2, gr, a.eta, a.nonneg, c2, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], reg[2] * u3[k]);
+      step_row_warp<J, JP>(a.U[2], ix[2], sl[2], const_cast<float*>(rep[2]), stat[2],
+                           (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g4[k], reg[3] * u4[k]);
+      step_row_warp<J, JP>(a.U[3], ix[3], sl[3], const_cast<float*>(rep[3]), stat[3],
+                           (int)a.hot[3].off, active, u4, gr, a.eta, a.nonneg, c4, lane);
+#pragma unroll
+      for (int k = 0; k < JP; k += 4) {
+        *reinterpret_cast<float4*>(myst + k) =
+            make_float4(-r * u1[k], -r * u1[k + 1], -r * u1[k + 2], -r * u1[k + 3]);
+        *reinterpret_cast<float4*>(myst + JP + k) = make_float4(u2[k], u2[k + 1], u2[k + 2], u2[k + 3]);
+        *reinterpret_cast<float4*>(myst + 2 * JP + k) =
+            make_float4(u3[k], u3[k + 1], u3[k + 2], u3[k + 3]);
+        *reinterpret_cast<float4*>(myst + 3 * JP + k) =
+            make_float4(u4[k], u4[k + 1], u4[k + 2], u4[k + 3]);
+      }
+    }
+    const bool push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
+    if (push) {
+      const float kws = warp_sum(kw);
+      const float lgs = warp_sum(lamG);
+      if (lane == 0) {
+        red_kw[w] = kws;
+        red_lam[w] = lgs;
+      }
+      kw = 0.f;
+      lamG = 0.f;
+    }
+    __syncthreads();  // (A) all NW*32 entries staged
+
+    // ---- core gradient slab a = w on the tensor cores (K = the block's entries) ----
+#pragma unroll 2
+    for (int ks = 0; ks < NW * 4; ++ks) {
+      const float* s0 = stg + (ks * 8 + t4) * SW;
+      const float* s1 = s0 + 4 * SW;
+      const float p0 = s0[w] * s0[2 * JP + g8];  // -r u1[a=w] u3[c=g8]
+      const float p1 = s1[w] * s1[2 * JP + g8];
+      uint32_t av[4];
+      av[0] = __float_as_uint(s0[3 * JP + g8]);  // A[d=g8][e0] = u4_e0[g8]
+      av[1] = 0u;
+      av[2] = __float_as_uint(s1[3 * JP + g8]);
+      av[3] = 0u;
+      const float4 b00 = *reinterpret_cast<const float4*>(s0 + JP);
+      const float4 b01 = *reinterpret_cast<const float4*>(s0 + JP + 4);
+      const float4 b10 = *reinterpret_cast<const float4*>(s1 + JP);
+      const float4 b11 = *reinterpret_cast<const float4*>(s1 + JP + 4);
+      const float v0[8] = {b00.x, b00.y, b00.z, b00.w, b01.x, b01.y, b01.z, b01.w};
+      const float v1[8] = {b10.x, b10.y, b10.z, b10.w, b11.x, b11.y, b11.z, b11.w};
+#pragma unroll
+      for (int ib = 0; ib < J; ++ib) {
+        uint32_t bv[2];
+        bv[0] = __float_as_uint(p0 * v0[ib]);  // B[e0][c=g8] = Q_e0[(ib, g8)]
+        bv[1] = __float_as_uint(p1 * v1[ib]);
+        float d[4] = {acc[ib][0], acc[ib][1], 0.f, 0.f};
+        mma_tf32(d, av, bv);
+        acc[ib][0] = d[0];  // D[d=g8][c=2t4], D[g8][2t4+1]
+        acc[ib][1] = d[1];
+      }
+    }
+
+    // ---- interleaved matrix entries ----
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
+                                lane);
+
+    // ---- damped block-level core push of slab a = w, refresh from global ----
+    if (push) {
+      float kb = 0.f, lb = 0.f;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        kb += red_kw[q];
+        lb += red_lam[q];
+      }
+      if (kb > 0.f) {
+        const float q = a.eta * (lb / kb) * a.nhat_core;
+        const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
+        const float s = -a.eta * alpha;
+        const float kr = kb * a.core_reg;
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = ((w * J + ib) * J + 2 * t4 + h) * JP + g8;
+            const float delta = s * fmaf(kr, Gs[o], acc[ib][h]);
+            float v = atomicAdd(a.G + o, delta) + delta;
+            if (a.nonneg) v = fmaxf(v, 0.f);
+            Gs[o] = v;
+            acc[ib][h] = 0.f;
+          }
+      }
+    }
+    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
+      flush_all_hot<J, JP, NW, 4>(a, sm, w, lane);
+    __syncthreads();  // (B) core slabs refreshed, staging consumed
+  }
+  matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
+  __syncthreads();
+  flush_all_hot<J, JP, NW, 4>(a, sm, w, lane);
+}
+
+// Eval pass for order 4, J = 8: thread per entry, fixed kEvalBlock-entry
+// blocks (src/eval.cpp:10-65), double accumulation, deterministic order.
+__global__ void __launch_bounds__(256)
+eval4_kernel(const uint32_t* rec, uint64_t nnz, const float* U1, const float* U2,
+             const float* U3, const float* U4, const float* G, double* partial) {
+  constexpr int J = 8, BT = 256;
+  extern __shared__ __align__(16) float sm[];
+  float* Gs = sm;  // [abc][d]
+  __shared__ double acc_s[BT / 32];
+  const int t = threadIdx.x;
+  for (int q = t; q < J * J * J * J; q += BT) Gs[q] = G[q];
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * kEvalBlock;
+  const uint64_t hi = lo + kEvalBlock < nnz ? lo + kEvalBlock : nnz;
+  double acc = 0.0;
+  for (uint64_t e = lo + t; e < hi; e += BT) {
+    const uint32_t* rp = rec + e * 5;
+    float u1[J], u2[J], u3[J], u4[J];
+    load_row<J>(U1, __ldg(rp), -1, nullptr, u1);
+    load_row<J>(U2, __ldg(rp + 1), -1, nullptr, u2);
+    load_row<J>(U3, __ldg(rp + 2), -1, nullptr, u3);
+    load_row<J>(U4, __ldg(rp + 3), -1, nullptr, u4);
+    float xh = 0.f;
+#pragma unroll 1
+    for (int ia = 0; ia < J; ++ia) {
+      float ua = 0.f;  // select u1[ia] without local-memory indexing
+#pragma unroll
+      for (int k = 0; k < J; ++k) ua = k == ia ? u1[k] : ua;
+      const float* ga = Gs + ia * J * J * J;
+      float w = 0.f;
+#pragma unroll
+      for (int ib = 0; ib < J; ++ib) {
+        float sab = 0.f;
+#pragma unroll
+        for (int ic = 0; ic < J; ++ic) {
+          const float4 q0 = *reinterpret_cast<const float4*>(ga + (ib * J + ic) * J);
+          const float4 q1 = *reinterpret_cast<const float4*>(ga + (ib * J + ic) * J + 4);
+          float t0 = q0.x * u4[0], t1 = q0.y * u4[1];
+          t0 = fmaf(q0.z, u4[2], t0); t1 = fmaf(q0.w, u4[3], t1);
+          t0 = fmaf(q1.x, u4[4], t0); t1 = fmaf(q1.y, u4[5], t1);
+          t0 = fmaf(q1.z, u4[6], t0); t1 = fmaf(q1.w, u4[7], t1);
+          sab = fmaf(t0 + t1, u3[ic], sab);
+        }
+        w = fmaf(sab, u2[ib], w);
+      }
+      xh = fmaf(w, ua, xh);
+    }
+    const double r = (double)__uint_as_float(__ldg(rp + 4)) - (double)xh;
+    acc += r * r;
+  }
+  acc = warp_sum_d(acc);
+  if ((t & 31) == 0) acc_s[t >> 5] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double s2 = 0.0;
+    for (int i = 0; i < BT / 32; ++i) s2 += acc_s[i];
+    partial[blockIdx.x] = s2;
+  }
+}
+
+}  // namespace cmtfb

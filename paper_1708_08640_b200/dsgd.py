@@ -187,13 +187,21 @@ def run_epoch_emulated(ranks: Sequence[RankState]):
         r.state._check(L.cmtf_gpu_end_epoch(r.state._h))
 
 
+def _map_torch_nccl():
+    """The C library resolves NCCL at first use from whatever libnccl.so.2 the
+    process has mapped; importing torch first makes that PyTorch's copy."""
+    import torch  # noqa: F401
+
+
 def comm_init(rank_state: RankState, world: int, rank: int, unique_id: bytes):
+    _map_torch_nccl()
     L, h = rank_state.state._L, rank_state.state._h
     buf = C.create_string_buffer(unique_id, 128)
     rank_state.state._check(L.cmtf_gpu_comm_init(h, world, rank, buf))
 
 
 def new_unique_id() -> bytes:
+    _map_torch_nccl()
     buf = C.create_string_buffer(128)
     L = _abi.lib()
     _raise(L.cmtf_gpu_comm_unique_id(buf), L.cmtf_gpu_last_error().decode())

@@ -196,3 +196,30 @@ def config2(scale: float = 1.0) -> PlantedSpec:
         matrices=[MatrixSpec(0, 100_000, int(1_000_000 * scale), symmetric=True),
                   MatrixSpec(1, 200, int(2_000_000 * scale))],
         test_fraction=0.1, seed=0)
+
+
+def config4_small(nnz: int = 160_000) -> PlantedSpec:
+    """A CPU-oracle-sized stand-in for configs[3] (4-way, planted 8^4 core,
+    uniform indices, coupled matrices on modes 1 and 2) used by the parity
+    tests of the order-4 kernel: the same laws, dimensions shrunk so that a
+    block sees about the same number of concurrent updates per row of the
+    small modes as at full size (configs[3], mode 4: ~2.6 per iteration) and
+    modes 1 / 2 keep ~9 / ~36 observations per row."""
+    k = nnz / 40_000
+    return PlantedSpec(dims=[int(4000 * k), int(1000 * k), 200, 100], nnz=nnz, ranks=[8, 8, 8, 8],
+                       laws=["uniform"] * 4, factor_law="ref", noise=0.1,
+                       matrices=[MatrixSpec(0, 200, nnz // 10), MatrixSpec(1, 200, nnz // 10)],
+                       test_fraction=0.1, seed=0)
+
+
+def config4(scale: float = 1.0) -> PlantedSpec:
+    """configs[3] on the host (numpy): 4-way 1e6 x 1e5 x 1e3 x 100, 3e8 * scale
+    uniform nonzeros, planted 8^4 core + N(0, 0.1); coupled matrices on modes 1
+    and 2 (1e4 columns each, unspecified in BASELINE) with 3e7 * scale nonzeros
+    each.  Used at scale 0.1 for the reference-vs-GPU parity run; the bench
+    generates full size on the device (synth_gpu.config4)."""
+    return PlantedSpec(dims=[1_000_000, 100_000, 1000, 100], nnz=int(3e8 * scale),
+                       ranks=[8, 8, 8, 8], laws=["uniform"] * 4, factor_law="ref", noise=0.1,
+                       matrices=[MatrixSpec(0, 10_000, int(3e7 * scale)),
+                                 MatrixSpec(1, 10_000, int(3e7 * scale))],
+                       test_fraction=0.1, seed=0)

@@ -14,6 +14,8 @@ else:
     cfg = api.TrainConfig(ranks=[10, 10, 10], seed=0, eta0=1e-3, lambda_reg=0.01)
     REF = ({"train": 0.12004720232059254, "test": 0.12562375225231276} if scale == 1.0 else
            {"train": 0.1907186572058697, "test": 0.21336790418762466})
+if len(sys.argv) > 3:
+    cfg.kappa = float(sys.argv[3])
 for G in Gs:
     part = dsgd.partition(b, G)
     ranks = [dsgd.RankState(part, p, cfg) for p in range(G)]

@@ -355,3 +355,55 @@ def test_dsgd_emulated_ranks_within_1pct(G):
     te = api.test_rmse(full, test)
     assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
+
+
+@pytest.fixture(scope="module")
+def order4_reference():
+    """Serial oracle run on the configs[3] stand-in (4-way, 8^4 core), 20
+    epochs: tests/golden/config4_small_oracle.json (make_order4_golden.py)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "config4_small_oracle.json")))
+    b, test, _ = synth.generate(synth.config4_small())
+    return b, test, ref
+
+
+@pytest.mark.parametrize("kernel", ["opt", "naive"])
+def test_order4_kernel_rmse_within_1pct_of_oracle(kernel, order4_reference):
+    """hog4 (4-way, J = 8, tensor-core core gradient, interleaved matrices on
+    modes 1 and 2): train / test RMSE after 10 epochs (the configs' epoch
+    count) within 1% of the serial oracle, whose own seed-to-seed spread
+    there is 0.8%."""
+    b, test, ref = order4_reference
+    cfg = TrainConfig(ranks=[8] * 4, seed=0, eta0=ref["eta0"], mu=ref["mu"],
+                      lambda_reg=ref["lambda"], kernel=kernel)
+    st = api.make_state(cfg, b)
+    epochs = 10
+    for _ in range(epochs):
+        api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == "order4"
+    ref_train, ref_test = ref["seeds"]["0"][epochs - 1]
+    gpu_train = api.epoch_stats(st, ref["lambda"]).train_rmse
+    gpu_test = api.test_rmse(st, test)
+    msg = (gpu_train, ref_train, gpu_test, ref_test)
+    assert abs(gpu_train - ref_train) <= 0.01 * ref_train, msg
+    assert abs(gpu_test - ref_test) <= 0.01 * ref_test, msg
+
+
+def test_order4_single_entry_steps_match_oracle():
+    """One tensor entry per epoch (no concurrency): the hog4 sweep's row and
+    core steps equal the oracle's serial step (fp32 / TF32 core gradient)."""
+    dims = [9, 8, 10, 8]
+    idx = np.array([[1, 2, 3, 0]], dtype=np.uint32)
+    b = api.DataBundle(api.SparseTensor(dims, idx, np.array([2.5])), [])
+    cfg = TrainConfig(ranks=[8] * 4, seed=5, eta0=0.05, lambda_reg=0.1)
+    st = api.make_state(cfg, b)
+    tr = O.SerialTrainer(b, [8] * 4, seed=5, eta0=0.05, mu=0.1, lambda_reg=0.1)
+    tr.model.copy_from(st.model)
+    tr.run_epoch()
+    api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == "order4"
+    m = st.model
+    for a, ref in zip([m.core.reshape(-1)] + m.factors, [tr.model.core] + tr.model.factors):
+        scale_close(a, ref, 1e-3 * np.abs(ref).max(), 1e-4)
