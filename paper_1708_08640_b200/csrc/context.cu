@@ -135,6 +135,19 @@ struct cmtf_gpu_ctx {
   uint32_t* s_ids = nullptr;
   uint64_t s_ids_cap = 0;
   uint64_t rec_cap = 0, pos_cap = 0;
+  // per-epoch reshuffle: double buffers, and the affine map (posA, posB)
+  // from pos[] to the current physical position of an entry
+  uint32_t* rec_alt = nullptr;
+  uint64_t rec_alt_cap = 0;
+  uint64_t posA = 1, posB = 0;
+  uint4* mrec_alt = nullptr;
+  uint64_t mrec_alt_cap = 0;
+  // the next epoch's gathers run on a side stream, overlapping the current
+  // sweep (they only read rec / mrec and write the spare buffers)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_side_start = nullptr, ev_side_done = nullptr;
+  int64_t pend_t_epoch = -1, pend_m_epoch = -1;  // epoch whose order sits in *_alt
+  uint64_t pend_ta = 1, pend_tb = 0;
 
   // scratch
   double* d_partial = nullptr;
@@ -331,6 +344,55 @@ __global__ void gather_records_kernel(const uint32_t* src, const uint32_t* ids,
   }
 }
 
+// Per-epoch reshuffle (the reference reshuffles its schedule every epoch,
+// src/trainer.cpp:122-128): the records move in groups of kShuffleGroup
+// consecutive ones (the storage order is already a random permutation, so a
+// group is a random set; 8 x 16 B = one 128-B line keeps the gather at
+// streaming efficiency): dst group g = src group (a*g + b) mod ng.  Records
+// past ng * kShuffleGroup stay in place.  Each warp walks runs of 32 records
+// (32 / kShuffleGroup groups), a lane's source group advancing by
+// step = (32 / kShuffleGroup) * a mod ng.
+constexpr int kShuffleGroup = 8;
+constexpr int kReshuffleRun = 64;
+template <int WORDS>
+__global__ void reshuffle_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                 uint64_t n, uint64_t a, uint64_t b, uint64_t step) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t ng = n / kShuffleGroup, body = ng * kShuffleGroup;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t run = 32ull * kReshuffleRun;
+  for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * run;
+       base < n; base += warps * run) {
+    uint64_t i = base + lane;
+    uint64_t g = i / kShuffleGroup;
+    uint64_t pg = g < ng ? (uint64_t)(((unsigned __int128)a * g + b) % ng) : 0;
+    for (int r = 0; r < kReshuffleRun && i < n; ++r, i += 32) {
+      const uint64_t q = i < body ? pg * kShuffleGroup + (i % kShuffleGroup) : i;
+      if (WORDS == 4) {
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      } else {
+#pragma unroll
+        for (int w = 0; w < WORDS; ++w) dst[i * WORDS + w] = __ldg(src + q * WORDS + w);
+      }
+      pg += step;
+      if (pg >= ng) pg -= ng;
+    }
+  }
+}
+
+// pos[i] <- current position: group (A * group + B) mod ng, same offset
+__global__ void remap_pos_kernel(uint32_t* pos, uint64_t count, uint64_t n, uint64_t A,
+                                 uint64_t B) {
+  const uint64_t ng = n / kShuffleGroup, body = ng * kShuffleGroup;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = pos[i];
+    if (p < body)
+      pos[i] = (uint32_t)((((unsigned __int128)A * (p / kShuffleGroup) + B) % ng) *
+                              kShuffleGroup + p % kShuffleGroup);
+  }
+}
+
 __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
                            float* reg) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -358,6 +420,11 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
   }
 }
 
+int normalize_pos(cmtf_gpu_ctx* ctx);  // reshuffle machinery, below
+int take_matrix_order(cmtf_gpu_ctx* ctx);
+int prefetch_orders(cmtf_gpu_ctx* ctx, bool tensor, bool matrices);
+void drain_side(cmtf_gpu_ctx* ctx);
+
 uint64_t gcd64(uint64_t x, uint64_t y) {
   while (y) {
     const uint64_t t = x % y;
@@ -376,6 +443,26 @@ void affine_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* b) {
   uint64_t s = seed * 0x9e3779b97f4a7c15ULL + 0x632be59bd9b4e019ULL;
   s ^= s >> 29;
   *b = n ? s % n : 0;
+}
+
+// A fresh affine visiting order for (seed, epoch, stream): multiplier drawn
+// uniformly among the units mod n, offset uniform.
+void epoch_affine(uint64_t n, uint64_t seed, uint64_t epoch, uint64_t stream, uint64_t* a,
+                  uint64_t* b) {
+  *a = 1;
+  *b = 0;
+  if (n < 3) return;
+  auto mix = [](uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+  };
+  const uint64_t s = mix(mix(mix(seed) ^ epoch) ^ (stream * 0x632be59bd9b4e019ULL));
+  uint64_t m = 1 + mix(s) % (n - 1);
+  while (gcd64(m, n) != 1) m = m + 1 < n ? m + 1 : 1;
+  *a = m;
+  *b = mix(s + 1) % n;
 }
 
 unsigned grid_for(uint64_t n, unsigned bt = 256) {
@@ -761,6 +848,7 @@ size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
 
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
+  drain_side(ctx);  // mrec is rebuilt below
   const uint32_t JP = (uint32_t)round_up4(J);
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
@@ -815,7 +903,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
   const size_t fixed = four ? sizeof(float) * (size_t)V4Layout<8, 8>::FIXED_FLOATS
                             : v2_fixed_bytes_rt(J, sh);
-  const size_t limit = 227 * 1024 - 1024;
+  const size_t limit = 227 * 1024 - 2048;  // room for a co-resident gather block
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   struct Cand {
     uint32_t count;
@@ -902,6 +990,7 @@ int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
   return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
+
 // Fill the sweep arguments shared by hog3v2 and hog4 for tensor records
 // [t_lo, t_hi) and matrix records [m_lo[m], m_hi[m]) (NULL ranges = every
 // matrix entry).  Returns false when there is nothing to sweep.
@@ -977,9 +1066,12 @@ bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint6
 int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
              const uint64_t* m_lo, const uint64_t* m_hi) {
   if (ctx->v2_dirty) TRY(prepare_v2(ctx, J));
+  const bool mshuf = ctx->cfg.order_policy == 1 && !(m_lo && m_hi);
+  if (mshuf) TRY(take_matrix_order(ctx));
   Hog3v2Args a{};
   a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
   if (!fill_sweep_args<3>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
+  TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
 #define V2_CASE(JV)                                                            \
@@ -1013,9 +1105,12 @@ int launch_v4(cmtf_gpu_ctx* ctx, const Hog4Args& args) {
 int v4_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
              const uint64_t* m_hi) {
   if (ctx->v2_dirty) TRY(prepare_v2(ctx, 8));
+  const bool mshuf = ctx->cfg.order_policy == 1 && !(m_lo && m_hi);
+  if (mshuf) TRY(take_matrix_order(ctx));
   Hog4Args a{};
   a.rec = ctx->rec + t_lo * 5;
   if (!fill_sweep_args<4>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
+  TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 2;
   return ctx->cfg.kernel == CMTF_KERNEL_OPT ? launch_v4<true>(ctx, a) : launch_v4<false>(ctx, a);
 }
@@ -1072,6 +1167,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t
   return CMTF_OK;
 }
 
+
 int serial_epoch(cmtf_gpu_ctx* ctx, float eta) {
   // build_schedule / shuffle_schedule (src/trainer.cpp:114-128), applied to
   // the persisted schedule so shuffles accumulate across epochs.
@@ -1090,6 +1186,7 @@ int serial_epoch(cmtf_gpu_ctx* ctx, float eta) {
   }
   CU(cudaMemcpyAsync(ctx->d_sched, ctx->schedule.data(), total * sizeof(uint64_t),
                      cudaMemcpyHostToDevice, ctx->stream));
+  TRY(normalize_pos(ctx));
   SerialArgs a{};
   a.cs = core_shape(ctx);
   a.G = ctx->G;
@@ -1223,6 +1320,10 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
     return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->uev) cudaEventCreate(&ev);
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
+  cudaEventCreateWithFlags(&ctx->ev_side_start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_side_done, cudaEventDisableTiming);
   if (cudaMalloc(&ctx->d_first, sizeof(unsigned long long) * (1 + kMaxOrder + kMaxMats)) !=
       cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "allocation failed"));
@@ -1234,8 +1335,11 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   if (!ctx) return CMTF_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
   dfree(ctx->rec);
   dfree(ctx->pos);
+  dfree(ctx->rec_alt);
+  dfree(ctx->mrec_alt);
   dfree(ctx->s_idx);
   dfree(ctx->s_vals);
   dfree(ctx->s_rec);
@@ -1278,6 +1382,9 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   for (auto& ev : ctx->uev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_side_start) cudaEventDestroy(ctx->ev_side_start);
+  if (ctx->ev_side_done) cudaEventDestroy(ctx->ev_side_done);
   delete ctx;
   return CMTF_OK;
 }
@@ -1300,6 +1407,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   const bool same_shape =
       ctx->dims.size() == (size_t)N && std::equal(ctx->dims.begin(), ctx->dims.end(), dims);
+  drain_side(ctx);  // a pending reshuffle reads rec
   ctx->dims.assign(dims, dims + N);
   ctx->nnz = nnz;
   ctx->v2_dirty = true;
@@ -1357,6 +1465,8 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
   TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
+  ctx->posA = 1;
+  ctx->posB = 0;
   uint32_t* sorted_ids = nullptr;
   if (ctx->cfg.order_policy == 2) {  // caller order (DSGD strata)
     scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, 1, 0,
@@ -1609,6 +1719,147 @@ int cmtf_gpu_set_state(cmtf_gpu_ctx* ctx, int32_t epoch, double eta) {
 
 namespace {
 
+uint64_t mulmod(uint64_t x, uint64_t y, uint64_t n) {
+  return (uint64_t)(((unsigned __int128)x * y) % n);
+}
+uint64_t inv_mod(uint64_t a, uint64_t n) {  // gcd(a, n) = 1
+  __int128 t = 0, nt = 1, r = (__int128)n, nr = (__int128)(a % n);
+  while (nr != 0) {
+    const __int128 q = r / nr, tt = t - q * nt, rr = r - q * nr;
+    t = nt; nt = tt; r = nr; nr = rr;
+  }
+  if (t < 0) t += n;
+  return (uint64_t)t;
+}
+
+template <int WORDS>
+void launch_reshuffle(const uint32_t* src, uint32_t* dst, uint64_t n, uint64_t a, uint64_t b,
+                      cudaStream_t st) {
+  const uint64_t ng = n / kShuffleGroup;
+  const uint64_t per_block = 8ull * 32 * kReshuffleRun;  // 8 warps
+  uint64_t blocks = (n + per_block - 1) / per_block;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  reshuffle_kernel<WORDS><<<(unsigned)std::max<uint64_t>(1, blocks), 256, 0, st>>>(
+      src, dst, n, a, b, mulmod(a, (32 / kShuffleGroup) % ng, ng));
+}
+
+int launch_tensor_gather(cmtf_gpu_ctx* ctx, uint64_t epoch, cudaStream_t st, uint64_t* a,
+                         uint64_t* b) {
+  const uint64_t n = ctx->nnz, ng = n / kShuffleGroup;
+  epoch_affine(ng, ctx->cfg.seed, epoch, 1, a, b);
+  switch (ctx->order + 1) {
+    case 4: launch_reshuffle<4>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 5: launch_reshuffle<5>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 3: launch_reshuffle<3>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 6: launch_reshuffle<6>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 7: launch_reshuffle<7>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 8: launch_reshuffle<8>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 9: launch_reshuffle<9>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    default: return set_err(ctx, CMTF_EUNSUPPORTED, "order %d", ctx->order);
+  }
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
+void launch_matrix_gather(cmtf_gpu_ctx* ctx, uint64_t epoch, cudaStream_t st) {
+  uint64_t a = 1, b = 0;
+  epoch_affine(ctx->mnnz / kShuffleGroup, ctx->cfg.seed, epoch, 2, &a, &b);
+  launch_reshuffle<4>(reinterpret_cast<const uint32_t*>(ctx->mrec),
+                      reinterpret_cast<uint32_t*>(ctx->mrec_alt), ctx->mnnz, a, b, st);
+}
+
+// Drop pending next-epoch gathers (before buffers change or are reallocated).
+void drain_side(cmtf_gpu_ctx* ctx) {
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
+  ctx->pend_t_epoch = ctx->pend_m_epoch = -1;
+}
+
+bool tensor_shuffles(const cmtf_gpu_ctx* ctx) { return ctx->nnz / kShuffleGroup >= 3; }
+bool matrix_shuffles(const cmtf_gpu_ctx* ctx) {
+  return ctx->mrec && ctx->mnnz / kShuffleGroup >= 3;
+}
+
+// This epoch's random visiting order of the training records (random order
+// policy, whole-epoch sweeps): the gather prefetched during the previous
+// epoch if there is one, else a gather now; then swap buffers.  pos[] stays
+// valid through the group map (posA, posB).
+int take_tensor_order(cmtf_gpu_ctx* ctx) {
+  if (!tensor_shuffles(ctx)) return CMTF_OK;
+  const uint64_t ng = ctx->nnz / kShuffleGroup;
+  uint64_t a = 1, b = 0;
+  if (ctx->pend_t_epoch == ctx->epoch) {
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side_done, 0));
+    a = ctx->pend_ta;
+    b = ctx->pend_tb;
+    ctx->pend_t_epoch = -1;
+  } else {
+    drain_side(ctx);
+    TRY(ensure(ctx, &ctx->rec_alt, &ctx->rec_alt_cap, ctx->nnz * (ctx->order + 1)));
+    TRY(launch_tensor_gather(ctx, (uint64_t)ctx->epoch, ctx->stream, &a, &b));
+    ctx->last_launches += 1;
+  }
+  std::swap(ctx->rec, ctx->rec_alt);
+  std::swap(ctx->rec_cap, ctx->rec_alt_cap);
+  // the group at old position G moves to a^-1 (G - b)
+  const uint64_t ai = inv_mod(a, ng);
+  ctx->posA = mulmod(ai, ctx->posA, ng);
+  ctx->posB = mulmod(ai, (ctx->posB + ng - b) % ng, ng);
+  return CMTF_OK;
+}
+
+int take_matrix_order(cmtf_gpu_ctx* ctx) {
+  if (!matrix_shuffles(ctx)) return CMTF_OK;
+  if (ctx->pend_m_epoch == ctx->epoch) {
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side_done, 0));
+    ctx->pend_m_epoch = -1;
+  } else {
+    drain_side(ctx);
+    TRY(ensure(ctx, &ctx->mrec_alt, &ctx->mrec_alt_cap, ctx->mnnz));
+    launch_matrix_gather(ctx, (uint64_t)ctx->epoch, ctx->stream);
+    CU(cudaGetLastError());
+    ctx->last_launches += 1;
+  }
+  std::swap(ctx->mrec, ctx->mrec_alt);
+  std::swap(ctx->mrec_cap, ctx->mrec_alt_cap);
+  return CMTF_OK;
+}
+
+// Start the next epoch's gathers on the side stream; call right before the
+// sweep launch (the spare buffers were last read before this point).
+int prefetch_orders(cmtf_gpu_ctx* ctx, bool tensor, bool matrices) {
+  tensor = tensor && tensor_shuffles(ctx);
+  matrices = matrices && matrix_shuffles(ctx);
+  if (!tensor && !matrices) return CMTF_OK;
+  const uint64_t next = (uint64_t)ctx->epoch + 1;
+  if (tensor) TRY(ensure(ctx, &ctx->rec_alt, &ctx->rec_alt_cap, ctx->nnz * (ctx->order + 1)));
+  if (matrices) TRY(ensure(ctx, &ctx->mrec_alt, &ctx->mrec_alt_cap, ctx->mnnz));
+  CU(cudaEventRecord(ctx->ev_side_start, ctx->stream));
+  CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side_start, 0));
+  if (tensor) {
+    TRY(launch_tensor_gather(ctx, next, ctx->side, &ctx->pend_ta, &ctx->pend_tb));
+    ctx->pend_t_epoch = (int64_t)next;
+  }
+  if (matrices) {
+    launch_matrix_gather(ctx, next, ctx->side);
+    CU(cudaGetLastError());
+    ctx->pend_m_epoch = (int64_t)next;
+  }
+  CU(cudaEventRecord(ctx->ev_side_done, ctx->side));
+  ctx->last_launches += (tensor ? 1 : 0) + (matrices ? 1 : 0);
+  return CMTF_OK;
+}
+
+// Make pos[] exact again (serial replay and probes index records by pos).
+int normalize_pos(cmtf_gpu_ctx* ctx) {
+  if (ctx->posA == 1 && ctx->posB == 0) return CMTF_OK;
+  remap_pos_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(ctx->pos, ctx->nnz, ctx->nnz,
+                                                                 ctx->posA, ctx->posB);
+  CU(cudaGetLastError());
+  ctx->posA = 1;
+  ctx->posB = 0;
+  return CMTF_OK;
+}
+
 // One sweep (no epoch bookkeeping) over a tensor range and matrix ranges.
 int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
           const uint64_t* m_hi) {
@@ -1620,6 +1871,8 @@ int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     return CMTF_OK;
   }
+  const bool whole = t_lo == 0 && t_hi == ctx->nnz && !m_lo;
+  if (ctx->cfg.order_policy == 1 && whole) TRY(take_tensor_order(ctx));
   int J = 0;
   if (v4_supported(ctx)) {
     TRY(v4_sweep(ctx, eta, t_lo, t_hi, m_lo, m_hi));  // + interleaved matrices
@@ -1635,6 +1888,7 @@ int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     return CMTF_OK;
   }
+  if (ctx->cfg.order_policy == 1 && whole) TRY(prefetch_orders(ctx, true, false));
   TRY(hogwild_tensor_sweep(ctx, eta, t_lo, t_hi));
   ctx->last_launches += 1;
   CU(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -2056,6 +2310,7 @@ int cmtf_gpu_entry_grads(cmtf_gpu_ctx* ctx, const uint64_t* ids, uint64_t n,
   TRY(dalloc(ctx, &d_grow, n * sumJ));
   if (gcore) TRY(dalloc(ctx, &d_gcore, n * cs.size));
   CU(cudaMemcpyAsync(d_ids, ids, n * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  TRY(normalize_pos(ctx));
   ProbeArgs a{};
   a.cs = cs;
   a.G = ctx->G;
