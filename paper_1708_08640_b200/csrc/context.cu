@@ -793,6 +793,14 @@ int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M0, float eta, uint64_t lo,
 // ---------------------------------------------------------------------
 constexpr int kV2Warps = 8;  // default; 12 when registers and shared memory allow
 
+// order 4, opt kernel: the sweep's core contractions on the tensor cores
+// (CMTF_V4_TC=0 selects the CUDA-core sweep, for comparison)
+bool v4_tc(const cmtf_gpu_ctx* ctx) {
+  if (ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
+  const char* v = std::getenv("CMTF_V4_TC");
+  return !(v && v[0] == '0');
+}
+
 bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
   if (ctx->cfg.kernel_version == 1) return false;
   if (!fast3_supported(ctx, J)) return false;
@@ -901,7 +909,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
-  const size_t fixed = four ? sizeof(float) * (size_t)V4Layout<8, 8>::FIXED_FLOATS
+  const size_t fixed = four ? sizeof(float) * (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
+                                                                 : V4Layout<8, 8>::FIXED_FLOATS)
                             : v2_fixed_bytes_rt(J, sh);
   const size_t limit = 227 * 1024 - 2048;  // room for a co-resident gather block
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
@@ -1092,9 +1101,9 @@ bool v4_supported(const cmtf_gpu_ctx* ctx) {
   return ctx->mats.size() <= (size_t)kV2MaxMats;
 }
 
-template <bool OPT>
+template <int MODE>
 int launch_v4(cmtf_gpu_ctx* ctx, const Hog4Args& args) {
-  auto kern = hog4_kernel<8, OPT, 8>;
+  auto kern = hog4_kernel<8, MODE, 8>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)ctx->v2_smem));
   kern<<<ctx->v2_blocks, 8 * 32, ctx->v2_smem, ctx->stream>>>(args);
@@ -1112,7 +1121,8 @@ int v4_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi, const u
   if (!fill_sweep_args<4>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 2;
-  return ctx->cfg.kernel == CMTF_KERNEL_OPT ? launch_v4<true>(ctx, a) : launch_v4<false>(ctx, a);
+  if (ctx->cfg.kernel != CMTF_KERNEL_OPT) return launch_v4<0>(ctx, a);
+  return v4_tc(ctx) ? launch_v4<2>(ctx, a) : launch_v4<1>(ctx, a);
 }
 
 int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi) {

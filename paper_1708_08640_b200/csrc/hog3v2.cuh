@@ -38,6 +38,10 @@
 
 #include "common.cuh"
 
+#ifndef CMTF_COLD_RED
+#define CMTF_COLD_RED 1  // cold-row steps as vector REDs (no lost updates)
+#endif
+
 namespace cmtfb {
 
 constexpr int kV2MaxMats = 8;
@@ -113,6 +117,34 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_strong(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+// 16-byte global -> shared copies that bypass L1 (the rows of the next
+// iteration's entries land in the staging rows while this one finishes)
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 __device__ __forceinline__ float4 ld_strong4(const float* p) {
   float4 v;
   asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -176,6 +208,16 @@ __device__ __forceinline__ void step_row(float* U, uint32_t i, int slot, float* 
     }
     stat[3 * slot] += curv;
     atomicAdd(reinterpret_cast<int*>(stat) + 3 * slot + 1, 1);
+  } else if (!nonneg && CMTF_COLD_RED) {
+    // cold row: add the step with vector REDs instead of storing the whole
+    // row, so a concurrent update of the same row made between our read and
+    // our write is not overwritten (no lost updates on cold rows)
+#pragma unroll
+    for (int k = 0; k < JP; k += 4)
+      red_add_v4(U + (uint64_t)i * JP + k,
+                 make_float4(k + 0 < J ? -eta * grad[k] : 0.f, k + 1 < J ? -eta * grad[k + 1] : 0.f,
+                             k + 2 < J ? -eta * grad[k + 2] : 0.f,
+                             k + 3 < J ? -eta * grad[k + 3] : 0.f));
   } else {
     float v[JP];
 #pragma unroll
@@ -599,10 +641,29 @@ hog3v2_kernel(Hog3v2Args a) {
     stat[n] = sm + a.hot[n].stat_off;
   }
 
-  // software pipeline: records of the next E entries in flight, their slots
-  // looked up and cold rows prefetched into L1 while this group is computed
+  // software pipeline: records two groups ahead; slots and regularisation
+  // coefficients one group ahead; the next group's cold rows are copied
+  // (cp.async) into the staging rows at the end of each iteration, so the
+  // L2 gathers overlap the matrix entries, the core push and the barrier.
   uint4 rc[E], rc1[E];
   int sl[E][3];
+  float rg[E][3];
+  auto issue_rows = [&](const uint4* r, const int (*slx)[3], uint64_t ebase) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (ebase + j >= hi) continue;
+      float* myst = stg + (j * 32 + lane) * SW;
+      const uint32_t ix[3] = {r[j].x, r[j].y, r[j].z};
+#pragma unroll
+      for (int n = 0; n < 3; ++n)
+        if (slx[j][n] < 0) {
+          const float* src = a.U[n] + (uint64_t)ix[n] * JP;
+#pragma unroll
+          for (int k = 0; k < JP; k += 4) cp_async16(myst + n * JP + k, src + k);
+        }
+    }
+    cp_async_commit();
+  };
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     const uint64_t e = lo + j, e1 = lo + E + j;
@@ -613,15 +674,20 @@ hog3v2_kernel(Hog3v2Args a) {
   for (int j = 0; j < E; ++j) {
     const uint32_t ix[3] = {rc[j].x, rc[j].y, rc[j].z};
 #pragma unroll
-    for (int n = 0; n < 3; ++n)
+    for (int n = 0; n < 3; ++n) {
       sl[j][n] = (lo + j < hi && a.hot[n].slot) ? __ldg(a.hot[n].slot + ix[n]) : -1;
+      rg[j][n] = lo + j < hi ? __ldg(a.reg[n] + ix[n]) : 0.f;
+    }
   }
+  issue_rows(rc, sl, lo);
+  cp_async_commit();  // (empty) core-refresh group: see the push
 
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e0 = lo + it * E;
     bool active[E];
     uint4 rc2[E];
     int nsl[E][3];
+    float nrg[E][3];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
       active[j] = e0 + j < hi;
@@ -634,35 +700,40 @@ hog3v2_kernel(Hog3v2Args a) {
         // no select on the loaded value (that would wait here); an invalid
         // next entry is never used (`active` gates every use)
         nsl[j][n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
-        if (nxt) {
-          const char* p = reinterpret_cast<const char*>(a.U[n] + (uint64_t)nx[n] * JP);
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + JP * 4 - 4));
-        }
+        nrg[j][n] = __ldg(a.reg[n] + (nxt ? nx[n] : 0u));
       }
     }
 
-    // ---- gather rows; u1 goes to the lane's staging row (rolled a-loop) ----
-    float u2[E][JP], u3[E][JP], g2[E][J], g3[E][J], xh[E], reg1[E], reg2[E], reg3[E];
+    // ---- this group's rows: cold ones already in the staging rows (the
+    // newest cp.async group, the last core refresh, may still fly) ----
+    cp_async_wait_group<1>();
+    float u2[E][JP], u3[E][JP], g2[E][J], g3[E][J], xh[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-      float u1[JP];
+      float* myst = stg + (j * 32 + lane) * SW;
       if (active[j]) {
-        load_row<JP>(a.U[0], rc[j].x, sl[j][0], rep[0], u1);
-        load_row<JP>(a.U[1], rc[j].y, sl[j][1], rep[1], u2[j]);
-        load_row<JP>(a.U[2], rc[j].z, sl[j][2], rep[2], u3[j]);
-        reg1[j] = __ldg(a.reg[0] + rc[j].x);
-        reg2[j] = __ldg(a.reg[1] + rc[j].y);
-        reg3[j] = __ldg(a.reg[2] + rc[j].z);
+        if (sl[j][0] >= 0) {
+#pragma unroll
+          for (int k = 0; k < JP; k += 4)
+            *reinterpret_cast<float4*>(myst + k) =
+                *reinterpret_cast<const float4*>(rep[0] + sl[j][0] * JP + k);
+        }
+        const float* s2 = sl[j][1] >= 0 ? rep[1] + sl[j][1] * JP : myst + JP;
+        const float* s3 = sl[j][2] >= 0 ? rep[2] + sl[j][2] * JP : myst + 2 * JP;
+#pragma unroll
+        for (int k = 0; k < JP; k += 4) {
+          const float4 q2 = *reinterpret_cast<const float4*>(s2 + k);
+          const float4 q3 = *reinterpret_cast<const float4*>(s3 + k);
+          u2[j][k] = q2.x; u2[j][k + 1] = q2.y; u2[j][k + 2] = q2.z; u2[j][k + 3] = q2.w;
+          u3[j][k] = q3.x; u3[j][k + 1] = q3.y; u3[j][k + 2] = q3.z; u3[j][k + 3] = q3.w;
+        }
       } else {
 #pragma unroll
-        for (int k = 0; k < JP; ++k) { u1[k] = 0.f; u2[j][k] = 0.f; u3[j][k] = 0.f; }
-        reg1[j] = reg2[j] = reg3[j] = 0.f;
-      }
-      float* myst = stg + (j * 32 + lane) * SW;
+        for (int k = 0; k < JP; ++k) { u2[j][k] = 0.f; u3[j][k] = 0.f; }
 #pragma unroll
-      for (int k = 0; k < JP; k += 4)
-        *reinterpret_cast<float4*>(myst + k) = make_float4(u1[k], u1[k + 1], u1[k + 2], u1[k + 3]);
+        for (int k = 0; k < JP; k += 4)
+          *reinterpret_cast<float4*>(myst + k) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
       for (int k = 0; k < J; ++k) { g2[j][k] = 0.f; g3[j][k] = 0.f; }
       xh[j] = 0.f;
@@ -797,15 +868,15 @@ hog3v2_kernel(Hog3v2Args a) {
       // row steps: every lane of the warp takes part (hot-row aggregation)
       float gr[J];
 #pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], reg1[j] * u1[k]);
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], rg[j][0] * u1[k]);
       step_row_warp<J, JP>(a.U[0], rc[j].x, sl[j][0], const_cast<float*>(rep[0]), stat[0],
                            (int)a.hot[0].off, active[j], u1, gr, a.eta, a.nonneg, c1, lane);
 #pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[j][k], reg2[j] * u2[j][k]);
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[j][k], rg[j][1] * u2[j][k]);
       step_row_warp<J, JP>(a.U[1], rc[j].y, sl[j][1], const_cast<float*>(rep[1]), stat[1],
                            (int)a.hot[1].off, active[j], u2[j], gr, a.eta, a.nonneg, c2, lane);
 #pragma unroll
-      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[j][k], reg3[j] * u3[j][k]);
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[j][k], rg[j][2] * u3[j][k]);
       step_row_warp<J, JP>(a.U[2], rc[j].z, sl[j][2], const_cast<float*>(rep[2]), stat[2],
                            (int)a.hot[2].off, active[j], u3[j], gr, a.eta, a.nonneg, c3, lane);
       // stage (-r u1, u2, u3) at pre-update values (zeros for idle lanes)
@@ -825,6 +896,8 @@ hog3v2_kernel(Hog3v2Args a) {
 #pragma unroll
     for (int j = 0; j < E; ++j)
       core_grad_mma<J, JP, SW, AB, L::NT, L::MT>(stg + j * 32 * SW, dGw, g8, t4);
+    __syncwarp();  // the staging rows are free: start the next group's gathers
+    issue_rows(rc1, nsl, e0 + E);
 
     // ---- matrix entries due by this iteration (interleaved) ----
     matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
@@ -835,7 +908,10 @@ hog3v2_kernel(Hog3v2Args a) {
       rc[j] = rc1[j];
       rc1[j] = rc2[j];
 #pragma unroll
-      for (int n = 0; n < 3; ++n) sl[j][n] = nsl[j][n];
+      for (int n = 0; n < 3; ++n) {
+        sl[j][n] = nsl[j][n];
+        rg[j][n] = nrg[j][n];
+      }
     }
 
     // ---- periodic core push / refresh (block-level, every core_every) ----
@@ -864,24 +940,38 @@ hog3v2_kernel(Hog3v2Args a) {
         const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
         const float s = -a.eta * alpha;
         float* dG0 = sm + L::G_FLOATS;
-        for (int e = threadIdx.x; e < AB * J; e += NW * 32) {
-          const int ab = e / J, c = e - (e / J) * J;
-          const int o = ab * JP + c;
-          float sum = 0.f;
+        // fire-and-forget REDs; the shared copy becomes the global core as
+        // of the previous push plus this delta, and the global value is
+        // re-read now for the next push (no wait on an atomic's return)
 #pragma unroll
-          for (int q = 0; q < NW; ++q) {
-            float* dq = dG0 + q * (L::DG_FLOATS + L::STAGE_FLOATS) + o;
-            sum += *dq;
-            *dq = 0.f;
+        for (int k = 0; k < (AB * J + NW * 32 - 1) / (NW * 32); ++k) {
+          const int e = threadIdx.x + k * NW * 32;
+          if (e < AB * J) {
+            const int ab = e / J, c = e - (e / J) * J;
+            const int o = ab * JP + c;
+            float sum = 0.f;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+              float* dq = dG0 + q * (L::DG_FLOATS + L::STAGE_FLOATS) + o;
+              sum += *dq;
+              *dq = 0.f;
+            }
+            const float delta = s * fmaf(kb * a.core_reg, Gs[o], sum);
+            if (a.nonneg) {
+              Gs[o] = fmaxf(atomicAdd(a.G + e, delta) + delta, 0.f);
+            } else {
+              // fire-and-forget RED; the shared copy is refreshed from the
+              // global core asynchronously (the read follows our RED to the
+              // same address; warps see the old or the new value)
+              red_add_f32(a.G + e, delta);
+              cp_async4(Gs + o, a.G + e);
+            }
           }
-          const float delta = s * fmaf(kb * a.core_reg, Gs[o], sum);
-          float v = atomicAdd(a.G + e, delta) + delta;
-          if (a.nonneg) v = fmaxf(v, 0.f);
-          Gs[o] = v;
         }
       }
       __syncthreads();
     }
+    cp_async_commit();  // core refresh group (possibly empty)
     // ---- periodic hot-row merges: all warps in the same iteration, each a
     // 1/NW share (the core push already aligns the warps; a staggered flush
     // would make one warp late at every core-push barrier) ----
@@ -890,6 +980,7 @@ hog3v2_kernel(Hog3v2Args a) {
   }
   // remaining matrix entries (rounding) and the final hot flush of everything
   matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
+  cp_async_wait_all();
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);
 }
