@@ -272,6 +272,8 @@ def run_ours(args):
             "peak_source": f"nominal FP32: {sms} SMs x 128 FMA x 2 x 1965 MHz (no FP32 "
                            "entry in MEASURED_PEAKS.json)",
             "kernel": {"order3v2": "hog3v2_kernel (fused tensor+matrix epoch sweep)",
+                       "order3tc": "hog3tc_kernel (fused epoch sweep, tensor-core contractions)",
+                       "order4": "hog4_kernel (fused epoch sweep, tensor-core contractions)",
                        "order3": "hog3_kernel (tensor sweep)",
                        "generic": "hogwild_generic_kernel (tensor sweep)"}.get(info["kernel"]),
             "kernel_ms": ten_ms,

@@ -25,6 +25,7 @@
 #include "hog3.cuh"
 #include "hog3v2.cuh"
 #include "hog4.cuh"
+#include "hog3tc.cuh"
 
 using namespace cmtfb;
 
@@ -801,6 +802,17 @@ bool v4_tc(const cmtf_gpu_ctx* ctx) {
   return !(v && v[0] == '0');
 }
 
+// order 3, opt kernel: the sweep's core contractions on the tensor cores
+// (hog3tc).  Opt-in with CMTF_V3_TC=1: measured on config 2 it is slower than
+// the CUDA-core hog3v2 (4.18 vs 2.95 ms/epoch: less shared memory left for
+// hot-row replicas, per-component hot-row updates, E = 1), faster at 10%
+// scale (1.95 vs 2.61 ms).
+bool v3_tc(const cmtf_gpu_ctx* ctx) {
+  if (ctx->order != 3 || ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
+  const char* v = std::getenv("CMTF_V3_TC");
+  return v && v[0] == '1';
+}
+
 bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
   if (ctx->cfg.kernel_version == 1) return false;
   if (!fast3_supported(ctx, J)) return false;
@@ -860,7 +872,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const uint32_t JP = (uint32_t)round_up4(J);
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
-  const V2Shape sh = four ? V2Shape{8, 1} : v2_shape(ctx);
+  const bool tc3 = !four && v3_tc(ctx);
+  const V2Shape sh = four ? V2Shape{8, 1} : tc3 ? V2Shape{8, 1} : v2_shape(ctx);
   const int NW = sh.nw;
   ctx->v2_nw = NW;
   ctx->v2_e = sh.e;
@@ -909,9 +922,17 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
-  const size_t fixed = four ? sizeof(float) * (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
-                                                                 : V4Layout<8, 8>::FIXED_FLOATS)
-                            : v2_fixed_bytes_rt(J, sh);
+  size_t fixed = four ? sizeof(float) * (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
+                                                           : V4Layout<8, 8>::FIXED_FLOATS)
+                      : v2_fixed_bytes_rt(J, sh);
+  if (tc3) {
+    switch (J) {
+      case 4: fixed = sizeof(float) * (size_t)V3TCLayout<4, 8>::FIXED_FLOATS; break;
+      case 5: fixed = sizeof(float) * (size_t)V3TCLayout<5, 8>::FIXED_FLOATS; break;
+      case 8: fixed = sizeof(float) * (size_t)V3TCLayout<8, 8>::FIXED_FLOATS; break;
+      case 10: fixed = sizeof(float) * (size_t)V3TCLayout<10, 8>::FIXED_FLOATS; break;
+    }
+  }
   const size_t limit = 227 * 1024 - 2048;  // room for a co-resident gather block
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   struct Cand {
@@ -1000,6 +1021,16 @@ int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
 }
 
 
+template <int J>
+int launch_v3tc(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
+  auto kern = hog3tc_kernel<J, 8>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->v2_smem));
+  kern<<<ctx->v2_blocks, 8 * 32, ctx->v2_smem, ctx->stream>>>(args);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
+
 // Fill the sweep arguments shared by hog3v2 and hog4 for tensor records
 // [t_lo, t_hi) and matrix records [m_lo[m], m_hi[m]) (NULL ranges = every
 // matrix entry).  Returns false when there is nothing to sweep.
@@ -1083,6 +1114,15 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
+  if (v3_tc(ctx)) {
+    ctx->kernel_which = 4;
+    switch (J) {
+      case 4: return launch_v3tc<4>(ctx, a);
+      case 5: return launch_v3tc<5>(ctx, a);
+      case 8: return launch_v3tc<8>(ctx, a);
+      case 10: return launch_v3tc<10>(ctx, a);
+    }
+  }
 #define V2_CASE(JV)                                                            \
   case JV:                                                                     \
     return opt ? launch_v2_t<JV, true>(ctx, a) : launch_v2_t<JV, false>(ctx, a);
