@@ -192,6 +192,7 @@ struct cmtf_gpu_ctx {
   // timing
   cudaEvent_t ev[6] = {};
   cudaEvent_t uev[8] = {};
+  cudaEvent_t cev[4] = {};  // upload chunk copies
   double last_ms[4] = {0, 0, 0, 0};
   int32_t last_launches = 0;
   int kernel_which = 0;
@@ -297,27 +298,36 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t seed) {
   return x;
 }
 
-__global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals,
-                                   uint64_t nnz, int order, ModeTables mt,
+// Count with one atomic per distinct index per warp: Zipf heads would
+// otherwise serialise millions of same-address atomics in L2.
+__device__ __forceinline__ void count_aggregated(uint32_t* count, uint32_t i, bool valid) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, valid ? i : 0xffffffffu);
+  if (valid && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(count + i, __popc(peers));
+}
+
+// Records [e_lo, e_hi) of the upload: validation, counts, packing.
+__global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals, uint64_t e_lo,
+                                   uint64_t e_hi, int order, ModeTables mt,
                                    int sort_mode, uint32_t seed, uint32_t* rec,
                                    uint32_t* keys, uint32_t* ids,
                                    unsigned long long* bad) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+  for (uint64_t e = e_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < e_hi;
        e += (uint64_t)gridDim.x * blockDim.x) {
     for (int n = 0; n < order; ++n) {
       const uint32_t i = idx[e * order + n];
-      if (i >= mt.dims[n]) {
-        atomicMin(&bad[0], (unsigned long long)e);
-        continue;
-      }
-      atomicAdd(const_cast<uint32_t*>(mt.count[n]) + i, 1u);
+      const bool ok = i < mt.dims[n];
+      if (!ok) atomicMin(&bad[0], (unsigned long long)e);
+      count_aggregated(const_cast<uint32_t*>(mt.count[n]), i, ok);
       rec[e * (order + 1) + n] = i;
     }
     const double v = vals[e];
     if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
     rec[e * (order + 1) + order] = __float_as_uint((float)v);
-    keys[e] = sort_mode >= 0 ? idx[e * order + sort_mode] : mix32((uint32_t)e, seed);
-    ids[e] = (uint32_t)e;
+    if (keys) {  // sorted order only
+      keys[e] = sort_mode >= 0 ? idx[e * order + sort_mode] : mix32((uint32_t)e, seed);
+      ids[e] = (uint32_t)e;
+    }
   }
 }
 
@@ -409,8 +419,9 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = idx[2 * e], j = idx[2 * e + 1];
-    if (i >= rows || j >= cols) atomicMin(&bad[0], (unsigned long long)e);
-    else atomicAdd(count + j, 1u);
+    const bool ok = i < rows && j < cols;
+    if (!ok) atomicMin(&bad[0], (unsigned long long)e);
+    count_aggregated(count, j, ok);
     const double v = vals[e];
     if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
     rec[3 * e] = i;
@@ -1370,6 +1381,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
     return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   for (auto& ev : ctx->uev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->cev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
   cudaEventCreateWithFlags(&ctx->ev_side_start, cudaEventDisableTiming);
@@ -1431,6 +1443,8 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : ctx->uev)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ctx->cev)
+    if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_side_start) cudaEventDestroy(ctx->ev_side_start);
@@ -1478,11 +1492,20 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   uint32_t* d_idx = ctx->s_idx;
   double* d_vals = ctx->s_vals;
   uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
-  // cudaMemcpyDefault: host (pageable or pinned) or device source (UVA)
-  CU(cudaMemcpyAsync(d_idx, idx, nnz * N * sizeof(uint32_t), cudaMemcpyDefault,
-                     ctx->stream));
-  CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault,
-                     ctx->stream));
+  // cudaMemcpyDefault: host (pageable or pinned) or device source (UVA).
+  // The copies run in chunks on the side stream; each chunk is packed on the
+  // main stream as soon as it lands (H2D overlaps validation and packing).
+  constexpr int kChunks = 4;
+  const uint64_t chunk = (nnz + kChunks - 1) / kChunks;
+  for (int k = 0; k < kChunks; ++k) {
+    const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
+    if (c0 >= c1) break;
+    CU(cudaMemcpyAsync(d_idx + c0 * N, idx + c0 * N, (c1 - c0) * N * sizeof(uint32_t),
+                       cudaMemcpyDefault, ctx->side));
+    CU(cudaMemcpyAsync(d_vals + c0, vals + c0, (c1 - c0) * sizeof(double), cudaMemcpyDefault,
+                       ctx->side));
+    CU(cudaEventRecord(ctx->cev[k], ctx->side));
+  }
   for (int n = 0; n < N; ++n) {
     if (!same_shape || !ctx->count[n]) {
       TRY(dalloc(ctx, &ctx->count[n], dims[n]));
@@ -1493,9 +1516,15 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
   ModeTables mt = mode_tables(ctx);
   const bool shuffled = ctx->cfg.order_policy == 1;
-  pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-      d_idx, d_vals, nnz, N, mt, shuffled ? -1 : sm, (uint32_t)ctx->cfg.seed + 0x5bd1e995u,
-      d_rec, d_keys, d_ids, ctx->d_first);
+  const bool need_keys = ctx->cfg.order_policy == 0;  // sorted order needs the sort keys
+  for (int k = 0; k < kChunks; ++k) {
+    const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
+    if (c0 >= c1) break;
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->cev[k], 0));
+    pack_tensor_kernel<<<grid_for(c1 - c0), 256, 0, ctx->stream>>>(
+        d_idx, d_vals, c0, c1, N, mt, shuffled ? -1 : sm, (uint32_t)ctx->cfg.seed + 0x5bd1e995u,
+        d_rec, need_keys ? d_keys : nullptr, d_ids, ctx->d_first);
+  }
   CU(cudaGetLastError());
   unsigned long long bad[2];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
@@ -2280,7 +2309,7 @@ int cmtf_gpu_test_rmse(cmtf_gpu_ctx* ctx, const uint32_t* idx, const double* val
   }
   CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
   pack_tensor_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
-      d_idx, d_vals, nnz, N, mt, 0, 0u, d_rec, d_keys, d_ids, ctx->d_first);
+      d_idx, d_vals, 0, nnz, N, mt, 0, 0u, d_rec, nullptr, nullptr, ctx->d_first);
   CU(cudaGetLastError());
   unsigned long long bad[2];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));

@@ -24,3 +24,10 @@ for k in range(3):
     s = api.epoch_stats(st, 0.01); t5 = time.perf_counter()
     api.run_epoch(st); t6 = time.perf_counter()
     print(f"clear {1e3*(t1-t0):.2f} set_tensor {1e3*(t2-t1):.2f} add_matrix {1e3*(t3-t2):.2f} epoch(+prepare) {1e3*(t4-t3):.2f} stats {1e3*(t5-t4):.2f} plain epoch {1e3*(t6-t5):.2f} ms", flush=True)
+# raw pinned H2D bandwidth for the same bytes
+x = torch.empty(int(t.indices.nbytes + t.values.nbytes), dtype=torch.uint8).pin_memory()
+y = torch.empty_like(x, device="cuda")
+for _ in range(3):
+    torch.cuda.synchronize(); a0 = time.perf_counter()
+    y.copy_(x, non_blocking=True); torch.cuda.synchronize(); a1 = time.perf_counter()
+    print(f"raw pinned H2D {x.numel()/1e6:.0f} MB: {1e3*(a1-a0):.2f} ms = {x.numel()/(a1-a0)/1e9:.1f} GB/s", flush=True)
