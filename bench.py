@@ -281,6 +281,21 @@ def run_ours(args):
             "gather_gbs": bytes_t / (ten_ms * 1e-3) / 1e9,
             "frac_at_measured_clock": (achieved / fp32_peak_tflops(sms, clk["sm_mhz"])
                                        if clk.get("sm_mhz") else None)}
+    # DRAM traffic per launch of the dominant kernel, from the committed ncu
+    # --set full capture of the same command (profiles/ncu_r1_metrics.json)
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_r1_metrics.json")))
+        key = {"order3v2": "hog3v2", "order4": "hog4"}.get(info["kernel"])
+        for k, v in prof.items():
+            scale_ok = (f"scale {args.scale:g}" in k) if "scale" in k else args.scale == 1.0
+            if key and k.startswith(key) and args.config in k.replace("(", " ").split() and scale_ok:
+                roof["traffic"] = (v["dram__bytes_read.sum"]["value"]
+                                   + v["dram__bytes_write.sum"]["value"]) * 1e6
+                roof["traffic_unit"] = "bytes/launch (ncu dram read+write)"
+                roof["traffic_source"] = v["report"]
+                roof["algorithmic_bytes_per_launch"] = nt * Bt
+    except Exception:
+        pass
     # epoch roofline time: both terms, slower of HBM and FP32
     hbm = 6548.5e9
     try:
