@@ -54,6 +54,8 @@ def parse():
                    help="tensor entries in the bounded CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--strong", action="store_true",
+                   help="DSGD (N > 1): fixed total workload instead of weak scaling")
     p.add_argument("--dsgd", action="store_true",
                    help="use the DSGD/NCCL path even with one rank (testing)")
     return p.parse_args()
@@ -64,8 +66,15 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_workload(args):
+def make_workload(args, mult=1.0, device_gen=False):
+    """The BASELINE workload; `mult` scales its size (multi-GPU weak scaling,
+    generated on the device)."""
     from paper_1708_08640_b200 import synth
+    if args.config == "config2" and device_gen:
+        from paper_1708_08640_b200 import synth_gpu
+        spec = synth_gpu.config2(args.scale * mult)
+        bundle, test = synth_gpu.generate(spec, device=f"cuda:{dist_env()[2]}")
+        return spec, bundle, test, [10, 10, 10], 1e-3, 0.01
     if args.config == "config2":
         spec = synth.config2(args.scale)
         if args.uniform:
@@ -81,11 +90,11 @@ def make_workload(args):
         # device-side generation (1e8 - 1e9 nonzeros)
         from paper_1708_08640_b200 import synth_gpu
         if args.config == "config3":
-            spec = synth_gpu.config3(args.scale)
+            spec = synth_gpu.config3(args.scale * mult)
         elif args.config == "config4":
-            spec = synth_gpu.config4(args.scale)
+            spec = synth_gpu.config4(args.scale * mult)
         else:
-            spec = synth_gpu.config5(args.nnz, args.rank)
+            spec = synth_gpu.config5(args.nnz * mult, args.rank)
         bundle, test = synth_gpu.generate(spec, device=f"cuda:{dist_env()[2]}")
         return spec, bundle, test, list(spec.ranks), 1e-3, 0.01
     else:
@@ -393,7 +402,12 @@ def run_ours(args):
 def run_dsgd(args):
     """N > 1: DSGD strata over the ranks (one process per GPU), deltas of the
     replicated parameters all-reduced with NCCL inside the library after every
-    sub-epoch.  Total work is the fixed workload (strong scaling)."""
+    sub-epoch.  Default: weak scaling -- the workload grows with N (config 2 at
+    N x its size, generated on the device), so each GPU keeps a config-2-sized
+    share with all SMs busy under the same staleness bound (the worker rule
+    caps in-flight entries at ~1/112 of a rank's share; a config-2-sized
+    problem split 8 ways would leave 7/8 of every GPU idle).  --strong keeps
+    the total fixed."""
     import ctypes as C
 
     import torch
@@ -406,7 +420,13 @@ def run_dsgd(args):
     os.environ.setdefault("MASTER_PORT", "29511")
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"), rank=rank,
                             world_size=world)
-    spec, bundle, test, ranks, lr, lam = make_workload(args)
+    weak = not args.strong
+    spec, bundle, test, ranks, lr, lam = make_workload(
+        args, mult=world if weak else 1.0, device_gen=weak and world > 1)
+    bundle = host_bundle(bundle)  # partitioning runs on the host
+    if hasattr(test, "to_host"):
+        test = test.to_host()
+    torch.cuda.empty_cache()
     cfg = api.TrainConfig(ranks=ranks, seed=0, eta0=lr, lambda_reg=lam, kernel=args.kernel,
                           device=local)
     part = dsgd.partition(bundle, world)
@@ -454,11 +474,14 @@ def run_dsgd(args):
         line = {
             "metric": "tensor+matrix nonzero SGD updates/sec per epoch", "value": value,
             "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if weak else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}), "
                                f"scale {args.scale}" + (f", nnz {args.nnz:g}, rank {args.rank}"
-                                                         if args.config == "config5" else ""),
+                                                         if args.config == "config5" else "")
+                               + (f", x{world} (weak scaling: one config-sized share per GPU, "
+                                  "device-generated)" if weak and world > 1 else ""),
                        "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
                        "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
                        "parallelism": f"dsgd{world} (mode-1 x mode-2 strata, NCCL all-reduce "

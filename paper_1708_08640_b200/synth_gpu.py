@@ -139,6 +139,7 @@ class GpuMatrixSpec:
     nnz: int
     weight: float = 10.0
     noise: float = 0.1
+    symmetric: bool = False  # cols == rows; (i,j) and (j,i) stored, y = u_i . u_j
 
 
 @dataclass
@@ -182,6 +183,26 @@ def generate(spec: GpuSpec, device="cuda"):
     mats = []
     for ms in spec.matrices:
         rows = dims[ms.mode]
+        if ms.symmetric:
+            # unordered pairs i < j, distinct, then mirrored (no duplicates)
+            w = factors[ms.mode]
+            half = ms.nnz // 2
+            draw = distinct_coords(int(half * 1.05) + 1024, [rows, rows], ["uniform", "uniform"],
+                                   gen, device)
+            draw = draw[draw[:, 0] != draw[:, 1]]
+            lo_, hi_ = torch.minimum(draw[:, 0], draw[:, 1]), torch.maximum(draw[:, 0], draw[:, 1])
+            keys = torch.unique(lo_ * rows + hi_)
+            keys = keys[torch.randperm(keys.shape[0], generator=gen, device=device)[:half]]
+            pairs = torch.stack([keys // rows, keys % rows], 1)
+            y = (w[pairs[:, 0]] * w[pairs[:, 1]]).sum(1)
+            if ms.noise:
+                y += ms.noise * torch.randn(y.shape[0], generator=gen, device=device,
+                                            dtype=torch.float64)
+            ij = torch.cat([pairs, pairs.flip(1)])
+            y = torch.cat([y, y])
+            mats.append(DeviceMatrix(ms.mode, rows, rows, ij.to(torch.int32).contiguous(),
+                                     y.contiguous(), ms.weight))
+            continue
         w = torch.rand((ms.cols, ranks[ms.mode]), generator=gen, device=device,
                        dtype=torch.float64) / ranks[ms.mode] ** 0.5
         ij = distinct_coords(ms.nnz, [rows, ms.cols], ["uniform", "uniform"], gen, device,
@@ -199,6 +220,19 @@ def generate(spec: GpuSpec, device="cuda"):
 # ----------------------------------------------------------------------
 # BASELINE.json configs 3 - 5 (synthetic stand-ins)
 # ----------------------------------------------------------------------
+def config2(scale: float = 1.0) -> GpuSpec:
+    """configs[1] on the device (the host generator synth.config2 is the
+    reference stand-in at 1 GPU; this one feeds the multi-GPU weak-scaling
+    runs, where the problem grows with the GPU count): 1e5 x 1e5 x 1e3,
+    1e7 * scale Zipf(1.2) / Zipf(1.2) / uniform nonzeros, planted 10^3 core,
+    clipped to [1, 5]; symmetric 1e5 x 1e5 matrix (1e6 * scale) on mode 1 and
+    1e5 x 200 (2e6 * scale) on mode 2."""
+    return GpuSpec(dims=[100_000, 100_000, 1000], nnz=int(1e7 * scale), ranks=[10, 10, 10],
+                   laws=[("zipf", 1.2), ("zipf", 1.2), "uniform"], clip=(1.0, 5.0),
+                   matrices=[GpuMatrixSpec(0, 100_000, int(1e6 * scale), symmetric=True),
+                             GpuMatrixSpec(1, 200, int(2e6 * scale))])
+
+
 def config3(scale: float = 1.0) -> GpuSpec:
     """configs[2]: 1e6 x 1e6 x 1e4, 1e8 Zipf(1.1) nonzeros, planted 10^3 + noise;
     coupled 1e6 x 1e4 matrix with 1e7 nonzeros on mode 1."""
