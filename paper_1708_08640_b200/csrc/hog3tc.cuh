@@ -19,6 +19,10 @@
 
 #include "hog3v2.cuh"
 
+#ifndef CMTF_TC3_UNROLL
+#define CMTF_TC3_UNROLL 2
+#endif
+
 namespace cmtfb {
 
 template <int J, int NW>
@@ -50,6 +54,7 @@ hog3tc_kernel(Hog3v2Args a) {
   using L = V3TCLayout<J, NW>;
   constexpr int JP = L::JP, KB = L::KB, H = L::H, S1 = L::S1, S2 = L::S2, SW = L::SW;
   constexpr int AB = L::AB;
+  constexpr int kUnrollA = CMTF_TC3_UNROLL;
   extern __shared__ __align__(16) float sm[];
   float* G1 = sm;
   float* G2 = G1 + L::G1_FLOATS;
@@ -192,7 +197,7 @@ hog3tc_kernel(Hog3v2Args a) {
       float g3a[H][4] = {};  // g3[R0][c], g3[R0][c+1], g3[R1][c], g3[R1][c+1], c = nt*8+2t4
       float W1o[2][2 * H] = {};
       float xh0 = 0.f, xh1 = 0.f;
-#pragma unroll 1
+#pragma unroll kUnrollA
       for (int ia = 0; ia < J; ++ia) {
         const float ua0 = s0[ia], ua1 = s1[ia];
         const float* g1a = G1 + ia * KB * S1;
