@@ -854,13 +854,15 @@ struct V2Shape {
   int nw, e;
 };
 
-V2Shape v2_shape(const cmtf_gpu_ctx* ctx) {
+V2Shape v2_shape(const cmtf_gpu_ctx* ctx, int J) {
   (void)ctx;
-  V2Shape s{8, 2};
-  if (const char* v = std::getenv("CMTF_V2_SHAPE")) {  // "12x1" or "8x2" (experiments)
-    if (std::string(v) == "12x1") s = {12, 1};
+  // 8 warps x 2 entries per lane; one entry per lane for J <= 5, whose tiny
+  // sweep leaves the row gathers exposed (config 5 at rank 5: 22.2 vs 24.1
+  // ms/epoch; 4 entries per lane: 26.7 ms)
+  V2Shape s{8, J <= 5 ? 1 : 2};
+  if (const char* v = std::getenv("CMTF_V2_SHAPE")) {  // experiments: "8x1", "8x2"
+    if (std::string(v) == "8x1") s = {8, 1};
     if (std::string(v) == "8x2") s = {8, 2};
-    if (std::string(v) == "12x2") s = {12, 2};
   }
   return s;
 }
@@ -868,8 +870,7 @@ V2Shape v2_shape(const cmtf_gpu_ctx* ctx) {
 size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
 #define FB(JV)                                                                  \
   case JV:                                                                      \
-    return sh.nw == 12 ? (sh.e == 2 ? v2_fixed_bytes<JV, 12, 2>() : v2_fixed_bytes<JV, 12, 1>()) \
-                       : v2_fixed_bytes<JV, 8, 2>();
+    return sh.e == 1 ? v2_fixed_bytes<JV, 8, 1>() : v2_fixed_bytes<JV, 8, 2>();
   switch (J) {
     FB(4) FB(5) FB(8) FB(10)
   }
@@ -884,7 +885,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
   const bool tc3 = !four && v3_tc(ctx);
-  const V2Shape sh = four ? V2Shape{8, 1} : tc3 ? V2Shape{8, 1} : v2_shape(ctx);
+  const V2Shape sh = four ? V2Shape{8, 1} : tc3 ? V2Shape{8, 1} : v2_shape(ctx, J);
   const int NW = sh.nw;
   ctx->v2_nw = NW;
   ctx->v2_e = sh.e;
@@ -1025,9 +1026,7 @@ int launch_v2_nw(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
 
 template <int J, bool OPT>
 int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  if (ctx->v2_nw == 12)
-    return ctx->v2_e == 2 ? launch_v2_nw<J, OPT, 12, 2>(ctx, args)
-                          : launch_v2_nw<J, OPT, 12, 1>(ctx, args);
+  if (ctx->v2_e == 1) return launch_v2_nw<J, OPT, 8, 1>(ctx, args);
   return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
