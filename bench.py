@@ -282,6 +282,8 @@ def run_ours(args):
                            "entry in MEASURED_PEAKS.json)",
             "kernel": {"order3v2": "hog3v2_kernel (fused tensor+matrix epoch sweep)",
                        "order3tc": "hog3tc_kernel (fused epoch sweep, tensor-core contractions)",
+                       "order3tm": "hog3tm_kernel (fused epoch sweep, tcgen05 contractions + "
+                                   "core gradient, TMEM accumulators)",
                        "order4": "hog4_kernel (fused epoch sweep, tensor-core contractions)",
                        "order3": "hog3_kernel (tensor sweep)",
                        "generic": "hogwild_generic_kernel (tensor sweep)"}.get(info["kernel"]),

@@ -26,6 +26,7 @@
 #include "hog3v2.cuh"
 #include "hog4.cuh"
 #include "hog3tc.cuh"
+#include "hog3tm.cuh"
 
 using namespace cmtfb;
 
@@ -830,6 +831,17 @@ bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
   return *J == 4 || *J == 5 || *J == 8 || *J == 10;
 }
 
+// order 3, opt kernel: the sweep's core contractions and the core gradient
+// on the tcgen05 tensor cores with tensor-memory accumulators (hog3tm).
+// CMTF_V3_TM=0 selects the CUDA-core hog3v2.
+bool v3_tm(const cmtf_gpu_ctx* ctx) {
+  if (ctx->order != 3 || ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
+  int J = 0;
+  if (!v2_supported(ctx, &J)) return false;
+  const char* v = std::getenv("CMTF_V3_TM");
+  return !(v && v[0] == '0');
+}
+
 __global__ void merge_matrix_kernel(const uint32_t* rec, uint64_t n, uint32_t m, uint64_t base,
                                     uint4* out) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
@@ -885,7 +897,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
   const bool tc3 = !four && v3_tc(ctx);
-  const V2Shape sh = four ? V2Shape{8, 1} : tc3 ? V2Shape{8, 1} : v2_shape(ctx, J);
+  const bool tm3 = !four && !tc3 && v3_tm(ctx);
+  const V2Shape sh = four || tc3 || tm3 ? V2Shape{8, 1} : v2_shape(ctx, J);
   const int NW = sh.nw;
   ctx->v2_nw = NW;
   ctx->v2_e = sh.e;
@@ -898,7 +911,13 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     // synth.config4_small), so small problems stay close to sequential SGD
     // while large ones fill every SM
     const uint64_t per_slot = four ? 1024 : 112;
-    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (per_slot * NW * 32 * sh.e));
+    // hog3tm sweeps 256 entries per block per iteration like hog3v2 at E = 1,
+    // but it keeps hog3v2's block count (E = 2): more blocks means more
+    // replicas of every hot row and more, smaller, core pushes -- measured on
+    // config 2 at 10% scale: 31 blocks +0.78% RMSE vs the reference, 15
+    // blocks +0.40% (hog3v2: +0.34%)
+    const uint64_t e_rule = tm3 ? 2 : (uint64_t)sh.e;
+    const uint64_t cap = std::max<uint64_t>(1, ctx->nnz / (per_slot * NW * 32 * e_rule));
     blocks = (int)std::min<uint64_t>((uint64_t)blocks, cap);
   }
   ctx->v2_blocks = blocks;
@@ -937,6 +956,14 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   size_t fixed = four ? sizeof(float) * (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
                                                            : V4Layout<8, 8>::FIXED_FLOATS)
                       : v2_fixed_bytes_rt(J, sh);
+  if (tm3) {
+    switch (J) {
+      case 4: fixed = (size_t)TMLayout<4>::FIXED_BYTES; break;
+      case 5: fixed = (size_t)TMLayout<5>::FIXED_BYTES; break;
+      case 8: fixed = (size_t)TMLayout<8>::FIXED_BYTES; break;
+      case 10: fixed = (size_t)TMLayout<10>::FIXED_BYTES; break;
+    }
+  }
   if (tc3) {
     switch (J) {
       case 4: fixed = sizeof(float) * (size_t)V3TCLayout<4, 8>::FIXED_FLOATS; break;
@@ -1010,6 +1037,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   for (size_t m = 0; m < ctx->mats.size(); ++m)
     TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
   ctx->v2_smem = (size_t)off * sizeof(float);
+  // hog3tm allocates all 512 TMEM columns: keep it at one block per SM
+  if (tm3) ctx->v2_smem = std::max<size_t>(ctx->v2_smem, 116 * 1024);
   ctx->v2_dirty = false;
   return CMTF_OK;
 }
@@ -1030,6 +1059,16 @@ int launch_v2_t(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
   return launch_v2_nw<J, OPT, 8, 2>(ctx, args);
 }
 
+
+template <int J>
+int launch_v3tm(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
+  auto kern = hog3tm_kernel<J>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)ctx->v2_smem));
+  kern<<<ctx->v2_blocks, 8 * 32, ctx->v2_smem, ctx->stream>>>(args);
+  CU(cudaGetLastError());
+  return CMTF_OK;
+}
 
 template <int J>
 int launch_v3tc(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
@@ -1124,6 +1163,15 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
+  if (v3_tm(ctx) && !v3_tc(ctx)) {
+    ctx->kernel_which = 5;
+    switch (J) {
+      case 4: return launch_v3tm<4>(ctx, a);
+      case 5: return launch_v3tm<5>(ctx, a);
+      case 8: return launch_v3tm<8>(ctx, a);
+      case 10: return launch_v3tm<10>(ctx, a);
+    }
+  }
   if (v3_tc(ctx)) {
     ctx->kernel_which = 4;
     switch (J) {

@@ -386,7 +386,7 @@ hog3tc_kernel(Hog3v2Args a) {
           float* p2 = G2 + (ia * KB + ib) * S2 + c;
           const float delta = s * fmaf(kb * a.core_reg, *p1, sum);
           if (a.nonneg) {
-            const float v = fmaxf(atomicAdd(a.G + el, delta) + delta, 0.f);
+            const float v = atomic_add_clamp0(a.G + el, delta);
             *p1 = v;
             *p2 = v;
           } else {

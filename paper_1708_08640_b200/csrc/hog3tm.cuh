@@ -1,0 +1,495 @@
+// hog3tm.cuh -- order-3 S^3CMTF epoch kernel with the per-entry core
+// contractions AND the core gradient on the 5th-generation tensor cores
+// (tcgen05.mma, accumulators in tensor memory).
+//
+// Same epoch contract as hog3v2 (one launch = one epoch over the tensor and
+// the coupled matrices, hot-row replicas with damped merges, interleaved
+// matrix entries, block-level damped core push); only the arithmetic of a
+// tensor entry moves.  A block is 2 warpgroups; each warpgroup sweeps a tile
+// of 128 entries per iteration, thread e of the warpgroup owning entry e of
+// the tile (TMEM lane e).  Per tile (Algorithm 3's quantities,
+// src/gradients.cpp:130-223):
+//
+//   T[e][(a,b)] = sum_c u3_e[c] G[a,b,c]      MMA  A = U3 tile, B = G (ab x c)
+//   V[e][(a,c)] = sum_b u2_e[b] G[a,b,c]      MMA  A = U2 tile, B = G (ac x b)
+//   W1[a] = sum_b T[ab] u2[b],  g2[b] = sum_a T[ab] u1[a],  g3[c] = sum_a V[ac] u1[a],
+//   x_hat = sum_a W1[a] u1[a]                 FP32, 3 J^2 FMAs per entry
+//   dG[(a,b)][c] += sum_e P^T[ab][e] S[e][c]  MMA  A = P^T (u1[a] u2[b] per entry),
+//                                                  B = S^T (-r u3 per entry), fp16
+//
+// so an entry costs ~3J^2 FP32 FMAs instead of hog3v2's 2J^3 + 3J^2, and the
+// core gradient accumulates in tensor memory across the tile's 128 entries.
+// All operands are K-major, no-swizzle canonical layouts (umma.cuh): the
+// factor rows gathered with cp.async land directly in the U2/U3 operand tiles
+// (row e = 16-byte chunks at stride 2048 B), P^T and S^T are written as
+// transposed columns (one 4-byte store per element, bank-conflict-free).
+// The sweep MMAs take TF32 operands (the gathered fp32 rows as they are); the
+// core-gradient operands are fp16 (the same 10-bit mantissa as TF32, half the
+// shared memory: it goes to hot-row replicas), S^T pre-scaled by 2^8 so small
+// residuals stay normal; fp32 accumulation everywhere.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "hog3v2.cuh"
+#include "umma.cuh"
+
+#ifndef CMTF_TM_WGPUSH
+#define CMTF_TM_WGPUSH 1  // each warpgroup pushes its own core gradient (no block barrier)
+#endif
+#ifndef CMTF_TM_EXACT
+#define CMTF_TM_EXACT 0
+#endif
+
+namespace cmtfb {
+
+__host__ __device__ constexpr int round_up8(int x) { return (x + 7) & ~7; }
+__host__ __device__ constexpr int round_up16(int x) { return (x + 15) & ~15; }
+
+template <int J>
+struct TMLayout {
+  static constexpr int JP = round_up4(J);
+  static constexpr int KT = round_up8(J);      // K of the sweep MMAs (c or b, zero padded)
+  static constexpr int AB = J * J;
+  static constexpr int NT = round_up16(AB);    // N of the sweep MMAs ((a,b) or (a,c))
+  static constexpr int MR = round_up8(AB);     // stored rows of P^T (the MMA reads 128)
+  static constexpr int KC = 16;                // N of the core-gradient MMA (c, zero padded)
+  // byte strides between 4-column groups (K direction); rows are 16 B apart
+  static constexpr int G_KS = NT * 16;
+  static constexpr int U_KS = 128 * 16;
+  // fp16 core-gradient operands: 8 entries per 16-byte row chunk
+  static constexpr int PT_KS = MR * 16 + 16;   // +16: column writes hit distinct banks
+  static constexpr int ST_KS = KC * 16 + 16;
+  static constexpr int G_BYTES = (KT / 4) * G_KS;
+  static constexpr int U_BYTES = (KT / 4) * U_KS;
+  static constexpr int U1_BYTES = 128 * JP * 4;
+  static constexpr int PT_BYTES = 16 * PT_KS;  // 128 entries = 16 groups of 8
+  static constexpr int ST_BYTES = 16 * ST_KS;
+  // per warpgroup: P^T first (the M = 128 MMA reads rows MR..127 of the last
+  // column group past its end: they land in S^T / U tiles, and only feed the
+  // ignored core-gradient rows ab >= J^2)
+  static constexpr int WG_BYTES = PT_BYTES + ST_BYTES + 2 * U_BYTES + U1_BYTES;
+  static constexpr int FIXED_BYTES = 2 * G_BYTES + 2 * WG_BYTES;
+  static constexpr int FIXED_FLOATS = FIXED_BYTES / 4;
+  // tensor memory per warpgroup: T [0, NT), V [NT, 2 NT), dG [2 NT, 2 NT + KC)
+  static constexpr int TM_COLS = 2 * NT + KC;
+  static_assert(TM_COLS <= 256, "two warpgroups must fit in 512 TMEM columns");
+  static_assert(AB <= 128, "core-gradient MMA has M = 128 rows (a,b)");
+};
+
+template <int J>
+__global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
+  using L = TMLayout<J>;
+  constexpr int JP = L::JP, KT = L::KT, AB = L::AB, NT = L::NT;
+  constexpr int NW = 8;
+  extern __shared__ __align__(1024) float sm[];
+  uint8_t* smb = reinterpret_cast<uint8_t*>(sm);
+  uint8_t* Gc = smb;                 // B of T:  rows (a,b), K = c
+  uint8_t* Gb = smb + L::G_BYTES;    // B of V:  rows (a,c), K = b
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = threadIdx.x >> 7;    // warpgroup
+  const int e = threadIdx.x & 127;   // tile row = TMEM lane
+  uint8_t* wgb = smb + 2 * L::G_BYTES + g * L::WG_BYTES;
+  uint8_t* PT = wgb;
+  uint8_t* ST = PT + L::PT_BYTES;
+  uint8_t* tU2 = ST + L::ST_BYTES;
+  uint8_t* tU3 = tU2 + L::U_BYTES;
+  float* sU1 = reinterpret_cast<float*>(tU3 + L::U_BYTES);
+  __shared__ uint64_t mbar[2][2];    // [warpgroup][sweep MMAs, core MMA]
+  __shared__ uint32_t tmem_base;
+  __shared__ float red_kw[NW], red_lam[NW];
+
+  auto gc_off = [](int ab, int c) { return (c >> 2) * L::G_KS + ab * 16 + (c & 3) * 4; };
+
+  // ---- prologue: zero the operand tiles, core copies, TMEM, hot replicas ----
+  for (int q = threadIdx.x; q < L::FIXED_FLOATS; q += blockDim.x) sm[q] = 0.f;
+  __syncthreads();
+  for (int q = threadIdx.x; q < AB * J; q += blockDim.x) {
+    const int ab = q / J, c = q - (q / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
+    const float v = __ldcg(a.G + q);
+    *reinterpret_cast<float*>(Gc + gc_off(ab, c)) = v;
+    *reinterpret_cast<float*>(Gb + gc_off(ia * J + c, ib)) = v;
+  }
+  if (threadIdx.x == 0) {
+    umma::mbar_init(&mbar[0][0], 1);
+    umma::mbar_init(&mbar[0][1], 1);
+    umma::mbar_init(&mbar[1][0], 1);
+    umma::mbar_init(&mbar[1][1], 1);
+    umma::fence_mbar_init();
+  }
+  if (w == 0) umma::tmem_alloc<512>(&tmem_base);
+#pragma unroll
+  for (int n = 0; n < 3; ++n)
+    if (a.hot[n].H) load_hot<JP>(a.hot[n], a.U[n], sm + a.hot[n].off, sm + a.hot[n].stat_off);
+  for (int m = 0; m < a.n_mat; ++m)
+    if (a.mats[m].hotV.H)
+      load_hot<JP>(a.mats[m].hotV, a.mats[m].V, sm + a.mats[m].hotV.off,
+                   sm + a.mats[m].hotV.stat_off);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tm = tmem_base + (uint32_t)(g * 256);
+  const uint32_t tm_lane = (uint32_t)(32 * (w & 3)) << 16;
+  const uint32_t sPT = umma::smem_u32(PT), sST = umma::smem_u32(ST);
+  const uint32_t sU2 = umma::smem_u32(tU2), sU3 = umma::smem_u32(tU3);
+  const uint32_t sGc = umma::smem_u32(Gc), sGb = umma::smem_u32(Gb);
+  constexpr uint32_t ID_SWEEP = umma::idesc_tf32(128, NT, false, false);
+  constexpr uint32_t ID_CORE = umma::idesc_f16(128, L::KC);
+  constexpr float kSScale = 256.f;  // S^T = -r u3 * 2^8 in fp16
+
+  const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
+  const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
+  const uint64_t lo = a.nnz * gl / Wt, hi = a.nnz * (gl + 1) / Wt;
+  const uint64_t iters = (a.nnz + Wt - 1) / Wt;
+  const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
+  uint64_t mpos = mlo;
+  uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+  float kw = 0.f, lamG = 0.f;
+
+  const float* rep[3];
+  float* stat[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    rep[n] = sm + a.hot[n].off;
+    stat[n] = sm + a.hot[n].stat_off;
+  }
+  float* myU1 = sU1 + e * JP;
+  uint8_t* myU2 = tU2 + e * 16;  // chunk k4 at + k4 * U_KS
+  uint8_t* myU3 = tU3 + e * 16;
+
+  // records two ahead, slots and coefficients one ahead; the next entry's
+  // cold rows are copied (cp.async) straight into the operand tiles once the
+  // sweep MMAs of the current tile are done
+  auto issue_rows = [&](const uint4& r, const int* slx, bool act) {
+    if (act) {
+      if (slx[0] < 0) {
+        const float* src = a.U[0] + (uint64_t)r.x * JP;
+#pragma unroll
+        for (int k = 0; k < JP; k += 4) cp_async16(myU1 + k, src + k);
+      }
+      if (slx[1] < 0) {
+        const float* src = a.U[1] + (uint64_t)r.y * JP;
+#pragma unroll
+        for (int k = 0; k < JP; k += 4)
+          cp_async16(reinterpret_cast<float*>(myU2 + (k >> 2) * L::U_KS), src + k);
+      }
+      if (slx[2] < 0) {
+        const float* src = a.U[2] + (uint64_t)r.z * JP;
+#pragma unroll
+        for (int k = 0; k < JP; k += 4)
+          cp_async16(reinterpret_cast<float*>(myU3 + (k >> 2) * L::U_KS), src + k);
+      }
+    }
+    cp_async_commit();
+  };
+  uint4 rc = lo < hi ? __ldg(a.rec + lo) : make_uint4(0, 0, 0, 0);
+  uint4 rc1 = lo + 1 < hi ? __ldg(a.rec + lo + 1) : make_uint4(0, 0, 0, 0);
+  int sl[3];
+  float rg[3];
+  {
+    const uint32_t ix[3] = {rc.x, rc.y, rc.z};
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      sl[n] = (lo < hi && a.hot[n].slot) ? __ldg(a.hot[n].slot + ix[n]) : -1;
+      rg[n] = lo < hi ? __ldg(a.reg[n] + ix[n]) : 0.f;
+    }
+  }
+  issue_rows(rc, sl, lo < hi);
+  cp_async_commit();  // (empty) core-refresh group
+
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t e0 = lo + it;
+    const bool active = e0 < hi;
+    const uint32_t par = (uint32_t)(it & 1);
+    const uint4 rc2 = e0 + 2 < hi ? __ldg(a.rec + e0 + 2) : make_uint4(0, 0, 0, 0);
+    int nsl[3];
+    float nrg[3];
+    {
+      const bool nxt = e0 + 1 < hi;
+      const uint32_t nx[3] = {rc1.x, rc1.y, rc1.z};
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
+        nrg[n] = __ldg(a.reg[n] + (nxt ? nx[n] : 0u));
+      }
+    }
+
+    // ---- this entry's rows (cold ones landed in the tiles) ----
+    cp_async_wait_group<1>();
+    float u1[JP], u2[JP], u3[JP];
+    if (active) {
+      const float* s1 = sl[0] >= 0 ? rep[0] + sl[0] * JP : myU1;
+#pragma unroll
+      for (int k = 0; k < JP; k += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(s1 + k);
+        u1[k] = q.x; u1[k + 1] = q.y; u1[k + 2] = q.z; u1[k + 3] = q.w;
+      }
+#pragma unroll
+      for (int k = 0; k < JP; k += 4) {
+        float4* d2 = reinterpret_cast<float4*>(myU2 + (k >> 2) * L::U_KS);
+        float4* d3 = reinterpret_cast<float4*>(myU3 + (k >> 2) * L::U_KS);
+        float4 q2, q3;
+        if (sl[1] >= 0) {
+          q2 = *reinterpret_cast<const float4*>(rep[1] + sl[1] * JP + k);
+          *d2 = q2;
+        } else {
+          q2 = *d2;
+        }
+        if (sl[2] >= 0) {
+          q3 = *reinterpret_cast<const float4*>(rep[2] + sl[2] * JP + k);
+          *d3 = q3;
+        } else {
+          q3 = *d3;
+        }
+        u2[k] = q2.x; u2[k + 1] = q2.y; u2[k + 2] = q2.z; u2[k + 3] = q2.w;
+        u3[k] = q3.x; u3[k + 1] = q3.y; u3[k + 2] = q3.z; u3[k + 3] = q3.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < JP; ++k) u1[k] = u2[k] = u3[k] = 0.f;
+    }
+
+    // ---- P^T column (the previous tile's core MMA must be done with it) ----
+    if (it > 0) umma::mbar_wait(&mbar[g][1], par ^ 1u);
+    {
+      uint8_t* pcol = PT + (e >> 3) * L::PT_KS + (e & 7) * 2;
+#pragma unroll
+      for (int ia = 0; ia < J; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < J; ++ib)
+          *reinterpret_cast<__half*>(pcol + (ia * J + ib) * 16) = __float2half_rn(u1[ia] * u2[ib]);
+    }
+    umma::fence_async_smem();
+    umma::bar_sync(1 + g, 128);
+    if (e == 0) {
+      umma::fence_after();
+#pragma unroll
+      for (int ks = 0; ks < KT / 8; ++ks) {
+        umma::mma_tf32(tm, umma::desc(sU3 + ks * 2 * L::U_KS, L::U_KS, 128),
+                       umma::desc(sGc + ks * 2 * L::G_KS, L::G_KS, 128), ID_SWEEP, ks > 0);
+        umma::mma_tf32(tm + NT, umma::desc(sU2 + ks * 2 * L::U_KS, L::U_KS, 128),
+                       umma::desc(sGb + ks * 2 * L::G_KS, L::G_KS, 128), ID_SWEEP, ks > 0);
+      }
+      umma::commit(&mbar[g][0]);
+    }
+
+    // ---- contractions out of tensor memory (FP32) ----
+    float w1[J], g2[J], g3[J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) w1[k] = g2[k] = g3[k] = 0.f;
+    umma::mbar_wait(&mbar[g][0], par);
+    umma::fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < NT; c0 += 32) {
+      float v[32];
+      umma::ld16(tm + tm_lane + c0, v);
+      if (c0 + 16 < NT) umma::ld16(tm + tm_lane + c0 + 16, v + 16);
+      umma::ld_wait();
+      umma::ld_fence_regs<32>(v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int col = c0 + q;
+        if (col < AB) {
+          const int ia = col / J, ib = col % J;
+          w1[ia] = fmaf(v[q], u2[ib], w1[ia]);
+          g2[ib] = fmaf(v[q], u1[ia], g2[ib]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c0 = 0; c0 < NT; c0 += 32) {
+      float v[32];
+      umma::ld16(tm + tm_lane + NT + c0, v);
+      if (c0 + 16 < NT) umma::ld16(tm + tm_lane + NT + c0 + 16, v + 16);
+      umma::ld_wait();
+      umma::ld_fence_regs<32>(v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int col = c0 + q;
+        if (col < AB) {
+          const int ia = col / J, ic = col % J;
+          g3[ic] = fmaf(v[q], u1[ia], g3[ic]);
+        }
+      }
+    }
+#if CMTF_TM_EXACT  // diagnostics: the contractions in FP32 from the shared core copy
+#pragma unroll
+    for (int k = 0; k < J; ++k) w1[k] = g2[k] = g3[k] = 0.f;
+#pragma unroll 1
+    for (int ia = 0; ia < J; ++ia)
+#pragma unroll
+      for (int ib = 0; ib < J; ++ib) {
+        float tab = 0.f;
+        const float p = u1[ia] * u2[ib];
+#pragma unroll
+        for (int c = 0; c < J; ++c) {
+          const float gv = *reinterpret_cast<const float*>(Gc + gc_off(ia * J + ib, c));
+          tab = fmaf(gv, u3[c], tab);
+          g3[c] = fmaf(gv, p, g3[c]);
+        }
+        w1[ia] = fmaf(tab, u2[ib], w1[ia]);
+        g2[ib] = fmaf(tab, u1[ia], g2[ib]);
+      }
+#endif
+    float xh = 0.f;
+#pragma unroll
+    for (int k = 0; k < J; ++k) xh = fmaf(w1[k], u1[k], xh);
+
+    // ---- residual, row steps ----
+    const float r = active ? __uint_as_float(rc.w) - xh : 0.f;
+    {
+      float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < J; ++k) {
+        n1 = fmaf(u1[k], u1[k], n1); n2 = fmaf(u2[k], u2[k], n2); n3 = fmaf(u3[k], u3[k], n3);
+        c1 = fmaf(w1[k], w1[k], c1); c2 = fmaf(g2[k], g2[k], c2); c3 = fmaf(g3[k], g3[k], c3);
+      }
+      if (active) {
+        lamG += n1 * n2 * n3;
+        kw += 1.f;
+      }
+      float gr[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], rg[0] * u1[k]);
+      step_row_warp<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0],
+                           (int)a.hot[0].off, active, u1, gr, a.eta, a.nonneg, c1, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], rg[1] * u2[k]);
+      step_row_warp<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1],
+                           (int)a.hot[1].off, active, u2, gr, a.eta, a.nonneg, c2, lane);
+#pragma unroll
+      for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], rg[2] * u3[k]);
+      step_row_warp<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2],
+                           (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
+    }
+
+    // ---- S^T column (-r u3 at pre-update values), core-gradient MMA ----
+    {
+      uint8_t* scol = ST + (e >> 3) * L::ST_KS + (e & 7) * 2;
+#pragma unroll
+      for (int c = 0; c < J; ++c)
+        *reinterpret_cast<__half*>(scol + c * 16) =
+            __float2half_rn(fminf(fmaxf(-r * kSScale * u3[c], -65504.f), 65504.f));
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    umma::bar_sync(1 + g, 128);
+    if (e == 0) {
+      umma::fence_after();
+      const uint32_t acc0 = (it % (uint64_t)a.core_every) != 0 ? 1u : 0u;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        umma::mma_f16(tm + 2 * NT, umma::desc(sPT + ks * 2 * L::PT_KS, L::PT_KS, 128),
+                      umma::desc(sST + ks * 2 * L::ST_KS, L::ST_KS, 128), ID_CORE,
+                      ks > 0 ? 1u : acc0);
+      umma::commit(&mbar[g][1]);
+    }
+
+    // ---- next entry's rows into the tiles (the sweep MMAs are done) ----
+    issue_rows(rc1, nsl, e0 + 1 < hi);
+
+    // ---- matrix entries due by this iteration (interleaved) ----
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
+                                lane);
+
+    rc = rc1;
+    rc1 = rc2;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      sl[n] = nsl[n];
+      rg[n] = nrg[n];
+    }
+
+    // ---- periodic core push / refresh (block-level) ----
+    if ((it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters) {
+      const float kws = warp_sum(kw);
+      const float lgs = warp_sum(lamG);
+      if (lane == 0) {
+        red_kw[w] = kws;
+        red_lam[w] = lgs;
+      }
+      kw = 0.f;
+      lamG = 0.f;
+      // this warpgroup's accumulated gradient: TMEM lane e = row (a,b) -> the
+      // P^T buffer (free: the core MMA is done) as [ab][c]
+      umma::mbar_wait(&mbar[g][1], par);
+      umma::fence_after();
+      {
+        float v[16];
+        umma::ld16(tm + tm_lane + 2 * NT, v);
+        umma::ld_wait();
+        umma::ld_fence_regs<16>(v);
+        float* dg = reinterpret_cast<float*>(PT);
+        if (e < AB) {
+#pragma unroll
+          for (int c = 0; c < J; ++c) dg[e * J + c] = v[c] * (1.f / kSScale);
+        }
+      }
+      umma::fence_before();
+#if CMTF_TM_WGPUSH
+      // the warpgroup's own damped push: the two warpgroups run free
+      umma::bar_sync(1 + g, 128);
+      constexpr int PW = 4, PN = 128;
+      const int pw0 = 4 * g, pt = e;
+#else
+      __syncthreads();
+      constexpr int PW = NW, PN = 256;
+      const int pw0 = 0, pt = threadIdx.x;
+#endif
+      float kb = 0.f, lb = 0.f;
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        kb += red_kw[pw0 + q];
+        lb += red_lam[pw0 + q];
+      }
+      if (kb > 0.f) {
+        const float q = a.eta * (lb / kb) * a.nhat_core;
+        const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
+        const float s = -a.eta * alpha;
+#if CMTF_TM_WGPUSH
+        const float* dg0 = reinterpret_cast<const float*>(PT);
+#else
+        const float* dg0 = reinterpret_cast<const float*>(smb + 2 * L::G_BYTES);
+        const float* dg1 = reinterpret_cast<const float*>(smb + 2 * L::G_BYTES + L::WG_BYTES);
+#endif
+        for (int q2 = pt; q2 < AB * J; q2 += PN) {
+          const int ab = q2 / J, c = q2 - (q2 / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
+          float* gc = reinterpret_cast<float*>(Gc + gc_off(ab, c));
+          float* gb = reinterpret_cast<float*>(Gb + gc_off(ia * J + c, ib));
+#if CMTF_TM_WGPUSH
+          const float delta = s * fmaf(kb * a.core_reg, *gc, dg0[q2]);
+#else
+          const float delta = s * fmaf(kb * a.core_reg, *gc, dg0[q2] + dg1[q2]);
+#endif
+          if (a.nonneg) {
+            const float nv = atomic_add_clamp0(a.G + q2, delta);
+            *gc = nv;
+            *gb = nv;
+          } else {
+            red_add_f32(a.G + q2, delta);
+            cp_async4(gc, a.G + q2);
+            cp_async4(gb, a.G + q2);
+          }
+        }
+      }
+#if CMTF_TM_WGPUSH
+      umma::bar_sync(1 + g, 128);  // the P^T buffer is read before it is rewritten
+#else
+      __syncthreads();
+#endif
+    }
+    cp_async_commit();  // core refresh group (possibly empty)
+    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
+      flush_all_hot<J, JP, NW>(a, sm, w, lane);
+  }
+  matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
+  cp_async_wait_all();
+  umma::fence_before();
+  __syncthreads();
+  flush_all_hot<J, JP, NW>(a, sm, w, lane);
+  if (w == 0) umma::tmem_free<512>(tmem_base);
+}
+
+}  // namespace cmtfb

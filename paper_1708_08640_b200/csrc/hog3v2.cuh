@@ -120,6 +120,18 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+// p <- max(p + d, 0) atomically (nonnegative mode); returns the new value
+__device__ __forceinline__ float atomic_add_clamp0(float* p, float d) {
+  int* ip = reinterpret_cast<int*>(p);
+  int old = *ip, assumed;
+  float nv;
+  do {
+    assumed = old;
+    nv = fmaxf(__int_as_float(assumed) + d, 0.f);
+    old = atomicCAS(ip, assumed, __float_as_int(nv));
+  } while (old != assumed);
+  return nv;
+}
 __device__ __forceinline__ float ld_strong(const float* p) {
   float v;
   asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
@@ -958,7 +970,7 @@ hog3v2_kernel(Hog3v2Args a) {
             }
             const float delta = s * fmaf(kb * a.core_reg, Gs[o], sum);
             if (a.nonneg) {
-              Gs[o] = fmaxf(atomicAdd(a.G + e, delta) + delta, 0.f);
+              Gs[o] = atomic_add_clamp0(a.G + e, delta);
             } else {
               // fire-and-forget RED; the shared copy is refreshed from the
               // global core asynchronously (the read follows our RED to the

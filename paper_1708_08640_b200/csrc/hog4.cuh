@@ -660,7 +660,7 @@ hog4_kernel(Hog4Args a) {
             const int o = ((w * J + ib) * J + 2 * t4 + h) * JP + g8;
             const float delta = s * fmaf(kr, Gs[o], acc[ib][h]);
             if (a.nonneg) {
-              const float v = fmaxf(atomicAdd(a.G + o, delta) + delta, 0.f);
+              const float v = atomic_add_clamp0(a.G + o, delta);
               Gs[o] = v;
               if (TC) G1[((w * J + ib) * J + 2 * t4 + h) * L::S1 + g8] = v;
             } else {

@@ -310,19 +310,23 @@ def test_empty_matrix_is_allowed():
     assert np.isfinite(api.epoch_stats(st, 0.1).objective)
 
 
-def test_config2_rmse_within_1pct_of_reference():
+@pytest.mark.parametrize("tm", ["1", "0"])
+def test_config2_rmse_within_1pct_of_reference(tm, monkeypatch):
     """BASELINE configs[1] shape (Zipf 1.2 modes, clipped planted values,
     symmetric + 200-column coupled matrices) at 10% scale: 10 Hogwild epochs on
     the GPU vs the reference's own run (tests/golden/config2_s01_reference.json,
-    produced by scripts/oracle_config2.py with oracle/_ref, 6 threads)."""
+    produced by scripts/oracle_config2.py with oracle/_ref, 6 threads).
+    tm=1: the default tcgen05 kernel (hog3tm); tm=0: the CUDA-core hog3v2."""
     import json
     import os
     from conftest import GOLDEN
+    monkeypatch.setenv("CMTF_V3_TM", tm)
     ref = json.load(open(os.path.join(GOLDEN, "config2_s01_reference.json")))
     b, test, _ = synth.generate(synth.config2(0.1))
     st = api.make_state(TrainConfig(ranks=[10, 10, 10], eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
     for _ in range(10):
         api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == ("order3tm" if tm == "1" else "order3v2")
     tr = api.epoch_stats(st, 0.01).train_rmse
     te = api.test_rmse(st, test)
     assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
