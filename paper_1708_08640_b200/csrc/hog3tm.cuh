@@ -35,9 +35,6 @@
 #include "hog3v2.cuh"
 #include "umma.cuh"
 
-#ifndef CMTF_TM_WGPUSH
-#define CMTF_TM_WGPUSH 1  // each warpgroup pushes its own core gradient (no block barrier)
-#endif
 #ifndef CMTF_TM_EXACT
 #define CMTF_TM_EXACT 0
 #endif
@@ -65,7 +62,8 @@ struct TMLayout {
   static constexpr int U_BYTES = (KT / 4) * U_KS;
   static constexpr int U1_BYTES = 128 * JP * 4;
   static constexpr int PT_BYTES = 16 * PT_KS;  // 128 entries = 16 groups of 8
-  static constexpr int ST_BYTES = 16 * ST_KS;
+  // S^T also serves as the core push's transpose scratch (4 warps x 32 rows x J)
+  static constexpr int ST_BYTES = 16 * ST_KS > 4 * 32 * J * 4 ? 16 * ST_KS : 4 * 32 * J * 4;
   // per warpgroup: P^T first (the M = 128 MMA reads rows MR..127 of the last
   // column group past its end: they land in S^T / U tiles, and only feed the
   // ignored core-gradient rows ab >= J^2)
@@ -365,6 +363,19 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
                            (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
     }
 
+    // push statistics of this warpgroup; they cross the barrier below
+    const bool push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
+    if (push) {
+      const float kws = warp_sum(kw);
+      const float lgs = warp_sum(lamG);
+      if (lane == 0) {
+        red_kw[w] = kws;
+        red_lam[w] = lgs;
+      }
+      kw = 0.f;
+      lamG = 0.f;
+    }
+
     // ---- S^T column (-r u3 at pre-update values), core-gradient MMA ----
     {
       uint8_t* scol = ST + (e >> 3) * L::ST_KS + (e & 7) * 2;
@@ -402,83 +413,52 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       rg[n] = nrg[n];
     }
 
-    // ---- periodic core push / refresh (block-level) ----
-    if ((it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters) {
-      const float kws = warp_sum(kw);
-      const float lgs = warp_sum(lamG);
-      if (lane == 0) {
-        red_kw[w] = kws;
-        red_lam[w] = lgs;
-      }
-      kw = 0.f;
-      lamG = 0.f;
-      // this warpgroup's accumulated gradient: TMEM lane e = row (a,b) -> the
-      // P^T buffer (free: the core MMA is done) as [ab][c]
-      umma::mbar_wait(&mbar[g][1], par);
-      umma::fence_after();
-      {
-        float v[16];
-        umma::ld16(tm + tm_lane + 2 * NT, v);
-        umma::ld_wait();
-        umma::ld_fence_regs<16>(v);
-        float* dg = reinterpret_cast<float*>(PT);
-        if (e < AB) {
-#pragma unroll
-          for (int c = 0; c < J; ++c) dg[e * J + c] = v[c] * (1.f / kSScale);
-        }
-      }
-      umma::fence_before();
-#if CMTF_TM_WGPUSH
-      // the warpgroup's own damped push: the two warpgroups run free
-      umma::bar_sync(1 + g, 128);
-      constexpr int PW = 4, PN = 128;
-      const int pw0 = 4 * g, pt = e;
-#else
-      __syncthreads();
-      constexpr int PW = NW, PN = 256;
-      const int pw0 = 0, pt = threadIdx.x;
-#endif
+    // ---- periodic core push / refresh (per warpgroup, no block barrier).
+    // TMEM lane e holds core row (a,b) = e; each warp transposes its 32 rows
+    // through its slice of the S^T buffer (free until the next barrier) so the
+    // REDs to the global core are coalesced ----
+    if (push) {
       float kb = 0.f, lb = 0.f;
 #pragma unroll
-      for (int q = 0; q < PW; ++q) {
-        kb += red_kw[pw0 + q];
-        lb += red_lam[pw0 + q];
+      for (int q = 0; q < 4; ++q) {
+        kb += red_kw[4 * g + q];
+        lb += red_lam[4 * g + q];
       }
-      if (kb > 0.f) {
+      umma::mbar_wait(&mbar[g][1], par);
+      umma::fence_after();
+      float v[16];
+      umma::ld16(tm + tm_lane + 2 * NT, v);
+      umma::ld_wait();
+      umma::ld_fence_regs<16>(v);
+      float* scr = reinterpret_cast<float*>(ST) + (w & 3) * (32 * J);
+#pragma unroll
+      for (int c = 0; c < J; ++c) scr[lane * J + c] = v[c] * (1.f / kSScale);
+      __syncwarp();
+      const int row0 = 32 * (w & 3);
+      if (kb > 0.f && row0 < AB) {
         const float q = a.eta * (lb / kb) * a.nhat_core;
         const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
         const float s = -a.eta * alpha;
-#if CMTF_TM_WGPUSH
-        const float* dg0 = reinterpret_cast<const float*>(PT);
-#else
-        const float* dg0 = reinterpret_cast<const float*>(smb + 2 * L::G_BYTES);
-        const float* dg1 = reinterpret_cast<const float*>(smb + 2 * L::G_BYTES + L::WG_BYTES);
-#endif
-        for (int q2 = pt; q2 < AB * J; q2 += PN) {
-          const int ab = q2 / J, c = q2 - (q2 / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
+        const float creg = kb * a.core_reg;
+        const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
+        float* Gw = a.G + row0 * J;
+        for (int m = lane; m < nval; m += 32) {
+          const int ab = row0 + m / J, c = m - (m / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
           float* gc = reinterpret_cast<float*>(Gc + gc_off(ab, c));
           float* gb = reinterpret_cast<float*>(Gb + gc_off(ia * J + c, ib));
-#if CMTF_TM_WGPUSH
-          const float delta = s * fmaf(kb * a.core_reg, *gc, dg0[q2]);
-#else
-          const float delta = s * fmaf(kb * a.core_reg, *gc, dg0[q2] + dg1[q2]);
-#endif
+          const float delta = s * fmaf(creg, *gc, scr[m]);
           if (a.nonneg) {
-            const float nv = atomic_add_clamp0(a.G + q2, delta);
+            const float nv = atomic_add_clamp0(Gw + m, delta);
             *gc = nv;
             *gb = nv;
           } else {
-            red_add_f32(a.G + q2, delta);
-            cp_async4(gc, a.G + q2);
-            cp_async4(gb, a.G + q2);
+            red_add_f32(Gw + m, delta);
+            cp_async4(gc, Gw + m);
+            cp_async4(gb, Gw + m);
           }
         }
       }
-#if CMTF_TM_WGPUSH
-      umma::bar_sync(1 + g, 128);  // the P^T buffer is read before it is rewritten
-#else
-      __syncthreads();
-#endif
+      umma::fence_before();
     }
     cp_async_commit();  // core refresh group (possibly empty)
     if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
