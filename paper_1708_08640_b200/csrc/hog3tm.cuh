@@ -35,6 +35,12 @@
 #include "hog3v2.cuh"
 #include "umma.cuh"
 
+#ifndef CMTF_TM_REFRESH
+#define CMTF_TM_REFRESH 4  // pushes between refreshes of the shared core copies
+#endif
+#ifndef CMTF_TM_PROF
+#define CMTF_TM_PROF 0
+#endif
 #ifndef CMTF_TM_EXACT
 #define CMTF_TM_EXACT 0
 #endif
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   constexpr uint32_t ID_SWEEP = umma::idesc_tf32(128, NT, false, false);
   constexpr uint32_t ID_CORE = umma::idesc_f16(128, L::KC);
   constexpr float kSScale = 256.f;  // S^T = -r u3 * 2^8 in fp16
+  constexpr uint32_t kRefresh = CMTF_TM_REFRESH;
 
   const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
   const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
@@ -153,6 +160,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     rep[n] = sm + a.hot[n].off;
     stat[n] = sm + a.hot[n].stat_off;
   }
+  // core row (a,b) = e of this thread in the two shared core copies
+  const int ia_e = e / J, ib_e = e - (e / J) * J;
+  const int gb_row = (ib_e >> 2) * L::G_KS + (ib_e & 3) * 4;
+  uint32_t npush = 0;
   float* myU1 = sU1 + e * JP;
   uint8_t* myU2 = tU2 + e * 16;  // chunk k4 at + k4 * U_KS
   uint8_t* myU3 = tU3 + e * 16;
@@ -197,6 +208,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   issue_rows(rc, sl, lo < hi);
   cp_async_commit();  // (empty) core-refresh group
 
+#if CMTF_TM_PROF
+  long long tprof[12] = {0};
+  long long tlast = clock64();
+#define TMP(k) do { const long long tn = clock64(); tprof[k] += tn - tlast; tlast = tn; } while (0)
+#else
+#define TMP(k) do {} while (0)
+#endif
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e0 = lo + it;
     const bool active = e0 < hi;
@@ -260,6 +278,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
           *reinterpret_cast<__half*>(pcol + (ia * J + ib) * 16) = __float2half_rn(u1[ia] * u2[ib]);
     }
     umma::fence_async_smem();
+    TMP(0);
     umma::bar_sync(1 + g, 128);
     if (e == 0) {
       umma::fence_after();
@@ -273,11 +292,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       umma::commit(&mbar[g][0]);
     }
 
+    TMP(1);
     // ---- contractions out of tensor memory (FP32) ----
     float w1[J], g2[J], g3[J];
 #pragma unroll
     for (int k = 0; k < J; ++k) w1[k] = g2[k] = g3[k] = 0.f;
     umma::mbar_wait(&mbar[g][0], par);
+    TMP(2);
     umma::fence_after();
 #pragma unroll
     for (int c0 = 0; c0 < NT; c0 += 32) {
@@ -335,6 +356,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #pragma unroll
     for (int k = 0; k < J; ++k) xh = fmaf(w1[k], u1[k], xh);
 
+    TMP(3);
     // ---- residual, row steps ----
     const float r = active ? __uint_as_float(rc.w) - xh : 0.f;
     {
@@ -363,6 +385,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
                            (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
     }
 
+    TMP(4);
     // push statistics of this warpgroup; they cross the barrier below
     const bool push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
     if (push) {
@@ -398,13 +421,16 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       umma::commit(&mbar[g][1]);
     }
 
+    TMP(5);
     // ---- next entry's rows into the tiles (the sweep MMAs are done) ----
     issue_rows(rc1, nsl, e0 + 1 < hi);
 
+    TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----
     matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
                                 lane);
 
+    TMP(7);
     rc = rc1;
     rc1 = rc2;
 #pragma unroll
@@ -413,6 +439,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       rg[n] = nrg[n];
     }
 
+    TMP(8);
     // ---- periodic core push / refresh (per warpgroup, no block barrier).
     // TMEM lane e holds core row (a,b) = e; each warp transposes its 32 rows
     // through its slice of the S^T buffer (free until the next barrier) so the
@@ -431,38 +458,51 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       umma::ld_wait();
       umma::ld_fence_regs<16>(v);
       float* scr = reinterpret_cast<float*>(ST) + (w & 3) * (32 * J);
-#pragma unroll
-      for (int c = 0; c < J; ++c) scr[lane * J + c] = v[c] * (1.f / kSScale);
-      __syncwarp();
       const int row0 = 32 * (w & 3);
       if (kb > 0.f && row0 < AB) {
         const float q = a.eta * (lb / kb) * a.nhat_core;
         const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
         const float s = -a.eta * alpha;
         const float creg = kb * a.core_reg;
-        const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
-        float* Gw = a.G + row0 * J;
-        for (int m = lane; m < nval; m += 32) {
-          const int ab = row0 + m / J, c = m - (m / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
-          float* gc = reinterpret_cast<float*>(Gc + gc_off(ab, c));
-          float* gb = reinterpret_cast<float*>(Gb + gc_off(ia * J + c, ib));
-          const float delta = s * fmaf(creg, *gc, scr[m]);
-          if (a.nonneg) {
-            const float nv = atomic_add_clamp0(Gw + m, delta);
-            *gc = nv;
-            *gb = nv;
-          } else {
-            red_add_f32(Gw + m, delta);
-            cp_async4(gc, Gw + m);
-            cp_async4(gb, Gw + m);
+        float* Grow = a.G + e * J;
+        // the shared copies follow the global core every kRefresh pushes
+        // (and right away in nonnegative mode)
+        const bool refresh = ++npush % kRefresh == 0;
+        if (e < AB) {
+          // row owner: the gradient of its row plus the regulariser, and the
+          // refresh of its row in both shared copies
+#pragma unroll
+          for (int c = 0; c < J; ++c) {
+            float* gc = reinterpret_cast<float*>(Gc + gc_off(e, c));
+            float* gb = reinterpret_cast<float*>(Gb + gb_row + (ia_e * J + c) * 16);
+            const float gr = fmaf(creg, *gc, v[c] * (1.f / kSScale));
+            if (a.nonneg) {
+              const float nv = atomic_add_clamp0(Grow + c, s * gr);
+              *gc = nv;
+              *gb = nv;
+            } else {
+              scr[lane * J + c] = gr;
+              if (refresh) {
+                cp_async4(gc, Grow + c);
+                cp_async4(gb, Grow + c);
+              }
+            }
           }
+        }
+        __syncwarp();
+        if (!a.nonneg) {  // coalesced REDs of the warp's 32 rows
+          const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
+          float* Gw = a.G + row0 * J;
+          for (int m = lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
         }
       }
       umma::fence_before();
     }
+    TMP(9);
     cp_async_commit();  // core refresh group (possibly empty)
     if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
       flush_all_hot<J, JP, NW>(a, sm, w, lane);
+    TMP(10);
   }
   matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
   cp_async_wait_all();
@@ -470,6 +510,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);
   if (w == 0) umma::tmem_free<512>(tmem_base);
+#if CMTF_TM_PROF
+  if (blockIdx.x == 0 && (threadIdx.x & 127) == 0)
+    printf("prof wg%d iters %llu: wait+tiles+PT %lld | bar1+issue %lld | mma wait %lld | contract %lld | "
+           "rowsteps %lld | ST+bar2+issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld\n",
+           g, (unsigned long long)iters, tprof[0], tprof[1], tprof[2], tprof[3], tprof[4], tprof[5],
+           tprof[6], tprof[7], tprof[8], tprof[9], tprof[10]);
+#endif
 }
 
 }  // namespace cmtfb
