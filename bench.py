@@ -296,7 +296,7 @@ def run_ours(args):
     # --set full capture of the same command (profiles/ncu_r1_metrics.json)
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_r1_metrics.json")))
-        key = {"order3v2": "hog3v2", "order4": "hog4"}.get(info["kernel"])
+        key = {"order3v2": "hog3v2", "order3tm": "hog3tm", "order4": "hog4"}.get(info["kernel"])
         for k, v in prof.items():
             scale_ok = (f"scale {args.scale:g}" in k) if "scale" in k else args.scale == 1.0
             if key and k.startswith(key) and args.config in k.replace("(", " ").split() and scale_ok:
