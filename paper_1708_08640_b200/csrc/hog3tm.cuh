@@ -38,6 +38,9 @@
 #ifndef CMTF_TM_REFRESH
 #define CMTF_TM_REFRESH 4  // pushes between refreshes of the shared core copies
 #endif
+#ifndef CMTF_TM_MPF
+#define CMTF_TM_MPF 0  // matrix entries with prefetched rows (measured slower: +3.5%)
+#endif
 #ifndef CMTF_TM_PROF
 #define CMTF_TM_PROF 0
 #endif
@@ -150,7 +153,12 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   const uint64_t iters = (a.nnz + Wt - 1) / Wt;
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
+#if CMTF_TM_MPF
+  MatPrefetch mpf;
+  mat_prefetch_init<JP>(a, mpf, mlo, mhi);
+#else
   uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+#endif
   float kw = 0.f, lamG = 0.f;
 
   const float* rep[3];
@@ -427,8 +435,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----
+#if CMTF_TM_MPF
+    matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
+                                   lane);
+#else
     matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
                                 lane);
+#endif
 
     TMP(7);
     rc = rc1;
@@ -504,7 +517,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       flush_all_hot<J, JP, NW>(a, sm, w, lane);
     TMP(10);
   }
+#if CMTF_TM_MPF
+  matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mhi, mhi, lane);
+#else
   matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
+#endif
   cp_async_wait_all();
   umma::fence_before();
   __syncthreads();

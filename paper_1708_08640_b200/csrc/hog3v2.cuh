@@ -567,6 +567,90 @@ __device__ __forceinline__ void matrix_entry(const Args& a, float* sm, const uin
                        a.eta, a.nonneg, M.weight * nu, lane);
 }
 
+// Prefetching variant (hog3tm): the next entry's record, row slots and global
+// rows are in registers before it is due, so an entry costs no L2 round trip
+// (matrix entries come every few iterations; a cold row read is up to that
+// stale, hot rows are read from the replica at use time).
+struct MatPrefetch {
+  uint4 mr;       // next entry's record
+  uint4 mr2;      // the one after
+  int su, sv;     // hot slots of its rows
+  float4 u[3], v[3];
+};
+
+template <int JP, class Args>
+__device__ __forceinline__ void mat_prefetch_rows(const Args& a, MatPrefetch& p, bool valid) {
+  const MatDesc3& M = a.mats[valid ? p.mr.w : 0];
+  const int mode = M.mode;
+  const uint32_t i = valid ? p.mr.x : 0u, j = valid ? p.mr.y : 0u;
+  p.su = valid && a.hot[mode].slot ? __ldg(a.hot[mode].slot + i) : -1;
+  p.sv = valid && M.hotV.slot ? __ldg(M.hotV.slot + j) : -1;
+#pragma unroll
+  for (int k = 0; k < JP / 4; ++k) {
+    p.u[k] = ld_weak4(a.U[mode] + (uint64_t)i * JP + 4 * k);
+    p.v[k] = ld_weak4(M.V + (uint64_t)j * JP + 4 * k);
+  }
+}
+
+template <int JP, class Args>
+__device__ __forceinline__ void mat_prefetch_init(const Args& a, MatPrefetch& p, uint64_t mlo,
+                                                  uint64_t mhi) {
+  p.mr = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+  p.mr2 = mlo + 1 < mhi ? __ldg(a.mrec + mphys(a, mlo + 1)) : make_uint4(0, 0, 0, 0);
+  mat_prefetch_rows<JP>(a, p, mlo < mhi);
+}
+
+template <int J, int JP, class Args>
+__device__ __forceinline__ void matrix_entries_until_pf(const Args& a, float* sm, uint64_t& mpos,
+                                                        MatPrefetch& p, uint64_t due,
+                                                        uint64_t mhi, int lane) {
+  static_assert(JP <= 12, "prefetch holds rows of up to 12 floats");
+  while (__any_sync(0xffffffffu, mpos < due)) {
+    const bool has = mpos < due;
+    const uint4 mr = p.mr;
+    const MatDesc3& M = a.mats[has ? mr.w : 0];
+    const int mode = M.mode;
+    const int su = has ? p.su : -1, sv = has ? p.sv : -1;
+    float uu[JP], vv[JP];
+    float* repU = sm + a.hot[mode].off;
+    float* repV = sm + M.hotV.off;
+#pragma unroll
+    for (int k = 0; k < JP / 4; ++k) {
+      float4 qu = p.u[k], qv = p.v[k];
+      if (su >= 0) qu = *reinterpret_cast<const float4*>(repU + su * JP + 4 * k);
+      if (sv >= 0) qv = *reinterpret_cast<const float4*>(repV + sv * JP + 4 * k);
+      if (!has) qu = qv = make_float4(0.f, 0.f, 0.f, 0.f);
+      uu[4 * k] = qu.x; uu[4 * k + 1] = qu.y; uu[4 * k + 2] = qu.z; uu[4 * k + 3] = qu.w;
+      vv[4 * k] = qv.x; vv[4 * k + 1] = qv.y; vv[4 * k + 2] = qv.z; vv[4 * k + 3] = qv.w;
+    }
+    if (has) {  // advance: the record after next, and the next entry's rows
+      ++mpos;
+      p.mr = p.mr2;
+      if (mpos + 1 < mhi) p.mr2 = __ldg(a.mrec + mphys(a, mpos + 1));
+      mat_prefetch_rows<JP>(a, p, mpos < mhi);
+    }
+    float yh = 0.f, nu = 0.f, nv = 0.f;
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      yh = fmaf(uu[k], vv[k], yh);
+      nu = fmaf(uu[k], uu[k], nu);
+      nv = fmaf(vv[k], vv[k], nv);
+    }
+    const float rr = has ? __uint_as_float(mr.z) - yh : 0.f;
+    const float vr = has ? __ldg(M.vreg + mr.y) : 0.f;
+    float du[J], dv[J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      du[k] = -M.weight * rr * vv[k];
+      dv[k] = fmaf(-M.weight * rr, uu[k], vr * vv[k]);
+    }
+    step_row_warp<J, JP>(a.U[mode], mr.x, su, repU, sm + a.hot[mode].stat_off,
+                         (int)a.hot[mode].off, has, uu, du, a.eta, a.nonneg, M.weight * nv, lane);
+    step_row_warp<J, JP>(M.V, mr.y, sv, repV, sm + M.hotV.stat_off, (int)M.hotV.off, has, vv, dv,
+                         a.eta, a.nonneg, M.weight * nu, lane);
+  }
+}
+
 // Matrix entries of this lane up to `due`, in lockstep across the warp.
 template <int J, int JP, class Args>
 __device__ __forceinline__ void matrix_entries_until(const Args& a, float* sm, uint64_t& mpos,
