@@ -156,6 +156,13 @@ struct cmtf_gpu_ctx {
   uint64_t partial_cap = 0;
   unsigned long long* d_first = nullptr;
 
+  // device-side hot-row selection scratch
+  unsigned long long* hs_keys = nullptr;  // [2][cap]
+  uint64_t hs_keys_cap = 0;
+  uint8_t* hs_tmp = nullptr;
+  uint64_t hs_tmp_cap = 0;
+  uint32_t* hs_cnt = nullptr;  // [1 + 16]: candidate count, per-array H
+
   // v2 sweep state (built lazily after a bundle change)
   bool v2_dirty = true;
   uint4* mrec = nullptr;  // merged matrix records {row, col, bits(y), m}, random order
@@ -890,9 +897,75 @@ size_t v2_fixed_bytes_rt(int J, V2Shape sh) {
   return 0;
 }
 
+// ---------------------------------------------------------------------
+// Device-side hot-row selection (the host path below is the reference for
+// it): candidates are rows with count >= thr, ordered by count descending,
+// then array (modes, then matrices), then row -- the order of the host's
+// stable sort -- via one 64-bit radix key ((~count) << 32 | arr << 28 | row).
+// ---------------------------------------------------------------------
+struct HotArrays {
+  const uint32_t* count[16];
+  uint32_t n[16];
+  int32_t* slot[16];
+  uint32_t* row_of[16];
+  uint32_t start[16];
+  int narr;
+};
+
+__global__ void hot_cand_kernel(HotArrays h, uint64_t thr, unsigned long long* keys,
+                                uint32_t* ncand, bool write) {
+  const int arr = blockIdx.y;
+  if (arr >= h.narr) return;
+  const uint32_t* c = h.count[arr];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h.n[arr];
+       i += gridDim.x * blockDim.x) {
+    const uint32_t v = c[i];
+    if (v >= thr) {
+      const uint32_t q = atomicAdd(ncand, 1u);
+      if (write)
+        keys[q] = ((unsigned long long)(0xffffffffu - v) << 32) |
+                  ((unsigned long long)arr << 28) | i;
+    }
+  }
+}
+
+__global__ void hot_count_kernel(const unsigned long long* keys, uint64_t take, uint32_t* H,
+                                 unsigned long long* keys2) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < take;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t arr = (uint32_t)(keys[q] >> 28) & 15u;
+    atomicAdd(H + arr, 1u);
+    keys2[q] = ((unsigned long long)arr << 32) | q;  // group by array, keep rank order
+  }
+}
+
+__global__ void hot_assign_kernel(const unsigned long long* keys, const unsigned long long* keys2,
+                                  uint64_t take, HotArrays h) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < take;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t arr = (uint32_t)(keys2[x] >> 32);
+    const uint32_t q = (uint32_t)keys2[x];
+    const uint32_t row = (uint32_t)keys[q] & ((1u << 28) - 1u);
+    const uint32_t slot = (uint32_t)x - h.start[arr];
+    h.row_of[arr][slot] = row;
+    h.slot[arr][row] = (int32_t)slot;
+  }
+}
+
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
+  static const bool ptime = std::getenv("CMTF_PREP_TIMING") != nullptr;
+  auto pt0 = std::chrono::steady_clock::now();
+  auto ptick = [&](const char* what) {
+    if (!ptime) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "prepare_v2 %-12s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - pt0).count());
+    pt0 = t;
+  };
   drain_side(ctx);  // mrec is rebuilt below
+  ptick("drain");
   const uint32_t JP = (uint32_t)round_up4(J);
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
@@ -950,6 +1023,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     CU(cudaGetLastError());
   }
 
+  ptick("merge");
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
@@ -974,54 +1048,17 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   }
   const size_t limit = 227 * 1024 - 2048;  // room for a co-resident gather block
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
-  struct Cand {
-    uint32_t count;
-    int arr;  // 0..N-1 modes, 100+m matrices
-    uint32_t row;
-  };
-  std::vector<Cand> cand;
-  std::vector<std::vector<uint32_t>> hcounts(ctx->order), vcounts(ctx->mats.size());
   const uint64_t thr = tau > 0 ? (uint64_t)std::ceil(tau * (double)ctx->nnz / W) : ~0ull;
-  for (int n = 0; n < ctx->order; ++n) {
-    hcounts[n].resize(ctx->dims[n]);
-    CU(cudaMemcpy(hcounts[n].data(), ctx->count[n], ctx->dims[n] * sizeof(uint32_t),
-                  cudaMemcpyDeviceToHost));
-    if (tau > 0)
-      for (uint32_t i = 0; i < ctx->dims[n]; ++i)
-        if (hcounts[n][i] >= std::max<uint64_t>(thr, 1)) cand.push_back({hcounts[n][i], n, i});
-  }
-  for (size_t m = 0; m < ctx->mats.size(); ++m) {
-    const auto& M = ctx->mats[m];
-    vcounts[m].resize(M.cols);
-    CU(cudaMemcpy(vcounts[m].data(), M.count, M.cols * sizeof(uint32_t),
-                  cudaMemcpyDeviceToHost));
-    // a V row's updates are spread over the same iterations as the tensor's
-    if (tau > 0)
-      for (uint32_t j = 0; j < M.cols; ++j)
-        if (vcounts[m][j] >= std::max<uint64_t>(thr, 1))
-          cand.push_back({vcounts[m][j], 100 + (int)m, j});
-  }
-  std::stable_sort(cand.begin(), cand.end(),
-                   [](const Cand& x, const Cand& y) { return x.count > y.count; });
   const size_t per_row = JP + 3;
   const size_t slack = 4 * (ctx->order + ctx->mats.size());  // alignment padding
-  size_t take = std::min(cand.size(), budget_floats > slack ? (budget_floats - slack) / per_row : 0);
-  std::vector<std::vector<uint32_t>> rows_of(ctx->order), vrows_of(ctx->mats.size());
-  for (size_t q = 0; q < take; ++q) {
-    if (cand[q].arr < 100) rows_of[cand[q].arr].push_back(cand[q].row);
-    else vrows_of[cand[q].arr - 100].push_back(cand[q].row);
-  }
+  const uint64_t max_take = budget_floats > slack ? (budget_floats - slack) / per_row : 0;
   uint32_t off = (uint32_t)(fixed / sizeof(float));
-  auto build = [&](cmtf_gpu_ctx::HotHost& h, const std::vector<uint32_t>& rows,
-                   uint32_t nrows) -> int {
-    h.H = (uint32_t)rows.size();
+  // per-array replica layout and device tables for H hot rows
+  auto place = [&](cmtf_gpu_ctx::HotHost& h, uint32_t H, uint32_t nrows) -> int {
+    h.H = H;
     if (!h.H) return CMTF_OK;
-    std::vector<int32_t> slot(nrows, -1);
-    for (uint32_t s = 0; s < h.H; ++s) slot[rows[s]] = (int32_t)s;
     TRY(ensure(ctx, &h.slot, &h.slot_cap, nrows));
     TRY(ensure(ctx, &h.row_of, &h.row_cap, h.H));
-    CU(cudaMemcpy(h.slot, slot.data(), nrows * sizeof(int32_t), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(h.row_of, rows.data(), h.H * sizeof(uint32_t), cudaMemcpyHostToDevice));
     const uint64_t need = (uint64_t)blocks * h.H * JP;
     if (h.base_cap < need) {
       TRY(dalloc(ctx, &h.base, need));
@@ -1033,9 +1070,183 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     off += (3 * h.H + 3) & ~3u;
     return CMTF_OK;
   };
-  for (int n = 0; n < ctx->order; ++n) TRY(build(ctx->hot[n], rows_of[n], ctx->dims[n]));
-  for (size_t m = 0; m < ctx->mats.size(); ++m)
-    TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
+  bool device_sel = !std::getenv("CMTF_HOT_HOST") && ctx->order + ctx->mats.size() <= 16 &&
+                    ctx->order <= 8;
+  for (int n = 0; n < ctx->order; ++n) device_sel = device_sel && ctx->dims[n] < (1u << 28);
+  for (auto& M : ctx->mats) device_sel = device_sel && M.cols < (1u << 28);
+  if (device_sel) {
+    HotArrays ha{};
+    ha.narr = 16;
+    for (int n = 0; n < ctx->order; ++n) {
+      ha.count[n] = ctx->count[n];
+      ha.n[n] = tau > 0 ? ctx->dims[n] : 0;
+    }
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      ha.count[8 + m] = ctx->mats[m].count;
+      ha.n[8 + m] = tau > 0 ? ctx->mats[m].cols : 0;
+    }
+    if (!ctx->hs_cnt) TRY(dalloc(ctx, &ctx->hs_cnt, 17));
+    uint32_t hcnt[17] = {0};
+    CU(cudaMemsetAsync(ctx->hs_cnt, 0, 17 * sizeof(uint32_t), ctx->stream));
+    const uint64_t th = std::max<uint64_t>(thr, 1);
+    hot_cand_kernel<<<dim3(64, 16), 256, 0, ctx->stream>>>(ha, th, nullptr, ctx->hs_cnt, false);
+    CU(cudaMemcpyAsync(hcnt, ctx->hs_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const uint64_t ncand = hcnt[0];
+    const uint64_t take = std::min<uint64_t>(ncand, max_take);
+    uint32_t H[16] = {0};
+    if (take) {
+      // [0, n): candidates, then (array, rank) keys; [n, 2n): sorted
+      // candidates; [2n, 3n): sorted (array, rank) keys
+      TRY(ensure(ctx, &ctx->hs_keys, &ctx->hs_keys_cap, 3 * ncand));
+      unsigned long long* k_in = ctx->hs_keys;
+      unsigned long long* k_out = ctx->hs_keys + ncand;
+      CU(cudaMemsetAsync(ctx->hs_cnt, 0, 17 * sizeof(uint32_t), ctx->stream));
+      hot_cand_kernel<<<dim3(64, 16), 256, 0, ctx->stream>>>(ha, th, k_in, ctx->hs_cnt, true);
+      size_t tb = 0;
+      CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, k_in, k_out, (int)ncand, 0, 64,
+                                        ctx->stream));
+      TRY(ensure(ctx, &ctx->hs_tmp, &ctx->hs_tmp_cap, tb));
+      CU(cub::DeviceRadixSort::SortKeys(ctx->hs_tmp, tb, k_in, k_out, (int)ncand, 0, 64,
+                                        ctx->stream));
+      // k_out = sorted candidates; k_in is reused for the (array, rank) keys
+      hot_count_kernel<<<grid_for(take), 256, 0, ctx->stream>>>(k_out, take, ctx->hs_cnt + 1,
+                                                                k_in);
+      CU(cudaMemcpyAsync(H, ctx->hs_cnt + 1, 16 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
+    uint32_t start = 0;
+    for (int n = 0; n < ctx->order; ++n) {
+      TRY(place(ctx->hot[n], H[n], ctx->dims[n]));
+      ha.slot[n] = ctx->hot[n].slot;
+      ha.row_of[n] = ctx->hot[n].row_of;
+      ha.start[n] = start;
+      start += H[n];
+      if (H[n]) CU(cudaMemsetAsync(ctx->hot[n].slot, 0xff, ctx->dims[n] * sizeof(int32_t),
+                                   ctx->stream));
+    }
+    for (int n = ctx->order; n < 8; ++n) ha.start[n] = start;
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      TRY(place(ctx->hotV[m], H[8 + m], ctx->mats[m].cols));
+      ha.slot[8 + m] = ctx->hotV[m].slot;
+      ha.row_of[8 + m] = ctx->hotV[m].row_of;
+      ha.start[8 + m] = start;
+      start += H[8 + m];
+      if (H[8 + m]) CU(cudaMemsetAsync(ctx->hotV[m].slot, 0xff, ctx->mats[m].cols * sizeof(int32_t),
+                                       ctx->stream));
+    }
+    if (take) {
+      size_t tb = 0;
+      unsigned long long* k2_in = ctx->hs_keys;
+      unsigned long long* k_sorted = ctx->hs_keys + ncand;
+      unsigned long long* k2_out = ctx->hs_keys + 2 * ncand;
+      CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, k2_in, k2_out, (int)take, 0, 36,
+                                        ctx->stream));
+      TRY(ensure(ctx, &ctx->hs_tmp, &ctx->hs_tmp_cap, tb));
+      CU(cub::DeviceRadixSort::SortKeys(ctx->hs_tmp, tb, k2_in, k2_out, (int)take, 0, 36,
+                                        ctx->stream));
+      hot_assign_kernel<<<grid_for(take), 256, 0, ctx->stream>>>(k_sorted, k2_out, take, ha);
+      CU(cudaGetLastError());
+    }
+    if (std::getenv("CMTF_HOT_CHECK")) {
+      // test hook: the host's stable-sort selection must give the same rows
+      // in the same slots
+      struct C2 { uint32_t count; int arr; uint32_t row; };
+      std::vector<C2> cand;
+      std::vector<std::vector<uint32_t>> cnt(16);
+      for (int a = 0; a < 16; ++a) {
+        if (!ha.n[a]) continue;
+        cnt[a].resize(ha.n[a]);
+        CU(cudaMemcpy(cnt[a].data(), ha.count[a], ha.n[a] * sizeof(uint32_t),
+                      cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < ha.n[a]; ++i)
+          if (cnt[a][i] >= th) cand.push_back({cnt[a][i], a, i});
+      }
+      std::stable_sort(cand.begin(), cand.end(),
+                       [](const C2& x, const C2& y) { return x.count > y.count; });
+      std::vector<std::vector<uint32_t>> want(16);
+      for (uint64_t q = 0; q < std::min<uint64_t>(cand.size(), max_take); ++q)
+        want[cand[q].arr].push_back(cand[q].row);
+      for (int a = 0; a < 16; ++a) {
+        if (want[a].size() != H[a])
+          return set_err(ctx, CMTF_ECUDA, "hot check: array %d has %u rows, host %zu", a, H[a],
+                         want[a].size());
+        if (!H[a]) continue;
+        std::vector<uint32_t> got(H[a]);
+        std::vector<int32_t> sl(ha.n[a]);
+        CU(cudaMemcpy(got.data(), ha.row_of[a], H[a] * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(sl.data(), ha.slot[a], ha.n[a] * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (uint32_t q = 0; q < H[a]; ++q)
+          if (got[q] != want[a][q] || sl[want[a][q]] != (int32_t)q)
+            return set_err(ctx, CMTF_ECUDA, "hot check: array %d slot %u differs", a, q);
+        uint64_t nhot = 0;
+        for (int32_t v : sl) nhot += v >= 0;
+        if (nhot != H[a]) return set_err(ctx, CMTF_ECUDA, "hot check: array %d stray slots", a);
+      }
+    }
+  } else {
+    struct Cand {
+      uint32_t count;
+      int arr;  // 0..N-1 modes, 100+m matrices
+      uint32_t row;
+    };
+    std::vector<Cand> cand;
+    std::vector<std::vector<uint32_t>> hcounts(ctx->order), vcounts(ctx->mats.size());
+    for (int n = 0; n < ctx->order; ++n) {
+      hcounts[n].resize(ctx->dims[n]);
+      CU(cudaMemcpy(hcounts[n].data(), ctx->count[n], ctx->dims[n] * sizeof(uint32_t),
+                    cudaMemcpyDeviceToHost));
+      if (tau > 0)
+        for (uint32_t i = 0; i < ctx->dims[n]; ++i)
+          if (hcounts[n][i] >= std::max<uint64_t>(thr, 1)) cand.push_back({hcounts[n][i], n, i});
+    }
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      const auto& M = ctx->mats[m];
+      vcounts[m].resize(M.cols);
+      CU(cudaMemcpy(vcounts[m].data(), M.count, M.cols * sizeof(uint32_t),
+                    cudaMemcpyDeviceToHost));
+      // a V row's updates are spread over the same iterations as the tensor's
+      if (tau > 0)
+        for (uint32_t j = 0; j < M.cols; ++j)
+          if (vcounts[m][j] >= std::max<uint64_t>(thr, 1))
+            cand.push_back({vcounts[m][j], 100 + (int)m, j});
+    }
+    ptick("counts+cand");
+    std::stable_sort(cand.begin(), cand.end(),
+                     [](const Cand& x, const Cand& y) { return x.count > y.count; });
+    size_t take = std::min<size_t>(cand.size(), max_take);
+    std::vector<std::vector<uint32_t>> rows_of(ctx->order), vrows_of(ctx->mats.size());
+    for (size_t q = 0; q < take; ++q) {
+      if (cand[q].arr < 100) rows_of[cand[q].arr].push_back(cand[q].row);
+      else vrows_of[cand[q].arr - 100].push_back(cand[q].row);
+    }
+    auto build = [&](cmtf_gpu_ctx::HotHost& h, const std::vector<uint32_t>& rows,
+                     uint32_t nrows) -> int {
+      h.H = (uint32_t)rows.size();
+      if (!h.H) return CMTF_OK;
+      std::vector<int32_t> slot(nrows, -1);
+      for (uint32_t s = 0; s < h.H; ++s) slot[rows[s]] = (int32_t)s;
+      TRY(ensure(ctx, &h.slot, &h.slot_cap, nrows));
+      TRY(ensure(ctx, &h.row_of, &h.row_cap, h.H));
+      CU(cudaMemcpy(h.slot, slot.data(), nrows * sizeof(int32_t), cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(h.row_of, rows.data(), h.H * sizeof(uint32_t), cudaMemcpyHostToDevice));
+      const uint64_t need = (uint64_t)blocks * h.H * JP;
+      if (h.base_cap < need) {
+        TRY(dalloc(ctx, &h.base, need));
+        h.base_cap = need;
+      }
+      h.off = off;  // float4-aligned (off and H*JP are multiples of 4)
+      off += h.H * JP;
+      h.stat_off = off;
+      off += (3 * h.H + 3) & ~3u;
+      return CMTF_OK;
+    };
+    for (int n = 0; n < ctx->order; ++n) TRY(build(ctx->hot[n], rows_of[n], ctx->dims[n]));
+    for (size_t m = 0; m < ctx->mats.size(); ++m)
+      TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
+  }
+  ptick("build");
   ctx->v2_smem = (size_t)off * sizeof(float);
   // hog3tm allocates all 512 TMEM columns: keep it at one block per SM
   if (tm3) ctx->v2_smem = std::max<size_t>(ctx->v2_smem, 116 * 1024);

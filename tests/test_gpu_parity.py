@@ -461,3 +461,21 @@ def test_order3_tensor_core_sweep_rmse_within_1pct(monkeypatch):
     te = api.test_rmse(st, test)
     assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
+
+
+@pytest.mark.parametrize("which", ["config1", "config2"])
+def test_device_hot_selection_matches_host(which, monkeypatch):
+    """The device-side hot-row selection (radix sort of (count, array, row)
+    keys) picks the same rows in the same replica slots as the host's stable
+    sort (CMTF_HOT_CHECK compares them inside prepare and fails the epoch)."""
+    monkeypatch.setenv("CMTF_HOT_CHECK", "1")
+    if which == "config1":
+        b, _, _ = synth.generate(synth.config1(literal=False))
+        ranks = [5, 5, 5]
+    else:
+        b, _, _ = synth.generate(synth.config2(0.1))
+        ranks = [10, 10, 10]
+    for tau in (0.0, 0.1):
+        st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, lambda_reg=0.01, hot_tau=tau), b)
+        api.run_epoch(st)
+        assert np.isfinite(api.epoch_stats(st, 0.01).train_rmse)
