@@ -315,23 +315,45 @@ __device__ __forceinline__ void count_aggregated(uint32_t* count, uint32_t i, bo
 }
 
 // Records [e_lo, e_hi) of the upload: validation, counts, packing.
+// perm_n > 0: the record goes straight to its place in the affine entry
+// order, p = (pa * e + pb) mod perm_n (pos[e] = p), instead of position e.
 __global__ void pack_tensor_kernel(const uint32_t* idx, const double* vals, uint64_t e_lo,
                                    uint64_t e_hi, int order, ModeTables mt,
                                    int sort_mode, uint32_t seed, uint32_t* rec,
                                    uint32_t* keys, uint32_t* ids,
-                                   unsigned long long* bad) {
+                                   unsigned long long* bad, uint64_t perm_n = 0,
+                                   uint64_t pa = 1, uint64_t pb = 0, uint32_t* pos = nullptr) {
   for (uint64_t e = e_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < e_hi;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    for (int n = 0; n < order; ++n) {
-      const uint32_t i = idx[e * order + n];
-      const bool ok = i < mt.dims[n];
-      if (!ok) atomicMin(&bad[0], (unsigned long long)e);
-      count_aggregated(const_cast<uint32_t*>(mt.count[n]), i, ok);
-      rec[e * (order + 1) + n] = i;
+    const uint64_t p = perm_n ? (uint64_t)(((unsigned __int128)pa * e + pb) % perm_n) : e;
+    if (perm_n) pos[e] = (uint32_t)p;
+    if (order == 3) {  // one 16-byte record store
+      uint4 r;
+      uint32_t* ri = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        const uint32_t i = idx[e * 3 + n];
+        const bool ok = i < mt.dims[n];
+        if (!ok) atomicMin(&bad[0], (unsigned long long)e);
+        count_aggregated(const_cast<uint32_t*>(mt.count[n]), i, ok);
+        ri[n] = i;
+      }
+      const double v = vals[e];
+      if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
+      r.w = __float_as_uint((float)v);
+      reinterpret_cast<uint4*>(rec)[p] = r;
+    } else {
+      for (int n = 0; n < order; ++n) {
+        const uint32_t i = idx[e * order + n];
+        const bool ok = i < mt.dims[n];
+        if (!ok) atomicMin(&bad[0], (unsigned long long)e);
+        count_aggregated(const_cast<uint32_t*>(mt.count[n]), i, ok);
+        rec[p * (order + 1) + n] = i;
+      }
+      const double v = vals[e];
+      if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
+      rec[p * (order + 1) + order] = __float_as_uint((float)v);
     }
-    const double v = vals[e];
-    if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
-    rec[e * (order + 1) + order] = __float_as_uint((float)v);
     if (keys) {  // sorted order only
       keys[e] = sort_mode >= 0 ? idx[e * order + sort_mode] : mix32((uint32_t)e, seed);
       ids[e] = (uint32_t)e;
@@ -419,17 +441,31 @@ __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
     reg[i] = count[i] ? lambda / (float)count[i] : 0.f;
 }
 
+constexpr uint32_t kPackHistCols = 8192;
 __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
                                    uint64_t nnz, uint32_t rows, uint32_t cols,
                                    int shuffled, uint32_t seed, uint32_t* rec,
                                    uint32_t* keys, uint32_t* ids, uint32_t* count,
                                    unsigned long long* bad) {
+  // few columns (e.g. a 200-column side matrix): per-block shared-memory
+  // histogram, one global atomic per (block, column) -- two million entries on
+  // 200 column counters otherwise serialise in L2
+  extern __shared__ uint32_t hist[];
+  const bool small = cols <= kPackHistCols;
+  if (small) {
+    for (uint32_t c = threadIdx.x; c < cols; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+  }
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = idx[2 * e], j = idx[2 * e + 1];
     const bool ok = i < rows && j < cols;
     if (!ok) atomicMin(&bad[0], (unsigned long long)e);
-    count_aggregated(count, j, ok);
+    if (small) {
+      if (ok) atomicAdd(hist + j, 1u);
+    } else {
+      count_aggregated(count, j, ok);
+    }
     const double v = vals[e];
     if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
     rec[3 * e] = i;
@@ -437,6 +473,11 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
     rec[3 * e + 2] = __float_as_uint((float)v);
     keys[e] = shuffled ? mix32((uint32_t)e, seed) : i;
     ids[e] = (uint32_t)e;
+  }
+  if (small) {
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < cols; c += blockDim.x)
+      if (hist[c]) atomicAdd(count + c, hist[c]);
   }
 }
 
@@ -1778,13 +1819,23 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   ModeTables mt = mode_tables(ctx);
   const bool shuffled = ctx->cfg.order_policy == 1;
   const bool need_keys = ctx->cfg.order_policy == 0;  // sorted order needs the sort keys
+  // random and caller orders: each record is packed straight into its place
+  // in the entry order (no separate scatter pass)
+  const bool direct = ctx->cfg.order_policy != 0;
+  uint64_t pa = 1, pb = 0;
+  if (shuffled) affine_params(nnz, ctx->cfg.seed, &pa, &pb);
+  if (direct) {
+    TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
+    TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
+  }
   for (int k = 0; k < kChunks; ++k) {
     const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
     if (c0 >= c1) break;
     CU(cudaStreamWaitEvent(ctx->stream, ctx->cev[k], 0));
     pack_tensor_kernel<<<grid_for(c1 - c0), 256, 0, ctx->stream>>>(
         d_idx, d_vals, c0, c1, N, mt, shuffled ? -1 : sm, (uint32_t)ctx->cfg.seed + 0x5bd1e995u,
-        d_rec, need_keys ? d_keys : nullptr, d_ids, ctx->d_first);
+        direct ? ctx->rec : d_rec, need_keys ? d_keys : nullptr, d_ids, ctx->d_first,
+        direct ? nnz : 0, pa, pb, ctx->pos);
   }
   CU(cudaGetLastError());
   unsigned long long bad[2];
@@ -1808,15 +1859,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   ctx->posA = 1;
   ctx->posB = 0;
   uint32_t* sorted_ids = nullptr;
-  if (ctx->cfg.order_policy == 2) {  // caller order (DSGD strata)
-    scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, 1, 0,
-                                                                  ctx->rec, ctx->pos);
-  } else if (shuffled) {
-    uint64_t pa, pb;
-    affine_params(nnz, ctx->cfg.seed, &pa, &pb);
-    scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, N + 1, pa, pb,
-                                                                  ctx->rec, ctx->pos);
-  } else {
+  if (!direct) {
     TRY(sort_ids(ctx, d_keys, d_ids, nnz, dims[sm], &sorted_ids));
     gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
         d_rec, sorted_ids, nnz, N + 1, ctx->rec, ctx->pos);
@@ -1910,7 +1953,8 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
                        ctx->stream));
     CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
     const int shuffled = ctx->cfg.order_policy == 1;
-    pack_matrix_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
+    pack_matrix_kernel<<<grid_for(nnz), 256,
+                         cols <= kPackHistCols ? cols * sizeof(uint32_t) : 0, ctx->stream>>>(
         d_idx, d_vals, nnz, rows, cols, shuffled,
         (uint32_t)ctx->cfg.seed + 0x27d4eb2fu + (uint32_t)ctx->mats.size(), d_rec, d_keys,
         d_ids, M.count, ctx->d_first);
