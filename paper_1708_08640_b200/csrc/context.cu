@@ -664,7 +664,7 @@ template <int J>
 int launch_eval3_t(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
                    double* partial) {
   constexpr int J3P = round_up4(J);
-  const size_t smem = sizeof(float) * (size_t)(J * J * J3P + round_up4(J) * 256);
+  const size_t smem = sizeof(float) * (size_t)(J * J * J3P + 4 * round_up4(J) * 256);
   auto kern = eval3_kernel<J, J, J>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));

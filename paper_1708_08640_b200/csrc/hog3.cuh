@@ -392,7 +392,7 @@ hog3_kernel(Hog3Args a) {
 // Eval pass for order 3: thread per entry, fixed 1024-entry blocks
 // (src/eval.cpp:10-65), double accumulation, deterministic order.
 template <int J1, int J2, int J3>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 eval3_kernel(const uint4* rec, uint64_t nnz, const float* U1, const float* U2,
              const float* U3, const float* G, double* partial) {
   constexpr int J1P = round_up4(J1), J2P = round_up4(J2), J3P = round_up4(J3);
@@ -409,37 +409,64 @@ eval3_kernel(const uint4* rec, uint64_t nnz, const float* U1, const float* U2,
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * kEvalBlock;
   const uint64_t hi = lo + kEvalBlock < nnz ? lo + kEvalBlock : nnz;
-  double acc = 0.0;
-  for (uint64_t e = lo + t; e < hi; e += BT) {
-    const uint4 rc = __ldg(rec + e);
-    float u2[J2P], u3[J3P];
-    load_row_regs<J2P>(U2 + (uint64_t)rc.y * J2P, u2);
-    load_row_regs<J3P>(U3 + (uint64_t)rc.z * J3P, u3);
+  // the block's 1024 entries, 4 per thread at once: every core row read from
+  // shared memory (one broadcast LDS.128 per 4 values) feeds 4 entries
+  constexpr int EV = kEvalBlock / BT;
+  static_assert(EV == 4, "eval: 4 entries per thread");
+  uint4 rc[EV];
+  float u2[EV][J2P], u3[EV][J3P], xh[EV];
+#pragma unroll
+  for (int q = 0; q < EV; ++q) {
+    const uint64_t e = lo + t + (uint64_t)q * BT;
+    rc[q] = e < hi ? __ldg(rec + e) : make_uint4(0, 0, 0, 0);
+    xh[q] = 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < EV; ++q) {
+    load_row_regs<J2P>(U2 + (uint64_t)rc[q].y * J2P, u2[q]);
+    load_row_regs<J3P>(U3 + (uint64_t)rc[q].z * J3P, u3[q]);
 #pragma unroll
     for (int k = 0; k < J1P; k += 4) {
-      const float4 q = ld_row4(U1 + (uint64_t)rc.x * J1P + k);
-      u1s[k * BT + t] = q.x; u1s[(k + 1) * BT + t] = q.y;
-      u1s[(k + 2) * BT + t] = q.z; u1s[(k + 3) * BT + t] = q.w;
+      const float4 v = ld_row4(U1 + (uint64_t)rc[q].x * J1P + k);
+      u1s[((q * J1P) + k) * BT + t] = v.x; u1s[((q * J1P) + k + 1) * BT + t] = v.y;
+      u1s[((q * J1P) + k + 2) * BT + t] = v.z; u1s[((q * J1P) + k + 3) * BT + t] = v.w;
     }
-    float xh = 0.f;
+  }
 #pragma unroll 1
-    for (int ia = 0; ia < J1; ++ia) {
-      const float* grow = Gs + ia * J2 * J3P;
-      float w = 0.f;
+  for (int ia = 0; ia < J1; ++ia) {
+    const float* grow = Gs + ia * J2 * J3P;
+    float w[EV];
 #pragma unroll
-      for (int ib = 0; ib < J2; ++ib) {
+    for (int q = 0; q < EV; ++q) w[q] = 0.f;
+#pragma unroll
+    for (int ib = 0; ib < J2; ++ib) {
+      float gv[J3P];
+#pragma unroll
+      for (int c = 0; c < J3P; c += 4) {
+        const float4 g4 = *reinterpret_cast<const float4*>(grow + ib * J3P + c);
+        gv[c] = g4.x; gv[c + 1] = g4.y; gv[c + 2] = g4.z; gv[c + 3] = g4.w;
+      }
+#pragma unroll
+      for (int q = 0; q < EV; ++q) {
         float t0 = 0.f, t1 = 0.f;
 #pragma unroll
         for (int c = 0; c < J3; ++c) {
-          if (c & 1) t1 = fmaf(grow[ib * J3P + c], u3[c], t1);
-          else t0 = fmaf(grow[ib * J3P + c], u3[c], t0);
+          if (c & 1) t1 = fmaf(gv[c], u3[q][c], t1);
+          else t0 = fmaf(gv[c], u3[q][c], t0);
         }
-        w = fmaf(t0 + t1, u2[ib], w);
+        w[q] = fmaf(t0 + t1, u2[q][ib], w[q]);
       }
-      xh = fmaf(w, u1s[ia * BT + t], xh);
     }
-    const double r = (double)__uint_as_float(rc.w) - (double)xh;
-    acc += r * r;
+#pragma unroll
+    for (int q = 0; q < EV; ++q) xh[q] = fmaf(w[q], u1s[(q * J1P + ia) * BT + t], xh[q]);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < EV; ++q) {
+    if (lo + t + (uint64_t)q * BT < hi) {
+      const double r = (double)__uint_as_float(rc[q].w) - (double)xh[q];
+      acc += r * r;
+    }
   }
   acc = warp_sum_d(acc);
   if ((t & 31) == 0) acc_s[t >> 5] = acc;
