@@ -154,7 +154,21 @@ int cmtf_gpu_test_rmse(cmtf_gpu_ctx *ctx, const uint32_t *idx,
 /* matrix_rmse (src/eval.cpp:109-118) for coupled matrix m of the bundle. */
 int cmtf_gpu_matrix_rmse(cmtf_gpu_ctx *ctx, int32_t m, double *rmse);
 
-/* train (src/trainer.cpp:318-346) without the QR finalisation: epochs until
+/* The tail of train() (src/trainer.cpp:342-345) applied to the current
+ * model, into host buffers laid out like cmtf_gpu_get_model.  Nonnegative
+ * configurations: apply_nonnegative_projection (src/trainer.cpp:348-387).
+ * Otherwise finalize_orthogonalize (src/tucker.cpp:226-283): U_n = Q R with Q
+ * orthonormal and R upper triangular with a nonnegative diagonal (the
+ * reference's sign-fixed Householder QR; unique for full-rank factors,
+ * computed as CholeskyQR2 in f64 on the device), core <- core x_n R, coupled
+ * factors V <- V R^T.  The device training state is not modified.
+ * CMTF_EVALIDATION if a mode has fewer rows than its rank or a factor is
+ * rank deficient. */
+int cmtf_gpu_finalize_model(cmtf_gpu_ctx *ctx, double *core, double *const *factors,
+                            double *const *couplings);
+
+/* train (src/trainer.cpp:318-346) up to the finalisation (see
+ * cmtf_gpu_finalize_model for the tail of the reference's train()): epochs until
  * |delta rmse| / rmse < rel_tol or max_epochs.  log receives 4 doubles per
  * epoch (epoch, train_rmse, objective, seconds); capacity in entries. */
 int cmtf_gpu_train(cmtf_gpu_ctx *ctx, double *log, int32_t log_capacity,

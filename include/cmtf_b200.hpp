@@ -163,7 +163,9 @@ class TrainState {
     for (const auto& m : b.matrices) mat_shapes_.emplace_back(m.coupled_mode, m.cols);
   }
 
-  FactorModel model() const {
+  // finalized == true: the tail of train() (src/trainer.cpp:342-345) applied
+  // to the copy -- finalize_orthogonalize or the nonnegative projection.
+  FactorModel model(bool finalized = false) const {
     FactorModel m;
     std::size_t size = 1;
     for (auto j : config_.ranks) size *= j;
@@ -177,8 +179,11 @@ class TrainState {
       m.couplings.emplace_back(static_cast<std::size_t>(s.second) * config_.ranks[s.first]);
       vp.push_back(m.couplings.back().data());
     }
-    check(cmtf_gpu_get_model(ctx_, m.core.data(), fp.data(), vp.empty() ? nullptr : vp.data()),
-          ctx_);
+    double* const* vpp = vp.empty() ? nullptr : vp.data();
+    if (finalized)
+      check(cmtf_gpu_finalize_model(ctx_, m.core.data(), fp.data(), vpp), ctx_);
+    else
+      check(cmtf_gpu_get_model(ctx_, m.core.data(), fp.data(), vpp), ctx_);
     return m;
   }
   int epoch() const {
@@ -229,7 +234,8 @@ struct ConvergenceLogEntry {
   double seconds;
 };
 
-// train (trainer.hpp:89) without the QR finalisation (next row).
+// train (trainer.hpp:89): epochs until convergence, then the reference's
+// finalisation (src/trainer.cpp:342-345) of the returned model.
 inline std::pair<FactorModel, std::vector<ConvergenceLogEntry>> train(const DataBundle& bundle,
                                                                        const TrainConfig& config) {
   TrainState state(config, bundle);
@@ -239,7 +245,7 @@ inline std::pair<FactorModel, std::vector<ConvergenceLogEntry>> train(const Data
   std::vector<ConvergenceLogEntry> out;
   for (int32_t i = 0; i < n && i < config.max_epochs; ++i)
     out.push_back({static_cast<int>(log[4 * i]), log[4 * i + 1], log[4 * i + 2], log[4 * i + 3]});
-  return {state.model(), out};
+  return {state.model(true), out};
 }
 
 }  // namespace b200

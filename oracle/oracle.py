@@ -76,7 +76,7 @@ def ref():
         for n in ("ref_bundle_free", "ref_state_free", "ref_run_epoch", "ref_state_get_model",
                   "ref_state_set_model", "ref_state_info", "ref_epoch_stats",
                   "ref_test_rmse", "ref_train", "ref_bundle_sizes", "ref_bundle_get",
-                  "ref_state_get_schedule"):
+                  "ref_state_get_schedule", "ref_state_finalize"):
             getattr(_ref, n).argtypes = None
         _ref.ref_bundle_free.argtypes = [C.c_void_p]
         _ref.ref_state_free.argtypes = [C.c_void_p]
@@ -367,6 +367,13 @@ class RefRun:
                                                C.POINTER(f64p)]
         core = np.ascontiguousarray(m.core, dtype=np.float64).reshape(-1)
         self.L.ref_state_set_model(self.s, _p(core, C.c_double), fp, vp)
+
+    def finalize(self, nonneg=False):
+        """The tail of the reference's train() on the state's model, in place."""
+        self.L.ref_state_finalize.argtypes = [C.c_void_p, C.c_int32]
+        rc = self.L.ref_state_finalize(self.s, int(nonneg))
+        if rc != 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
 
     def info(self):
         e, eta = C.c_int32(), C.c_double()

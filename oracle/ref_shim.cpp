@@ -188,6 +188,22 @@ int ref_test_rmse(void* state, int32_t order, const uint32_t* dims,
   }
 }
 
+// The tail of train() (src/trainer.cpp:342-345) applied in place to the
+// state's model: apply_nonnegative_projection when nonneg, else
+// finalize_orthogonalize (QR through oracle/eigen_shim).
+int ref_state_finalize(void* state, int32_t nonneg) {
+  try {
+    FactorModel& m = static_cast<TrainState*>(state)->model;
+    if (nonneg)
+      apply_nonnegative_projection(m);
+    else
+      finalize_orthogonalize(m);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
 // train(): convergence loop + finalization. log holds 4 doubles per epoch
 // (epoch, train_rmse, objective, seconds).
 int ref_train(void* bundle, const ref_config* c, double* core,

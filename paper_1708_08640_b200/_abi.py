@@ -73,6 +73,7 @@ SIGNATURES = [
     ("cmtf_gpu_make_state", C.c_int, [P]),
     ("cmtf_gpu_set_model", C.c_int, [P, f64p, f64pp, f64pp]),
     ("cmtf_gpu_get_model", C.c_int, [P, f64p, f64pp, f64pp]),
+    ("cmtf_gpu_finalize_model", C.c_int, [P, f64p, f64pp, f64pp]),
     ("cmtf_gpu_get_state", C.c_int, [P, i32p, f64p]),
     ("cmtf_gpu_set_state", C.c_int, [P, C.c_int32, C.c_double]),
     ("cmtf_gpu_run_epoch", C.c_int, [P]),

@@ -258,6 +258,19 @@ class TrainState:
         self._check(self._L.cmtf_gpu_get_model(self._h, _ptr(core, C.c_double), fp, vp))
         return FactorModel(core.reshape(ranks), F, V)
 
+    def finalized_model(self) -> FactorModel:
+        """The tail of train() (src/trainer.cpp:342-345) on the current model:
+        finalize_orthogonalize (src/tucker.cpp:226-283), or
+        apply_nonnegative_projection in nonnegative mode.  Output only."""
+        ranks, fac, cpl = self._shapes()
+        core = np.zeros(int(np.prod(ranks)), dtype=np.float64)
+        F = [np.zeros(s, dtype=np.float64) for s in fac]
+        V = [np.zeros(s, dtype=np.float64) for s in cpl]
+        fp = (f64p_t * max(1, len(F)))(*[_ptr(f, C.c_double) for f in F])
+        vp = (f64p_t * max(1, len(V)))(*[_ptr(v, C.c_double) for v in V])
+        self._check(self._L.cmtf_gpu_finalize_model(self._h, _ptr(core, C.c_double), fp, vp))
+        return FactorModel(core.reshape(ranks), F, V)
+
     @model.setter
     def model(self, m: FactorModel):
         core = np.ascontiguousarray(m.core, dtype=np.float64).reshape(-1)
@@ -365,7 +378,9 @@ class TrainResult:
 
 
 def train(bundle: DataBundle, config: TrainConfig) -> TrainResult:
-    """train (src/trainer.cpp:318-346) without the QR finalisation (next row)."""
+    """train (src/trainer.cpp:318-346): epochs until convergence, then the
+    reference's finalisation (orthogonalised factors, or the nonnegative
+    projection); `state` keeps the un-finalised device model."""
     s = TrainState(config, bundle)
     cap = max(1, config.max_epochs)
     log = np.zeros(4 * cap)
@@ -373,7 +388,7 @@ def train(bundle: DataBundle, config: TrainConfig) -> TrainResult:
     s._check(s._L.cmtf_gpu_train(s._h, _ptr(log, C.c_double), cap, C.byref(n)))
     entries = [(int(log[4 * i]), log[4 * i + 1], log[4 * i + 2], log[4 * i + 3])
                for i in range(min(n.value, cap))]
-    return TrainResult(s.model, entries, s)
+    return TrainResult(s.finalized_model(), entries, s)
 
 
 def entry_grads(state: TrainState, ids, with_core: bool = True):

@@ -2647,6 +2647,243 @@ int cmtf_gpu_matrix_rmse(cmtf_gpu_ctx* ctx, int32_t m, double* rmse) {
   return CMTF_OK;
 }
 
+// ---------------------------------------------------------------------
+// finalize_orthogonalize (src/tucker.cpp:226-283): every factor U_n = Q R
+// with Q orthonormal and R upper triangular with a nonnegative diagonal (the
+// reference's sign fix after Householder QR, :250-255) -- for a full-rank U_n
+// that factorisation is unique, so it is computed here as CholeskyQR2 in f64
+// on the device (Gram matrix -> Cholesky -> Q = U R^{-1}, twice); the core
+// takes core x_n R (core_mode_product, :167-206) and every coupled factor of
+// mode n becomes V R^T (:270-282).  Output only: the device training state is
+// left as it is (the reference finalises the model train() returns).
+// ---------------------------------------------------------------------
+__global__ void rows_to_f64_kernel(const float* U, uint64_t rows, uint32_t J, uint32_t JP,
+                                   double* X) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < rows * J;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = q / J;
+    X[q] = (double)U[i * JP + (q - i * J)];
+  }
+}
+
+// gram[a][b] += sum_i X[i][a] X[i][b]; thread t of a block owns pair t
+__global__ void gram_f64_kernel(const double* X, uint64_t rows, uint32_t J, double* gram) {
+  const uint32_t t = threadIdx.x;
+  const uint32_t a = t / J, b = t - (t / J) * J;
+  if (t >= J * J) return;
+  double acc = 0.0;
+  for (uint64_t i = blockIdx.x; i < rows; i += gridDim.x) acc += X[i * J + a] * X[i * J + b];
+  atomicAdd(gram + t, acc);
+}
+
+// X <- X M (M: J x J row-major)
+__global__ void right_mult_f64_kernel(double* X, uint64_t rows, uint32_t J, const double* M) {
+  extern __shared__ double Ms[];
+  for (uint32_t q = threadIdx.x; q < J * J; q += blockDim.x) Ms[q] = M[q];
+  __syncthreads();
+  double row[kMaxRank];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint32_t k = 0; k < J; ++k) row[k] = X[i * J + k];
+    for (uint32_t k = 0; k < J; ++k) {
+      double acc = 0.0;
+      for (uint32_t j = 0; j < J; ++j) acc += row[j] * Ms[j * J + k];
+      X[i * J + k] = acc;
+    }
+  }
+}
+
+namespace {
+// Upper R (row-major, J x J) with R^T R = A; false if A is not positive definite.
+bool cholesky_upper(const std::vector<double>& A, uint32_t J, std::vector<double>& R) {
+  R.assign((size_t)J * J, 0.0);
+  for (uint32_t k = 0; k < J; ++k) {
+    double d = A[(size_t)k * J + k];
+    for (uint32_t i = 0; i < k; ++i) d -= R[(size_t)i * J + k] * R[(size_t)i * J + k];
+    if (!(d > 0.0)) return false;
+    const double rkk = std::sqrt(d);
+    R[(size_t)k * J + k] = rkk;
+    for (uint32_t j = k + 1; j < J; ++j) {
+      double v = A[(size_t)k * J + j];
+      for (uint32_t i = 0; i < k; ++i) v -= R[(size_t)i * J + k] * R[(size_t)i * J + j];
+      R[(size_t)k * J + j] = v / rkk;
+    }
+  }
+  return true;
+}
+
+// inverse of an upper-triangular R (row-major)
+std::vector<double> upper_inverse(const std::vector<double>& R, uint32_t J) {
+  std::vector<double> X((size_t)J * J, 0.0);
+  for (uint32_t c = 0; c < J; ++c) {  // solve R x = e_c by back substitution
+    for (int r = (int)J - 1; r >= 0; --r) {
+      double v = (uint32_t)r == c ? 1.0 : 0.0;
+      for (uint32_t k = r + 1; k < J; ++k) v -= R[(size_t)r * J + k] * X[(size_t)k * J + c];
+      X[(size_t)r * J + c] = v / R[(size_t)r * J + r];
+    }
+  }
+  return X;
+}
+
+std::vector<double> matmul(const std::vector<double>& A, const std::vector<double>& B, uint32_t J) {
+  std::vector<double> C((size_t)J * J, 0.0);
+  for (uint32_t i = 0; i < J; ++i)
+    for (uint32_t k = 0; k < J; ++k)
+      for (uint32_t j = 0; j < J; ++j) C[(size_t)i * J + j] += A[(size_t)i * J + k] * B[(size_t)k * J + j];
+  return C;
+}
+}  // namespace
+
+// apply_nonnegative_projection (src/trainer.cpp:348-387), on host f64 copies:
+// clamp at 0, unit-norm factor columns, norms absorbed by the core slices and
+// the coupled factors' columns.
+int finalize_nonnegative(cmtf_gpu_ctx* ctx, double* core, double* const* factors,
+                         double* const* couplings) {
+  const int N = ctx->order;
+  std::vector<double> G(ctx->core_size());
+  std::vector<std::vector<double>> F(N), V(ctx->mats.size());
+  std::vector<double*> fp(N), vp(ctx->mats.size());
+  for (int n = 0; n < N; ++n) {
+    F[n].resize((uint64_t)ctx->dims[n] * ctx->J(n));
+    fp[n] = F[n].data();
+  }
+  for (size_t m = 0; m < ctx->mats.size(); ++m) {
+    V[m].resize((uint64_t)ctx->mats[m].cols * ctx->J(ctx->mats[m].mode));
+    vp[m] = V[m].data();
+  }
+  TRY(cmtf_gpu_get_model(ctx, G.data(), fp.data(), vp.empty() ? nullptr : vp.data()));
+  auto clamp = [](std::vector<double>& v) {
+    for (double& x : v)
+      if (x < 0) x = 0;
+  };
+  clamp(G);
+  for (auto& f : F) clamp(f);
+  for (auto& v : V) clamp(v);
+  for (int n = 0; n < N; ++n) {
+    const uint32_t J = ctx->J(n);
+    uint64_t stride = 1;
+    for (int m = N - 1; m > n; --m) stride *= ctx->J(m);
+    for (uint32_t k = 0; k < J; ++k) {
+      double nsq = 0.0;
+      for (uint64_t i = 0; i < ctx->dims[n]; ++i) nsq += F[n][i * J + k] * F[n][i * J + k];
+      if (nsq == 0.0) continue;  // absorbed as norm 1
+      const double norm = std::sqrt(nsq);
+      for (uint64_t i = 0; i < ctx->dims[n]; ++i) F[n][i * J + k] /= norm;
+      const uint64_t block = stride * J;
+      for (uint64_t base = 0; base < G.size(); base += block)
+        for (uint64_t t = 0; t < stride; ++t) G[base + k * stride + t] *= norm;
+      for (size_t m = 0; m < ctx->mats.size(); ++m)
+        if (ctx->mats[m].mode == n)
+          for (uint64_t i = 0; i < ctx->mats[m].cols; ++i) V[m][i * J + k] *= norm;
+    }
+  }
+  if (core) std::copy(G.begin(), G.end(), core);
+  for (int n = 0; n < N; ++n)
+    if (factors && factors[n]) std::copy(F[n].begin(), F[n].end(), factors[n]);
+  for (size_t m = 0; m < ctx->mats.size(); ++m)
+    if (couplings && couplings[m]) std::copy(V[m].begin(), V[m].end(), couplings[m]);
+  return CMTF_OK;
+}
+
+int cmtf_gpu_finalize_model(cmtf_gpu_ctx* ctx, double* core, double* const* factors,
+                            double* const* couplings) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  // train()'s tail (src/trainer.cpp:342-345)
+  if (ctx->cfg.nonnegative) return finalize_nonnegative(ctx, core, factors, couplings);
+  const int N = ctx->order;
+  for (int n = 0; n < N; ++n)
+    if (ctx->dims[n] < ctx->ranks[n])
+      return set_err(ctx, CMTF_EVALIDATION,
+                     "mode %d has fewer rows than its rank; cannot orthogonalize", n + 1);
+  // the core in f64, row-major, last mode fastest (src/tucker.cpp:49-54)
+  std::vector<float> cf(ctx->core_size());
+  CU(cudaMemcpy(cf.data(), ctx->G, cf.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<double> G(cf.begin(), cf.end());
+  uint64_t maxrows = 0;
+  for (int n = 0; n < N; ++n) maxrows = std::max<uint64_t>(maxrows, ctx->dims[n]);
+  for (auto& M : ctx->mats) maxrows = std::max<uint64_t>(maxrows, M.cols);
+  uint32_t maxJ = 0;
+  for (int n = 0; n < N; ++n) maxJ = std::max(maxJ, ctx->J(n));
+  double *X = nullptr, *dM = nullptr, *dgram = nullptr;
+  CU(cudaMalloc(&X, maxrows * maxJ * sizeof(double)));
+  CU(cudaMalloc(&dM, (size_t)maxJ * maxJ * sizeof(double)));
+  CU(cudaMalloc(&dgram, (size_t)maxJ * maxJ * sizeof(double)));
+  std::vector<std::vector<double>> R_by_mode(N);
+  int rc = CMTF_OK;
+  auto run = [&]() -> int {
+    for (int n = 0; n < N; ++n) {
+      const uint32_t J = ctx->J(n), JP = ctx->JP(n);
+      const uint64_t rows = ctx->dims[n];
+      rows_to_f64_kernel<<<grid_for(rows * J), 256, 0, ctx->stream>>>(ctx->U[n], rows, J, JP, X);
+      std::vector<double> R((size_t)J * J, 0.0);
+      for (uint32_t k = 0; k < J; ++k) R[(size_t)k * J + k] = 1.0;
+      for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2
+        CU(cudaMemsetAsync(dgram, 0, (size_t)J * J * sizeof(double), ctx->stream));
+        gram_f64_kernel<<<(unsigned)std::min<uint64_t>(rows, 4096), (J * J + 31) / 32 * 32, 0,
+                          ctx->stream>>>(X, rows, J, dgram);
+        std::vector<double> A((size_t)J * J), Rk;
+        CU(cudaMemcpyAsync(A.data(), dgram, A.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (!cholesky_upper(A, J, Rk))
+          return set_err(ctx, CMTF_EVALIDATION,
+                         "factor %d is rank deficient; cannot orthogonalize", n + 1);
+        const std::vector<double> Ri = upper_inverse(Rk, J);
+        CU(cudaMemcpyAsync(dM, Ri.data(), Ri.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        right_mult_f64_kernel<<<grid_for(rows), 128, (size_t)J * J * sizeof(double),
+                                ctx->stream>>>(X, rows, J, dM);
+        R = matmul(Rk, R, J);
+        CU(cudaStreamSynchronize(ctx->stream));  // Ri lives on the host stack
+      }
+      if (factors && factors[n])
+        CU(cudaMemcpy(factors[n], X, rows * J * sizeof(double), cudaMemcpyDeviceToHost));
+      // core <- core x_n R: new[.. j ..] = sum_i R[j][i] core[.. i ..]
+      uint64_t stride = 1;
+      for (int m = N - 1; m > n; --m) stride *= ctx->J(m);
+      const uint64_t outer = G.size() / (stride * J);
+      std::vector<double> H(G.size(), 0.0);
+      for (uint64_t o = 0; o < outer; ++o)
+        for (uint32_t j = 0; j < J; ++j)
+          for (uint32_t i = 0; i < J; ++i) {
+            const double r = R[(size_t)j * J + i];
+            if (r == 0.0) continue;
+            const double* src = G.data() + (o * J + i) * stride;
+            double* dst = H.data() + (o * J + j) * stride;
+            for (uint64_t s2 = 0; s2 < stride; ++s2) dst[s2] += r * src[s2];
+          }
+      G.swap(H);
+      R_by_mode[n] = R;
+    }
+    // coupled factors: V <- V R^T
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      const auto& M = ctx->mats[m];
+      const uint32_t J = ctx->J(M.mode), JP = ctx->JP(M.mode);
+      if (!couplings || !couplings[m]) continue;
+      std::vector<double> Rt((size_t)J * J);
+      for (uint32_t a = 0; a < J; ++a)
+        for (uint32_t b = 0; b < J; ++b) Rt[(size_t)a * J + b] = R_by_mode[M.mode][(size_t)b * J + a];
+      rows_to_f64_kernel<<<grid_for((uint64_t)M.cols * J), 256, 0, ctx->stream>>>(M.V, M.cols, J,
+                                                                                  JP, X);
+      CU(cudaMemcpyAsync(dM, Rt.data(), Rt.size() * sizeof(double), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      right_mult_f64_kernel<<<grid_for(M.cols), 128, (size_t)J * J * sizeof(double),
+                              ctx->stream>>>(X, M.cols, J, dM);
+      CU(cudaMemcpy(couplings[m], X, (uint64_t)M.cols * J * sizeof(double),
+                    cudaMemcpyDeviceToHost));
+    }
+    if (core) std::copy(G.begin(), G.end(), core);
+    return CMTF_OK;
+  };
+  rc = run();
+  cudaFree(X);
+  cudaFree(dM);
+  cudaFree(dgram);
+  return rc;
+}
+
 // train (src/trainer.cpp:318-346) minus the QR finalisation.
 int cmtf_gpu_train(cmtf_gpu_ctx* ctx, double* log, int32_t log_capacity,
                    int32_t* n_log) {

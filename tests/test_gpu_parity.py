@@ -479,3 +479,57 @@ def test_device_hot_selection_matches_host(which, monkeypatch):
         st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, lambda_reg=0.01, hot_tau=tau), b)
         api.run_epoch(st)
         assert np.isfinite(api.epoch_stats(st, 0.01).train_rmse)
+
+
+# ----------------------------------------------------------------------
+# train()'s finalisation: finalize_orthogonalize /
+# apply_nonnegative_projection vs the reference on the same model
+# ----------------------------------------------------------------------
+def _predict_all(m, idx):
+    """x_hat for entries idx (numpy, f64) of a dense-core model."""
+    G = m.core
+    out = np.einsum("abc,ea,eb,ec->e", G, m.factors[0][idx[:, 0]], m.factors[1][idx[:, 1]],
+                    m.factors[2][idx[:, 2]])
+    return out
+
+
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_finalized_model_matches_reference(nonneg):
+    spec = synth.config1(literal=False)
+    spec.nnz, spec.dims = 20000, [300, 200, 100]
+    spec.matrices[0].cols, spec.matrices[0].nnz = 50, 3000
+    b, _, _ = synth.generate(spec)
+    ranks = [5, 5, 5]
+    st = api.make_state(TrainConfig(ranks=ranks, seed=3, eta0=0.01, lambda_reg=0.01,
+                                    nonnegative=nonneg), b)
+    for _ in range(2):
+        api.run_epoch(st)
+    raw = st.model
+    fin = st.finalized_model()
+    ref = O.RefRun(b, ranks, seed=3, eta0=0.01, lambda_reg=0.01, nonnegative=nonneg)
+    ref.set_model(O.OracleModel(b, ranks).copy_from(raw))
+    ref.finalize(nonneg=nonneg)
+    rm = ref.model()
+    tol = 1e-9
+    for got, want in zip([fin.core.reshape(-1)] + fin.factors + fin.couplings,
+                         [rm.core.reshape(-1)] + rm.factors + rm.couplings):
+        assert np.abs(got - want).max() <= tol * max(1.0, np.abs(want).max()), (
+            np.abs(got - want).max())
+    idx = b.tensor.indices[:2000].astype(np.int64)
+    if not nonneg:  # orthonormal factors, predictions and couplings' products preserved
+        for f in fin.factors:
+            assert np.abs(f.T @ f - np.eye(f.shape[1])).max() <= 1e-9
+        p0, p1 = _predict_all(raw, idx), _predict_all(fin, idx)
+        assert np.abs(p1 - p0).max() <= 1e-9 * np.abs(p0).max()
+        M = b.matrices[0]
+        u0 = raw.factors[M.coupled_mode] @ raw.couplings[0].T
+        u1 = fin.factors[M.coupled_mode] @ fin.couplings[0].T
+        assert np.abs(u1 - u0).max() <= 1e-9 * np.abs(u0).max()
+    # train() returns the finalised model
+    res = api.train(b, TrainConfig(ranks=ranks, seed=3, eta0=0.01, lambda_reg=0.01,
+                                   max_epochs=2, nonnegative=nonneg))
+    if not nonneg:
+        for f in res.model.factors:
+            assert np.abs(f.T @ f - np.eye(f.shape[1])).max() <= 1e-9
+    else:
+        assert all(a.min() >= 0 for a in [res.model.core] + res.model.factors)
