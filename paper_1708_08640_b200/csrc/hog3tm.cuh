@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   cp_async_commit();  // (empty) core-refresh group
 
 #if CMTF_TM_PROF
-  long long tprof[12] = {0};
+  long long tprof[14] = {0};
   long long tlast = clock64();
 #define TMP(k) do { const long long tn = clock64(); tprof[k] += tn - tlast; tlast = tn; } while (0)
 #else
@@ -465,11 +465,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         lb += red_lam[4 * g + q];
       }
       umma::mbar_wait(&mbar[g][1], par);
+      TMP(11);
       umma::fence_after();
       float v[16];
       umma::ld16(tm + tm_lane + 2 * NT, v);
       umma::ld_wait();
       umma::ld_fence_regs<16>(v);
+      TMP(12);
       float* scr = reinterpret_cast<float*>(ST) + (w & 3) * (32 * J);
       const int row0 = 32 * (w & 3);
       if (kb > 0.f && row0 < AB) {
@@ -506,7 +508,12 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         if (!a.nonneg) {  // coalesced REDs of the warp's 32 rows
           const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
           float* Gw = a.G + row0 * J;
-          for (int m = lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
+          // vector REDs: 4 consecutive core elements per request
+          for (int m4 = lane; m4 < nval / 4; m4 += 32) {
+            const float4 d = *reinterpret_cast<const float4*>(scr + 4 * m4);
+            red_add_v4(Gw + 4 * m4, make_float4(s * d.x, s * d.y, s * d.z, s * d.w));
+          }
+          for (int m = (nval & ~3) + lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
         }
       }
       umma::fence_before();
@@ -530,9 +537,9 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #if CMTF_TM_PROF
   if (blockIdx.x == 0 && (threadIdx.x & 127) == 0)
     printf("prof wg%d iters %llu: wait+tiles+PT %lld | bar1+issue %lld | mma wait %lld | contract %lld | "
-           "rowsteps %lld | ST+bar2+issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld\n",
+           "rowsteps %lld | ST+bar2+issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld | push.mbar %lld | push.tmem %lld\n",
            g, (unsigned long long)iters, tprof[0], tprof[1], tprof[2], tprof[3], tprof[4], tprof[5],
-           tprof[6], tprof[7], tprof[8], tprof[9], tprof[10]);
+           tprof[6], tprof[7], tprof[8], tprof[9], tprof[10], tprof[11], tprof[12]);
 #endif
 }
 
