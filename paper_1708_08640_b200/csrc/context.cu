@@ -993,6 +993,24 @@ __global__ void hot_assign_kernel(const unsigned long long* keys, const unsigned
   }
 }
 
+// hog3tm: flag records whose U / V row is hot (kMrecHotU / kMrecHotV)
+struct MatHotSlots {
+  const int32_t* su[kV2MaxMats];
+  const int32_t* sv[kV2MaxMats];
+};
+__global__ void mrec_hot_flags_kernel(uint4* mrec, uint64_t n, MatHotSlots f) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 r = mrec[e];
+    const uint32_t m = r.w & kMrecMat;
+    uint32_t w = m;
+    if (f.su[m] && f.su[m][r.x] >= 0) w |= kMrecHotU;
+    if (f.sv[m] && f.sv[m][r.y] >= 0) w |= kMrecHotV;
+    r.w = w;
+    mrec[e] = r;
+  }
+}
+
 // Build the merged random-order matrix records and the hot-row replicas.
 int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   static const bool ptime = std::getenv("CMTF_PREP_TIMING") != nullptr;
@@ -1288,6 +1306,16 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
       TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
   }
   ptick("build");
+  if (tm3 && ctx->mnnz && CMTF_TM_MPF) {
+    MatHotSlots f{};
+    for (size_t m = 0; m < ctx->mats.size(); ++m) {
+      const int mode = ctx->mats[m].mode;
+      f.su[m] = ctx->hot[mode].H ? ctx->hot[mode].slot : nullptr;
+      f.sv[m] = ctx->hotV[m].H ? ctx->hotV[m].slot : nullptr;
+    }
+    mrec_hot_flags_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(ctx->mrec, ctx->mnnz, f);
+    CU(cudaGetLastError());
+  }
   ctx->v2_smem = (size_t)off * sizeof(float);
   // hog3tm allocates all 512 TMEM columns: keep it at one block per SM
   if (tm3) ctx->v2_smem = std::max<size_t>(ctx->v2_smem, 116 * 1024);

@@ -39,7 +39,7 @@
 #define CMTF_TM_REFRESH 4  // pushes between refreshes of the shared core copies
 #endif
 #ifndef CMTF_TM_MPF
-#define CMTF_TM_MPF 0  // matrix entries with prefetched rows (measured slower: +3.5%)
+#define CMTF_TM_MPF 1  // matrix entries: cold rows, slots and V coefficients fetched one entry ahead
 #endif
 #ifndef CMTF_TM_PROF
 #define CMTF_TM_PROF 0

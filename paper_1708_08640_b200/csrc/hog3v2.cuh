@@ -575,20 +575,33 @@ struct MatPrefetch {
   uint4 mr;       // next entry's record
   uint4 mr2;      // the one after
   int su, sv;     // hot slots of its rows
+  float vr;       // its V row's regularisation coefficient
   float4 u[3], v[3];
 };
 
+// Record flags set by prepare (hog3tm): the row of the record's U / V is a
+// hot (replicated) row.  Low byte of .w = matrix id.
+constexpr uint32_t kMrecHotU = 1u << 30, kMrecHotV = 1u << 31, kMrecMat = 0xffu;
+
+// Hot rows come from the replica at use time (only their slot is fetched
+// ahead); cold rows are loaded from global ahead of use.  A hot row's global
+// line is the most contended one in the system, so it is never read here.
 template <int JP, class Args>
 __device__ __forceinline__ void mat_prefetch_rows(const Args& a, MatPrefetch& p, bool valid) {
-  const MatDesc3& M = a.mats[valid ? p.mr.w : 0];
+  const MatDesc3& M = a.mats[valid ? (p.mr.w & kMrecMat) : 0];
   const int mode = M.mode;
   const uint32_t i = valid ? p.mr.x : 0u, j = valid ? p.mr.y : 0u;
-  p.su = valid && a.hot[mode].slot ? __ldg(a.hot[mode].slot + i) : -1;
-  p.sv = valid && M.hotV.slot ? __ldg(M.hotV.slot + j) : -1;
+  const bool hu = valid && (p.mr.w & kMrecHotU), hv = valid && (p.mr.w & kMrecHotV);
+  p.su = hu ? __ldg(a.hot[mode].slot + i) : -1;
+  p.sv = hv ? __ldg(M.hotV.slot + j) : -1;
+  p.vr = valid ? __ldg(M.vreg + j) : 0.f;
+  if (valid && !hu) {
 #pragma unroll
-  for (int k = 0; k < JP / 4; ++k) {
-    p.u[k] = ld_weak4(a.U[mode] + (uint64_t)i * JP + 4 * k);
-    p.v[k] = ld_weak4(M.V + (uint64_t)j * JP + 4 * k);
+    for (int k = 0; k < JP / 4; ++k) p.u[k] = ld_weak4(a.U[mode] + (uint64_t)i * JP + 4 * k);
+  }
+  if (valid && !hv) {
+#pragma unroll
+    for (int k = 0; k < JP / 4; ++k) p.v[k] = ld_weak4(M.V + (uint64_t)j * JP + 4 * k);
   }
 }
 
@@ -608,9 +621,10 @@ __device__ __forceinline__ void matrix_entries_until_pf(const Args& a, float* sm
   while (__any_sync(0xffffffffu, mpos < due)) {
     const bool has = mpos < due;
     const uint4 mr = p.mr;
-    const MatDesc3& M = a.mats[has ? mr.w : 0];
+    const MatDesc3& M = a.mats[has ? (mr.w & kMrecMat) : 0];
     const int mode = M.mode;
     const int su = has ? p.su : -1, sv = has ? p.sv : -1;
+    const float vr = has ? p.vr : 0.f;
     float uu[JP], vv[JP];
     float* repU = sm + a.hot[mode].off;
     float* repV = sm + M.hotV.off;
@@ -637,7 +651,6 @@ __device__ __forceinline__ void matrix_entries_until_pf(const Args& a, float* sm
       nv = fmaf(vv[k], vv[k], nv);
     }
     const float rr = has ? __uint_as_float(mr.z) - yh : 0.f;
-    const float vr = has ? __ldg(M.vreg + mr.y) : 0.f;
     float du[J], dv[J];
 #pragma unroll
     for (int k = 0; k < J; ++k) {
