@@ -41,6 +41,9 @@
 #ifndef CMTF_TM_MPF
 #define CMTF_TM_MPF 1  // matrix entries: cold rows, slots and V coefficients fetched one entry ahead
 #endif
+#ifndef CMTF_TM_FSTAGE
+#define CMTF_TM_FSTAGE 1  // hot-row merges with cp.async-staged global reads
+#endif
 #ifndef CMTF_TM_PROF
 #define CMTF_TM_PROF 0
 #endif
@@ -83,7 +86,91 @@ struct TMLayout {
   static constexpr int TM_COLS = 2 * NT + KC;
   static_assert(TM_COLS <= 256, "two warpgroups must fit in 512 TMEM columns");
   static_assert(AB <= 128, "core-gradient MMA has M = 128 rows (a,b)");
+  // the staged hot-row merge fits a warp's P^T slice (J >= 8)
+  static constexpr bool FSTAGE = 2 * 32 * 2 * JP * 4 <= 4 * PT_KS;
 };
+
+// Hot-row merge (flush_hot's arithmetic, hog3v2.cuh) with the two global reads
+// of each row -- its current value and this block's base -- staged through
+// shared memory with cp.async two rows per lane ahead, so a lane's rows cost
+// one L2 round trip in all instead of one each.  `stage`: the warp's slice of
+// its P^T buffer (free after the core MMA), 2 slots x 32 lanes x 2 JP floats.
+template <int J, int JP>
+__device__ void flush_hot_staged(const HotDesc& h, float* U, float* rep, float* stat, float eta,
+                                 float kappa, int r0, int r1, int lane, float* stage) {
+  float* base_b = h.base + (uint64_t)blockIdx.x * h.H * JP;
+  auto issue = [&](int s, int slot) {
+    if (s < r1) {
+      float* st = stage + (slot * 32 + lane) * 2 * JP;
+      const float* g = U + (uint64_t)__ldg(h.row_of + s) * JP;
+#pragma unroll
+      for (int k = 0; k < JP; k += 4) {
+        cp_async16(st + k, g + k);
+        cp_async16(st + JP + k, base_b + s * JP + k);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(r0 + lane, 0);
+  int slot = 0;
+  for (int s = r0 + lane; s < r1; s += 32, slot ^= 1) {
+    issue(s + 32, slot ^ 1);
+    cp_async_wait_group<1>();
+    const float* st = stage + (slot * 32 + lane) * 2 * JP;
+    float4 gv[JP / 4], bv[JP / 4], sv[JP / 4];
+#pragma unroll
+    for (int k = 0; k < JP / 4; ++k) {
+      gv[k] = *reinterpret_cast<const float4*>(st + 4 * k);
+      bv[k] = *reinterpret_cast<const float4*>(st + JP + 4 * k);
+      sv[k] = *reinterpret_cast<const float4*>(rep + s * JP + 4 * k);
+    }
+    const float cnt = (float)atomicExch(reinterpret_cast<int*>(stat) + 3 * s + 1, 0);
+    const float lam = stat[3 * s];
+    stat[3 * s] = 0.f;
+    float alpha = 0.f;
+    if (cnt > 0.f) {
+      const float n_other = stat[3 * s + 2] * (1.f - 1.f / (float)gridDim.x);
+      const float gain = CMTF_SAT_GAIN ? -expm1f(-eta * lam) : eta * lam;
+      alpha = kappa / (kappa + (n_other / cnt) * gain);
+    }
+    float* g = U + (uint64_t)__ldg(h.row_of + s) * JP;
+#pragma unroll
+    for (int k = 0; k < JP / 4; ++k) {
+      float4 dl = make_float4(alpha * (sv[k].x - bv[k].x), alpha * (sv[k].y - bv[k].y),
+                              alpha * (sv[k].z - bv[k].z), alpha * (sv[k].w - bv[k].w));
+      if (cnt > 0.f) red_add_v4(g + 4 * k, dl);
+      const float4 nb = make_float4(gv[k].x + dl.x, gv[k].y + dl.y, gv[k].z + dl.z, gv[k].w + dl.w);
+      st_weak4(base_b + s * JP + 4 * k, nb);
+      float4 cur = *reinterpret_cast<float4*>(rep + s * JP + 4 * k);
+      cur.x += nb.x - sv[k].x; cur.y += nb.y - sv[k].y;
+      cur.z += nb.z - sv[k].z; cur.w += nb.w - sv[k].w;
+      *reinterpret_cast<float4*>(rep + s * JP + 4 * k) = cur;
+    }
+  }
+  cp_async_wait_all();
+}
+
+template <int J, int JP, int NW, class Args>
+__device__ __forceinline__ void flush_all_hot_staged(const Args& a, float* sm, int w, int lane,
+                                                     float* stage) {
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const HotDesc& h = a.hot[n];
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot_staged<J, JP>(h, a.U[n], sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0, r1,
+                              lane, stage);
+    }
+  }
+  for (int m = 0; m < a.n_mat; ++m) {
+    const HotDesc& h = a.mats[m].hotV;
+    if (h.H) {
+      const int r0 = (int)((uint64_t)h.H * w / NW), r1 = (int)((uint64_t)h.H * (w + 1) / NW);
+      flush_hot_staged<J, JP>(h, a.mats[m].V, sm + h.off, sm + h.stat_off, a.eta, a.kappa, r0,
+                              r1, lane, stage);
+    }
+  }
+}
 
 template <int J>
 __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
@@ -520,8 +607,17 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
     TMP(9);
     cp_async_commit();  // core refresh group (possibly empty)
-    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters)
-      flush_all_hot<J, JP, NW>(a, sm, w, lane);
+    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {
+      if (CMTF_TM_FSTAGE && L::FSTAGE) {
+        // staging: this warp's 4 column groups of its P^T buffer (only its
+        // own threads write them; the core MMA that read them is complete)
+        umma::mbar_wait(&mbar[g][1], par);
+        flush_all_hot_staged<J, JP, NW>(
+            a, sm, w, lane, reinterpret_cast<float*>(PT + (w & 3) * 4 * L::PT_KS));
+      } else {
+        flush_all_hot<J, JP, NW>(a, sm, w, lane);
+      }
+    }
     TMP(10);
   }
 #if CMTF_TM_MPF
