@@ -39,7 +39,7 @@
 #define CMTF_TM_REFRESH 4  // pushes between refreshes of the shared core copies
 #endif
 #ifndef CMTF_TM_MPF
-#define CMTF_TM_MPF 1  // matrix entries: cold rows, slots and V coefficients fetched one entry ahead
+#define CMTF_TM_MPF 0  // matrix entries fetched one entry ahead: config 2 -0.9%, config 5 (rank 5) +13% -- off
 #endif
 #ifndef CMTF_TM_FSTAGE
 #define CMTF_TM_FSTAGE 1  // hot-row merges with cp.async-staged global reads
