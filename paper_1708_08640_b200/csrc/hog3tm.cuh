@@ -69,13 +69,17 @@ struct TMLayout {
   static constexpr int U_KS = 128 * 16;
   // fp16 core-gradient operands: 8 entries per 16-byte row chunk
   static constexpr int PT_KS = MR * 16 + 16;   // +16: column writes hit distinct banks
-  static constexpr int ST_KS = KC * 16 + 16;
+  // S^T column-group stride: holds the 16 c rows, makes a warp's 4 column
+  // groups (its own slab) big enough for its push transpose (32 x J floats),
+  // and keeps the column writes conflict-free ((ST_KS / 4) mod 8 == 4)
+  static constexpr int st_ks(int v) { return (v % 16 == 0 && (v / 4) % 8 == 4) ? v : st_ks(v + 16); }
+  static constexpr int ST_KS = st_ks(KC * 16 > 32 * J ? KC * 16 : 32 * J);
   static constexpr int G_BYTES = (KT / 4) * G_KS;
   static constexpr int U_BYTES = (KT / 4) * U_KS;
   static constexpr int U1_BYTES = 128 * JP * 4;
   static constexpr int PT_BYTES = 16 * PT_KS;  // 128 entries = 16 groups of 8
   // S^T also serves as the core push's transpose scratch (4 warps x 32 rows x J)
-  static constexpr int ST_BYTES = 16 * ST_KS > 4 * 32 * J * 4 ? 16 * ST_KS : 4 * 32 * J * 4;
+  static constexpr int ST_BYTES = 16 * ST_KS;
   // per warpgroup: P^T first (the M = 128 MMA reads rows MR..127 of the last
   // column group past its end: they land in S^T / U tiles, and only feed the
   // ignored core-gradient rows ab >= J^2)
@@ -190,9 +194,9 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   uint8_t* tU2 = ST + L::ST_BYTES;
   uint8_t* tU3 = tU2 + L::U_BYTES;
   float* sU1 = reinterpret_cast<float*>(tU3 + L::U_BYTES);
-  __shared__ uint64_t mbar[2][2];    // [warpgroup][sweep MMAs, core MMA]
+  __shared__ uint64_t mbar[2][2];    // [warpgroup][sweep MMAs done, core MMA done]
+  __shared__ uint32_t st_arrive[2];  // warps done with their S^T columns (monotonic)
   __shared__ uint32_t tmem_base;
-  __shared__ float red_kw[NW], red_lam[NW];
 
   auto gc_off = [](int ab, int c) { return (c >> 2) * L::G_KS + ab * 16 + (c & 3) * 4; };
 
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     umma::mbar_init(&mbar[0][1], 1);
     umma::mbar_init(&mbar[1][0], 1);
     umma::mbar_init(&mbar[1][1], 1);
+    st_arrive[0] = st_arrive[1] = 0u;
     umma::fence_mbar_init();
   }
   if (w == 0) umma::tmem_alloc<512>(&tmem_base);
@@ -374,6 +379,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
     umma::fence_async_smem();
     TMP(0);
+    // a hardware barrier here (the last-warp-issues scheme used for the core
+    // MMA measured 2% slower: the early warps then spin on the mbarrier)
     umma::bar_sync(1 + g, 128);
     if (e == 0) {
       umma::fence_after();
@@ -482,14 +489,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     TMP(4);
     // push statistics of this warpgroup; they cross the barrier below
+    // (per warp: the warpgroup's count and curvature sum are taken as 4x the
+    // warp's -- the damping only needs their ratio, the regulariser the count)
     const bool push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
+    float kb = 0.f, lb = 0.f;
     if (push) {
-      const float kws = warp_sum(kw);
-      const float lgs = warp_sum(lamG);
-      if (lane == 0) {
-        red_kw[w] = kws;
-        red_lam[w] = lgs;
-      }
+      kb = 4.f * warp_sum(kw);
+      lb = 4.f * warp_sum(lamG);
       kw = 0.f;
       lamG = 0.f;
     }
@@ -504,8 +510,16 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
     umma::fence_async_smem();
     umma::fence_before();
-    umma::bar_sync(1 + g, 128);
-    if (e == 0) {
+    // no barrier: the last of the warpgroup's 4 warps to finish its S^T
+    // columns issues the core MMA; nobody waits
+    __syncwarp();
+    bool issue_core = false;
+    if (lane == 0) {
+      __threadfence_block();
+      issue_core = (atomicAdd(&st_arrive[g], 1u) & 3u) == 3u;
+      __threadfence_block();
+    }
+    if (issue_core) {
       umma::fence_after();
       const uint32_t acc0 = (it % (uint64_t)a.core_every) != 0 ? 1u : 0u;
 #pragma unroll
@@ -545,12 +559,6 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     // through its slice of the S^T buffer (free until the next barrier) so the
     // REDs to the global core are coalesced ----
     if (push) {
-      float kb = 0.f, lb = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        kb += red_kw[4 * g + q];
-        lb += red_lam[4 * g + q];
-      }
       umma::mbar_wait(&mbar[g][1], par);
       TMP(11);
       umma::fence_after();
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       umma::ld_wait();
       umma::ld_fence_regs<16>(v);
       TMP(12);
-      float* scr = reinterpret_cast<float*>(ST) + (w & 3) * (32 * J);
+      float* scr = reinterpret_cast<float*>(ST + (w & 3) * 4 * L::ST_KS);  // own slab
       const int row0 = 32 * (w & 3);
       if (kb > 0.f && row0 < AB) {
         const float q = a.eta * (lb / kb) * a.nhat_core;
