@@ -77,7 +77,19 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count)
                : "memory");
 }
+#ifndef CMTF_MBAR_SUSPEND
+#define CMTF_MBAR_SUSPEND 1000000  // try_wait suspend-time hint in ns (0: none)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+#if CMTF_MBAR_SUSPEND
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(parity), "n"(CMTF_MBAR_SUSPEND)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -85,6 +97,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar))
