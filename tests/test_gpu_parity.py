@@ -533,3 +533,27 @@ def test_finalized_model_matches_reference(nonneg):
             assert np.abs(f.T @ f - np.eye(f.shape[1])).max() <= 1e-9
     else:
         assert all(a.min() >= 0 for a in [res.model.core] + res.model.factors)
+
+
+@pytest.mark.parametrize("J", [4, 8, 10])
+def test_tcgen05_kernel_ranks_within_1pct_of_oracle(J):
+    """hog3tm at every rank it is built for (4, 5, 8, 10; 5 is covered by the
+    config-1 test above): 10 Hogwild epochs on the config-1 shape vs the
+    serial oracle."""
+    spec = synth.config1(literal=False)
+    b, test, _ = synth.generate(spec)
+    ranks = [J, J, J]
+    epochs = 10
+    tr = O.SerialTrainer(b, ranks, seed=0, eta0=0.01, mu=0.1, lambda_reg=0.01)
+    for _ in range(epochs):
+        assert tr.run_epoch() == 0
+    ref_test = O.tensor_rmse(test, tr.model)
+    ref_train, _ = O.epoch_stats(b, tr.model, 0.01)
+    st = api.make_state(TrainConfig(ranks=ranks, seed=0, eta0=0.01, lambda_reg=0.01), b)
+    for _ in range(epochs):
+        api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == "order3tm"
+    gpu_test = api.test_rmse(st, test)
+    gpu_train = api.epoch_stats(st, 0.01).train_rmse
+    assert abs(gpu_train - ref_train) <= 0.01 * ref_train, (gpu_train, ref_train)
+    assert abs(gpu_test - ref_test) <= 0.01 * ref_test, (gpu_test, ref_test)
