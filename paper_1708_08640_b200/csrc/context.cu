@@ -442,11 +442,14 @@ __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
 }
 
 constexpr uint32_t kPackHistCols = 8192;
+// Entries [e_lo, e_hi) of a matrix upload; perm_n > 0: each record goes
+// straight to its place p = (pa * e + pb) mod perm_n of the entry order.
 __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
-                                   uint64_t nnz, uint32_t rows, uint32_t cols,
+                                   uint64_t e_lo, uint64_t nnz, uint32_t rows, uint32_t cols,
                                    int shuffled, uint32_t seed, uint32_t* rec,
                                    uint32_t* keys, uint32_t* ids, uint32_t* count,
-                                   unsigned long long* bad) {
+                                   unsigned long long* bad, uint64_t perm_n = 0,
+                                   uint64_t pa = 1, uint64_t pb = 0, uint32_t* pos = nullptr) {
   // few columns (e.g. a 200-column side matrix): per-block shared-memory
   // histogram, one global atomic per (block, column) -- two million entries on
   // 200 column counters otherwise serialise in L2
@@ -456,7 +459,7 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
     for (uint32_t c = threadIdx.x; c < cols; c += blockDim.x) hist[c] = 0;
     __syncthreads();
   }
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+  for (uint64_t e = e_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = idx[2 * e], j = idx[2 * e + 1];
     const bool ok = i < rows && j < cols;
@@ -468,11 +471,15 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
     }
     const double v = vals[e];
     if (!isfinite(v)) atomicMin(&bad[1], (unsigned long long)e);
-    rec[3 * e] = i;
-    rec[3 * e + 1] = j;
-    rec[3 * e + 2] = __float_as_uint((float)v);
-    keys[e] = shuffled ? mix32((uint32_t)e, seed) : i;
-    ids[e] = (uint32_t)e;
+    const uint64_t p = perm_n ? (uint64_t)(((unsigned __int128)pa * e + pb) % perm_n) : e;
+    if (perm_n) pos[e] = (uint32_t)p;
+    rec[3 * p] = i;
+    rec[3 * p + 1] = j;
+    rec[3 * p + 2] = __float_as_uint((float)v);
+    if (keys) {
+      keys[e] = shuffled ? mix32((uint32_t)e, seed) : i;
+      ids[e] = (uint32_t)e;
+    }
   }
   if (small) {
     __syncthreads();
@@ -1209,6 +1216,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
       CU(cudaGetLastError());
     }
     if (std::getenv("CMTF_HOT_CHECK")) {
+      CU(cudaStreamSynchronize(ctx->stream));
       // test hook: the host's stable-sort selection must give the same rows
       // in the same slots
       struct C2 { uint32_t count; int arr; uint32_t row; };
@@ -1301,6 +1309,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
       off += (3 * h.H + 3) & ~3u;
       return CMTF_OK;
     };
+    CU(cudaStreamSynchronize(ctx->stream));  // the previous sweep may still read the slots
     for (int n = 0; n < ctx->order; ++n) TRY(build(ctx->hot[n], rows_of[n], ctx->dims[n]));
     for (size_t m = 0; m < ctx->mats.size(); ++m)
       TRY(build(ctx->hotV[m], vrows_of[m], ctx->mats[m].cols));
@@ -1975,17 +1984,37 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     uint32_t* d_idx = ctx->s_idx;
     double* d_vals = ctx->s_vals;
     uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
-    CU(cudaMemcpyAsync(d_idx, idx, nnz * 2 * sizeof(uint32_t), cudaMemcpyDefault,
-                       ctx->stream));
-    CU(cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault,
-                       ctx->stream));
-    CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+    // chunked H2D on the side stream, each chunk packed as it lands; random
+    // and caller orders pack straight into the entry order (no scatter pass)
     const int shuffled = ctx->cfg.order_policy == 1;
-    pack_matrix_kernel<<<grid_for(nnz), 256,
-                         cols <= kPackHistCols ? cols * sizeof(uint32_t) : 0, ctx->stream>>>(
-        d_idx, d_vals, nnz, rows, cols, shuffled,
-        (uint32_t)ctx->cfg.seed + 0x27d4eb2fu + (uint32_t)ctx->mats.size(), d_rec, d_keys,
-        d_ids, M.count, ctx->d_first);
+    const bool direct = ctx->cfg.order_policy != 0;
+    uint64_t pa = 1, pb = 0;
+    if (shuffled) affine_params(nnz, ctx->cfg.seed + 7 + ctx->mats.size(), &pa, &pb);
+    constexpr int kChunks = 4;
+    const uint64_t chunk = (nnz + kChunks - 1) / kChunks;
+    CU(cudaEventRecord(ctx->ev_side_start, ctx->stream));  // count memset, staging reuse
+    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side_start, 0));
+    for (int k = 0; k < kChunks; ++k) {
+      const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
+      if (c0 >= c1) break;
+      CU(cudaMemcpyAsync(d_idx + 2 * c0, idx + 2 * c0, (c1 - c0) * 2 * sizeof(uint32_t),
+                         cudaMemcpyDefault, ctx->side));
+      CU(cudaMemcpyAsync(d_vals + c0, vals + c0, (c1 - c0) * sizeof(double), cudaMemcpyDefault,
+                         ctx->side));
+      CU(cudaEventRecord(ctx->cev[k], ctx->side));
+    }
+    CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+    for (int k = 0; k < kChunks; ++k) {
+      const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
+      if (c0 >= c1) break;
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->cev[k], 0));
+      pack_matrix_kernel<<<grid_for(c1 - c0), 256,
+                           cols <= kPackHistCols ? cols * sizeof(uint32_t) : 0, ctx->stream>>>(
+          d_idx, d_vals, c0, c1, rows, cols, shuffled,
+          (uint32_t)ctx->cfg.seed + 0x27d4eb2fu + (uint32_t)ctx->mats.size(),
+          direct ? M.rec : d_rec, direct ? nullptr : d_keys, d_ids, M.count, ctx->d_first,
+          direct ? nnz : 0, pa, pb, M.pos);
+    }
     CU(cudaGetLastError());
     unsigned long long bad[2];
     CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
@@ -2002,15 +2031,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
     }
     uint32_t* sorted_ids = nullptr;
-    if (ctx->cfg.order_policy == 2) {
-      scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, 3, 1, 0, M.rec,
-                                                                    M.pos);
-    } else if (shuffled) {
-      uint64_t pa, pb;
-      affine_params(nnz, ctx->cfg.seed + 7 + ctx->mats.size(), &pa, &pb);
-      scatter_affine_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_rec, nnz, 3, pa, pb,
-                                                                    M.rec, M.pos);
-    } else {
+    if (!direct) {
       TRY(sort_ids(ctx, d_keys, d_ids, nnz, rows, &sorted_ids));
       gather_records_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(
           d_rec, sorted_ids, nnz, 3, M.rec, M.pos);
@@ -2065,6 +2086,9 @@ int cmtf_gpu_set_model(cmtf_gpu_ctx* ctx, const double* core,
   if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
   if (!ctx->rec) return set_err(ctx, CMTF_EVALIDATION, "no training tensor set");
   CU(cudaSetDevice(ctx->device));
+  // the context streams are non-blocking: no kernel may still read the model
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaStreamSynchronize(ctx->side));
   std::vector<float> c(ctx->core_size());
   for (size_t d = 0; d < c.size(); ++d) c[d] = (float)core[d];
   CU(cudaMemcpy(ctx->G, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice));
@@ -2432,6 +2456,7 @@ int cmtf_gpu_set_counts(cmtf_gpu_ctx* ctx, int32_t which, const uint32_t* counts
   } else {
     return set_err(ctx, CMTF_EVALIDATION, "no such count array");
   }
+  CU(cudaStreamSynchronize(ctx->stream));  // non-blocking stream: prior readers done
   CU(cudaMemcpy(dst, counts, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
   reg_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(dst, n, lam, reg);
   CU(cudaGetLastError());
@@ -2866,8 +2891,11 @@ int cmtf_gpu_finalize_model(cmtf_gpu_ctx* ctx, double* core, double* const* fact
         R = matmul(Rk, R, J);
         CU(cudaStreamSynchronize(ctx->stream));  // Ri lives on the host stack
       }
-      if (factors && factors[n])
-        CU(cudaMemcpy(factors[n], X, rows * J * sizeof(double), cudaMemcpyDeviceToHost));
+      if (factors && factors[n]) {
+        CU(cudaMemcpyAsync(factors[n], X, rows * J * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+      }
       // core <- core x_n R: new[.. j ..] = sum_i R[j][i] core[.. i ..]
       uint64_t stride = 1;
       for (int m = N - 1; m > n; --m) stride *= ctx->J(m);
@@ -2899,8 +2927,10 @@ int cmtf_gpu_finalize_model(cmtf_gpu_ctx* ctx, double* core, double* const* fact
                          ctx->stream));
       right_mult_f64_kernel<<<grid_for(M.cols), 128, (size_t)J * J * sizeof(double),
                               ctx->stream>>>(X, M.cols, J, dM);
-      CU(cudaMemcpy(couplings[m], X, (uint64_t)M.cols * J * sizeof(double),
-                    cudaMemcpyDeviceToHost));
+      // (the context stream is non-blocking: copy on it, then wait)
+      CU(cudaMemcpyAsync(couplings[m], X, (uint64_t)M.cols * J * sizeof(double),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
     }
     if (core) std::copy(G.begin(), G.end(), core);
     return CMTF_OK;
