@@ -3,7 +3,10 @@
 //   1. T[e][ab]  = U3[e][c] * G[c][ab]       A K-major (rows e),  B K-major (rows ab)
 //   2. g3[e][c]  = P[e][ab] * G[ab][c]       A K-major (rows e),  B MN-major (G buffer)
 //   3. Dc[ab][c] = P^T[ab][e] * S[e][c]      A MN-major (P buffer), B MN-major (S buffer)
-// for both assignments of the two core-matrix strides to (LBO, SBO).
+// Variant 0 (LBO = K-direction stride, SBO = row-direction stride, every
+// operand K-major) is the layout the kernels use; exit status 1 if it is off.
+// Variant 2 reads two operands as MN-major: tf32 MN-major operands come back
+// as zeros on B200, which is why the kernels never use them.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I ../../paper_1708_08640_b200/csrc umma_test.cu -o umma_test
 #include <cmath>
 #include <cstdio>
@@ -158,6 +161,7 @@ int main() {
   const int smem = E * C * 4 + 128 * C * 4 + E * ABM * 4 + E * C * 4 + 16*128*4*2 + 128*128*4;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   Res* h = new Res;
+  int bad = 0;
   for (int variant = 0; variant < 4; variant += 2) {
     cudaMemset(dR, 0, sizeof(Res));
     kern<<<1, 128, smem>>>(dU3, dG, dP, dS, dR, variant);
@@ -186,6 +190,9 @@ int main() {
     printf("  g3[0][0..3] got %g %g %g %g   Dc[0][0..3] got %g %g %g %g\n", h->g3[0][0], h->g3[0][1], h->g3[0][2], h->g3[0][3], h->Dc[0][0], h->Dc[0][1], h->Dc[0][2], h->Dc[0][3]);
     printf("variant %d (K-major swap %d, MN-major swap %d): T err %.3g/%.3g  g3 err %.3g/%.3g  "
            "Dc err %.3g/%.3g\n", variant, variant & 1, (variant >> 1) & 1, e1, m1, e2, m2, e3, m3);
+    // TF32 operands: ~2^-11 relative per product
+    if (variant == 0 && (e1 > 2e-3 * m1 || e2 > 2e-3 * m2 || e3 > 2e-3 * m3)) bad = 1;
   }
-  return 0;
+  printf(bad ? "UMMA descriptors: FAIL\n" : "UMMA descriptors: ok\n");
+  return bad;
 }
