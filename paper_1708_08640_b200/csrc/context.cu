@@ -156,6 +156,14 @@ struct cmtf_gpu_ctx {
   uint64_t partial_cap = 0;
   unsigned long long* d_first = nullptr;
 
+  // duplicate-index check scratch (grow-only)
+  unsigned long long* dup_keys = nullptr;  // [2][cap]
+  uint64_t dup_keys_cap = 0;
+  uint32_t* dup_ids = nullptr;  // [2][cap]
+  uint64_t dup_ids_cap = 0;
+  uint8_t* dup_tmp = nullptr;
+  uint64_t dup_tmp_cap = 0;
+
   // device-side hot-row selection scratch
   unsigned long long* hs_keys = nullptr;  // [2][cap]
   uint64_t hs_keys_cap = 0;
@@ -1746,6 +1754,12 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->s_rec);
   dfree(ctx->s_keys);
   dfree(ctx->s_ids);
+  dfree(ctx->hs_keys);
+  dfree(ctx->hs_tmp);
+  dfree(ctx->hs_cnt);
+  dfree(ctx->dup_keys);
+  dfree(ctx->dup_ids);
+  dfree(ctx->dup_tmp);
   for (int n = 0; n < kMaxOrder; ++n) {
     dfree(ctx->count[n]);
     dfree(ctx->reg[n]);
@@ -1790,6 +1804,146 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   if (ctx->ev_side_done) cudaEventDestroy(ctx->ev_side_done);
   delete ctx;
   return CMTF_OK;
+}
+
+// ---------------------------------------------------------------------
+// Duplicate coordinates (check_entries, src/sparse_data.cpp:44-63): the
+// reference rejects a bundle whose tensor or matrix repeats an index tuple,
+// reporting the lexicographically smallest one.  Device version: a mixed-radix
+// key per entry (exact when the dims fit 64 bits; otherwise a 64-bit hash with
+// adjacent tuples compared), a radix sort, and a scan of neighbours.
+// ---------------------------------------------------------------------
+struct DupKey {
+  uint32_t dims[kMaxOrder];
+  int order;
+  int exact;
+};
+
+__global__ void dup_key_kernel(const uint32_t* idx, uint64_t nnz, DupKey k,
+                               unsigned long long* keys, uint32_t* ids) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0;
+    if (k.exact) {
+      for (int n = 0; n < k.order; ++n) key = key * k.dims[n] + idx[e * k.order + n];
+    } else {  // splitmix-style 64-bit hash of the tuple
+      key = 0x9e3779b97f4a7c15ull;
+      for (int n = 0; n < k.order; ++n) {
+        key ^= idx[e * k.order + n] + 0x9e3779b97f4a7c15ull + (key << 6) + (key >> 2);
+        key *= 0xbf58476d1ce4e5b9ull;
+        key ^= key >> 31;
+      }
+    }
+    keys[e] = key;
+    ids[e] = (uint32_t)e;
+  }
+}
+
+__global__ void dup_scan_kernel(const uint32_t* idx, uint64_t nnz, int order,
+                                const unsigned long long* keys, const uint32_t* ids,
+                                unsigned long long* first) {
+  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (keys[i] != keys[i - 1]) continue;
+    const uint32_t* a = idx + (uint64_t)ids[i] * order;
+    const uint32_t* b = idx + (uint64_t)ids[i - 1] * order;
+    bool same = true;
+    for (int n = 0; n < order; ++n) same = same && a[n] == b[n];
+    if (same) atomicMin(first, (unsigned long long)i);
+  }
+}
+
+// Exact keys: open-addressing set on the device (load factor <= 1/2); a
+// thread whose CAS finds its own key has a duplicate; the smallest duplicated
+// key (= the lexicographically smallest tuple) wins an atomicMin.
+__global__ void dup_hash_kernel(const uint32_t* idx, uint64_t nnz, DupKey k,
+                                unsigned long long* table, uint64_t cap_mask,
+                                unsigned long long* first_key) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0;
+    for (int n = 0; n < k.order; ++n) key = key * k.dims[n] + idx[e * k.order + n];
+    unsigned long long h = key * 0x9e3779b97f4a7c15ull;
+    h ^= h >> 29;
+    for (uint64_t s = h & cap_mask;; s = (s + 1) & cap_mask) {
+      const unsigned long long prev = atomicCAS(table + s, ~0ull, key);
+      if (prev == ~0ull) break;
+      if (prev == key) {
+        atomicMin(first_key, key);
+        break;
+      }
+    }
+  }
+}
+
+// 0: no duplicate; else writes the duplicated tuple (0-based) to *tuple.
+int find_duplicate(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int order,
+                   const uint32_t* dims, std::vector<uint32_t>* tuple, bool* found) {
+  *found = false;
+  if (nnz < 2 || std::getenv("CMTF_SKIP_DUP_CHECK")) return CMTF_OK;
+  DupKey k{};
+  k.order = order;
+  double bits = 0;
+  for (int n = 0; n < order; ++n) {
+    k.dims[n] = dims[n];
+    bits += std::log2((double)std::max<uint32_t>(dims[n], 1));
+  }
+  k.exact = bits < 63.5;
+  const int end_bit = k.exact ? std::max(1, (int)std::ceil(bits + 1e-9)) : 64;
+  if (k.exact) {
+    uint64_t cap = 1;
+    while (cap < 2 * nnz) cap <<= 1;
+    TRY(ensure(ctx, &ctx->dup_keys, &ctx->dup_keys_cap, cap));
+    unsigned long long* first = ctx->d_first;  // [0] is free after validation
+    CU(cudaMemsetAsync(ctx->dup_keys, 0xff, cap * sizeof(unsigned long long), ctx->stream));
+    CU(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
+    dup_hash_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, k, ctx->dup_keys,
+                                                            cap - 1, first);
+    unsigned long long f = ~0ull;
+    CU(cudaMemcpyAsync(&f, first, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (f != ~0ull) {  // decode the mixed-radix key
+      tuple->assign(order, 0u);
+      for (int n = order - 1; n >= 0; --n) {
+        (*tuple)[n] = (uint32_t)(f % dims[n]);
+        f /= dims[n];
+      }
+      *found = true;
+    }
+    return CMTF_OK;
+  }
+  TRY(ensure(ctx, &ctx->dup_keys, &ctx->dup_keys_cap, 2 * nnz));
+  TRY(ensure(ctx, &ctx->dup_ids, &ctx->dup_ids_cap, 2 * nnz));
+  unsigned long long *keys = ctx->dup_keys, *keys2 = ctx->dup_keys + nnz;
+  uint32_t *ids = ctx->dup_ids, *ids2 = ctx->dup_ids + nnz;
+  unsigned long long* first = ctx->d_first;  // [0] is free after validation
+  size_t tb = 0;
+  dup_key_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, k, keys, ids);
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, ids2, (int)nnz, 0, end_bit,
+                                     ctx->stream));
+  TRY(ensure(ctx, &ctx->dup_tmp, &ctx->dup_tmp_cap, tb));
+  CU(cub::DeviceRadixSort::SortPairs(ctx->dup_tmp, tb, keys, keys2, ids, ids2, (int)nnz, 0,
+                                     end_bit, ctx->stream));
+  CU(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
+  dup_scan_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, order, keys2, ids2, first);
+  unsigned long long f = ~0ull;
+  CU(cudaMemcpyAsync(&f, first, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (f != ~0ull) {
+    uint32_t id = 0;
+    CU(cudaMemcpy(&id, ids2 + f, sizeof id, cudaMemcpyDeviceToHost));
+    tuple->resize(order);
+    CU(cudaMemcpy(tuple->data(), d_idx + (uint64_t)id * order, order * sizeof(uint32_t),
+                  cudaMemcpyDeviceToHost));
+    *found = true;
+  }
+  return CMTF_OK;
+}
+
+std::string dup_message(const char* what, const std::vector<uint32_t>& t) {
+  std::string msg = std::string("duplicate ") + what + " index (";
+  for (size_t n = 0; n < t.size(); ++n) msg += (n ? " " : "") + std::to_string(t[n] + 1);
+  return msg + ")";
 }
 
 int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
@@ -1890,6 +2044,16 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
                          idx[e * N + n] + 1, dims[n]);
     }
     return set_err(ctx, CMTF_EVALIDATION, "tensor value is not finite");
+  }
+  {
+    std::vector<uint32_t> tup;
+    bool dup = false;
+    TRY(find_duplicate(ctx, d_idx, nnz, N, dims, &tup, &dup));
+    if (dup) {
+      dfree(ctx->rec);
+      ctx->rec_cap = 0;
+      return set_err(ctx, CMTF_EVALIDATION, "%s", dup_message("tensor", tup).c_str());
+    }
   }
   TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
   TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
@@ -2029,6 +2193,20 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
         return set_err(ctx, CMTF_EVALIDATION, "matrix index out of range (entry %llu)",
                        bad[0] + 1);
       return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
+    }
+    {
+      std::vector<uint32_t> tup;
+      bool dup = false;
+      const uint32_t mdims[2] = {rows, cols};
+      TRY(find_duplicate(ctx, d_idx, nnz, 2, mdims, &tup, &dup));
+      if (dup) {
+        dfree(M.count);
+        dfree(M.vreg);
+        dfree(M.V);
+        dfree(M.rec);
+        dfree(M.pos);
+        return set_err(ctx, CMTF_EVALIDATION, "%s", dup_message("matrix", tup).c_str());
+      }
     }
     uint32_t* sorted_ids = nullptr;
     if (!direct) {

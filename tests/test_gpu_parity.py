@@ -264,6 +264,39 @@ def test_validation_errors_on_bad_bundle():
         api.make_state(TrainConfig(ranks=[5, 2, 2]), api.DataBundle(t, []))
 
 
+def test_duplicate_indices_rejected_like_the_reference():
+    """check_entries (src/sparse_data.cpp:44-63): a repeated index tuple is a
+    ValidationError naming the lexicographically smallest duplicate, for the
+    tensor and for a coupled matrix -- same message as the reference's."""
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, 40, size=(5000, 3)).astype(np.uint32)
+    idx = np.unique(idx, axis=0)
+    rng.shuffle(idx)
+    dup = idx[[17, 321]].copy()
+    idx = np.concatenate([idx, dup])  # two duplicated tuples; the smaller one is reported
+    rng.shuffle(idx)
+    want = min(tuple(int(v) + 1 for v in d) for d in dup)
+    t = api.SparseTensor([40, 40, 40], idx, rng.random(len(idx)))
+    with pytest.raises(api.ValidationError) as ei:
+        api.make_state(TrainConfig(ranks=[2, 2, 2]), api.DataBundle(t, []))
+    assert str(ei.value) == "duplicate tensor index (%d %d %d)" % want
+    if O.ref_available():  # the reference's own message for the same bundle
+        with pytest.raises(ValueError) as er:
+            O.RefRun(api.DataBundle(t, []), [2, 2, 2])
+        assert str(er.value) == str(ei.value)
+    ok = np.unique(idx, axis=0)
+    t = api.SparseTensor([40, 40, 40], ok, rng.random(len(ok)))
+    m_idx = np.array([[1, 2], [3, 4], [1, 2]], dtype=np.uint32)
+    mat = api.CoupledMatrix(0, 40, 10, m_idx, np.ones(3), 1.0)
+    with pytest.raises(api.ValidationError, match=r"duplicate matrix index \(2 3\)"):
+        api.make_state(TrainConfig(ranks=[2, 2, 2]), api.DataBundle(t, [mat]))
+    # dims whose product exceeds 64 bits take the hashed path
+    big = np.array([[5, 6, 7, 8], [1, 2, 3, 4], [5, 6, 7, 8]], dtype=np.uint32)
+    t = api.SparseTensor([1 << 20] * 4, big, np.ones(3))
+    with pytest.raises(api.ValidationError, match=r"duplicate tensor index \(6 7 8 9\)"):
+        api.make_state(TrainConfig(ranks=[2, 2, 2, 2]), api.DataBundle(t, []))
+
+
 def test_order4_and_ragged_ranks_use_generic_path():
     rng = np.random.default_rng(7)
     dims, ranks = [9, 7, 6, 5], [3, 2, 4, 2]
