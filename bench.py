@@ -305,6 +305,11 @@ def run_ours(args):
                 roof["traffic_unit"] = "bytes/launch (ncu dram read+write)"
                 roof["traffic_source"] = v["report"]
                 roof["algorithmic_bytes_per_launch"] = nt * Bt
+                pick = {"fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                        "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                        "ipc": "sm__inst_executed.avg.per_cycle_active",
+                        "instructions": "smsp__inst_executed.sum"}
+                roof["ncu"] = {kk: v[name]["value"] for kk, name in pick.items() if name in v}
     except Exception:
         pass
     # epoch roofline time: both terms, slower of HBM and FP32
