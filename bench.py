@@ -281,7 +281,6 @@ def run_ours(args):
             "peak_source": f"nominal FP32: {sms} SMs x 128 FMA x 2 x 1965 MHz (no FP32 "
                            "entry in MEASURED_PEAKS.json)",
             "kernel": {"order3v2": "hog3v2_kernel (fused tensor+matrix epoch sweep)",
-                       "order3tc": "hog3tc_kernel (fused epoch sweep, tensor-core contractions)",
                        "order3tm": "hog3tm_kernel (fused epoch sweep, tcgen05 contractions + "
                                    "core gradient, TMEM accumulators)",
                        "order4": "hog4_kernel (fused epoch sweep, tensor-core contractions)",

@@ -308,7 +308,7 @@ class TrainState:
         w, t, s = C.c_int32(), C.c_int32(), C.c_int32()
         self._check(self._L.cmtf_gpu_kernel_info(self._h, C.byref(w), C.byref(t),
                                                   C.byref(s)))
-        return {"kernel": ["generic", "order3", "order4", "order3v2", "order3tc", "order3tm"][w.value],
+        return {"kernel": ["generic", "order3", "order4", "order3v2", "(retired)", "order3tm"][w.value],
                 "hog_threads": t.value, "sort_mode": s.value}
 
     def close(self):

@@ -25,7 +25,6 @@
 #include "hog3.cuh"
 #include "hog3v2.cuh"
 #include "hog4.cuh"
-#include "hog3tc.cuh"
 #include "hog3tm.cuh"
 
 using namespace cmtfb;
@@ -212,6 +211,14 @@ struct cmtf_gpu_ctx {
   double last_ms[4] = {0, 0, 0, 0};
   int32_t last_launches = 0;
   int kernel_which = 0;
+  // test / experiment switches, read once when the context is created
+  struct Env {
+    bool v4_tc = true;     // CMTF_V4_TC=0: order-4 CUDA-core sweep
+    bool v3_tm = true;     // CMTF_V3_TM=0: order-3 opt on hog3v2 instead of hog3tm
+    int v2_shape = 0;      // CMTF_V2_SHAPE: 1 = "8x1", 2 = "8x2"
+    bool hot_host = false; // CMTF_HOT_HOST: host hot-row selection
+    bool hot_check = false;// CMTF_HOT_CHECK: compare device vs host selection
+  } env;
   int hog_threads_used = 0;
 
   uint32_t J(int n) const { return ranks[n]; }
@@ -873,19 +880,7 @@ constexpr int kV2Warps = 8;  // default; 12 when registers and shared memory all
 // (CMTF_V4_TC=0 selects the CUDA-core sweep, for comparison)
 bool v4_tc(const cmtf_gpu_ctx* ctx) {
   if (ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
-  const char* v = std::getenv("CMTF_V4_TC");
-  return !(v && v[0] == '0');
-}
-
-// order 3, opt kernel: the sweep's core contractions on the tensor cores
-// (hog3tc).  Opt-in with CMTF_V3_TC=1: measured on config 2 it is slower than
-// the CUDA-core hog3v2 (4.18 vs 2.95 ms/epoch: less shared memory left for
-// hot-row replicas, per-component hot-row updates, E = 1), faster at 10%
-// scale (1.95 vs 2.61 ms).
-bool v3_tc(const cmtf_gpu_ctx* ctx) {
-  if (ctx->order != 3 || ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
-  const char* v = std::getenv("CMTF_V3_TC");
-  return v && v[0] == '1';
+  return ctx->env.v4_tc;
 }
 
 bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
@@ -901,8 +896,7 @@ bool v3_tm(const cmtf_gpu_ctx* ctx) {
   if (ctx->order != 3 || ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
   int J = 0;
   if (!v2_supported(ctx, &J)) return false;
-  const char* v = std::getenv("CMTF_V3_TM");
-  return !(v && v[0] == '0');
+  return ctx->env.v3_tm;
 }
 
 __global__ void merge_matrix_kernel(const uint32_t* rec, uint64_t n, uint32_t m, uint64_t base,
@@ -930,15 +924,12 @@ struct V2Shape {
 };
 
 V2Shape v2_shape(const cmtf_gpu_ctx* ctx, int J) {
-  (void)ctx;
   // 8 warps x 2 entries per lane; one entry per lane for J <= 5, whose tiny
   // sweep leaves the row gathers exposed (config 5 at rank 5: 22.2 vs 24.1
   // ms/epoch; 4 entries per lane: 26.7 ms)
   V2Shape s{8, J <= 5 ? 1 : 2};
-  if (const char* v = std::getenv("CMTF_V2_SHAPE")) {  // experiments: "8x1", "8x2"
-    if (std::string(v) == "8x1") s = {8, 1};
-    if (std::string(v) == "8x2") s = {8, 2};
-  }
+  if (ctx->env.v2_shape == 1) s = {8, 1};  // experiments
+  if (ctx->env.v2_shape == 2) s = {8, 2};
   return s;
 }
 
@@ -1043,9 +1034,8 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   const uint32_t JP = (uint32_t)round_up4(J);
   const bool four = ctx->order == 4;  // hog4: 8 warps, one entry per lane
   // grid: one block of kV2Warps warps per SM unless the caller caps workers
-  const bool tc3 = !four && v3_tc(ctx);
-  const bool tm3 = !four && !tc3 && v3_tm(ctx);
-  const V2Shape sh = four || tc3 || tm3 ? V2Shape{8, 1} : v2_shape(ctx, J);
+  const bool tm3 = !four && v3_tm(ctx);
+  const V2Shape sh = four || tm3 ? V2Shape{8, 1} : v2_shape(ctx, J);
   const int NW = sh.nw;
   ctx->v2_nw = NW;
   ctx->v2_e = sh.e;
@@ -1112,14 +1102,6 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
       case 10: fixed = (size_t)TMLayout<10>::FIXED_BYTES; break;
     }
   }
-  if (tc3) {
-    switch (J) {
-      case 4: fixed = sizeof(float) * (size_t)V3TCLayout<4, 8>::FIXED_FLOATS; break;
-      case 5: fixed = sizeof(float) * (size_t)V3TCLayout<5, 8>::FIXED_FLOATS; break;
-      case 8: fixed = sizeof(float) * (size_t)V3TCLayout<8, 8>::FIXED_FLOATS; break;
-      case 10: fixed = sizeof(float) * (size_t)V3TCLayout<10, 8>::FIXED_FLOATS; break;
-    }
-  }
   const size_t limit = 227 * 1024 - 2048;  // room for a co-resident gather block
   const size_t budget_floats = fixed < limit ? (limit - fixed) / sizeof(float) : 0;
   const uint64_t thr = tau > 0 ? (uint64_t)std::ceil(tau * (double)ctx->nnz / W) : ~0ull;
@@ -1144,7 +1126,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     off += (3 * h.H + 3) & ~3u;
     return CMTF_OK;
   };
-  bool device_sel = !std::getenv("CMTF_HOT_HOST") && ctx->order + ctx->mats.size() <= 16 &&
+  bool device_sel = !ctx->env.hot_host && ctx->order + ctx->mats.size() <= 16 &&
                     ctx->order <= 8;
   for (int n = 0; n < ctx->order; ++n) device_sel = device_sel && ctx->dims[n] < (1u << 28);
   for (auto& M : ctx->mats) device_sel = device_sel && M.cols < (1u << 28);
@@ -1223,7 +1205,7 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
       hot_assign_kernel<<<grid_for(take), 256, 0, ctx->stream>>>(k_sorted, k2_out, take, ha);
       CU(cudaGetLastError());
     }
-    if (std::getenv("CMTF_HOT_CHECK")) {
+    if (ctx->env.hot_check) {
       CU(cudaStreamSynchronize(ctx->stream));
       // test hook: the host's stable-sort selection must give the same rows
       // in the same slots
@@ -1367,16 +1349,6 @@ int launch_v3tm(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
   return CMTF_OK;
 }
 
-template <int J>
-int launch_v3tc(cmtf_gpu_ctx* ctx, const Hog3v2Args& args) {
-  auto kern = hog3tc_kernel<J, 8>;
-  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)ctx->v2_smem));
-  kern<<<ctx->v2_blocks, 8 * 32, ctx->v2_smem, ctx->stream>>>(args);
-  CU(cudaGetLastError());
-  return CMTF_OK;
-}
-
 // Fill the sweep arguments shared by hog3v2 and hog4 for tensor records
 // [t_lo, t_hi) and matrix records [m_lo[m], m_hi[m]) (NULL ranges = every
 // matrix entry).  Returns false when there is nothing to sweep.
@@ -1463,22 +1435,13 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
-  if (v3_tm(ctx) && !v3_tc(ctx)) {
+  if (v3_tm(ctx)) {
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
       case 5: return launch_v3tm<5>(ctx, a);
       case 8: return launch_v3tm<8>(ctx, a);
       case 10: return launch_v3tm<10>(ctx, a);
-    }
-  }
-  if (v3_tc(ctx)) {
-    ctx->kernel_which = 4;
-    switch (J) {
-      case 4: return launch_v3tc<4>(ctx, a);
-      case 5: return launch_v3tc<5>(ctx, a);
-      case 8: return launch_v3tc<8>(ctx, a);
-      case 10: return launch_v3tc<10>(ctx, a);
     }
   }
 #define V2_CASE(JV)                                                            \
@@ -1717,6 +1680,18 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
   ctx->cfg.ranks = ctx->ranks.data();
   ctx->device = cfg->device;
   ctx->eta = cfg->eta0;
+  {
+    auto off = [](const char* name) {
+      const char* v = std::getenv(name);
+      return v && v[0] == '0';
+    };
+    ctx->env.v4_tc = !off("CMTF_V4_TC");
+    ctx->env.v3_tm = !off("CMTF_V3_TM");
+    if (const char* v = std::getenv("CMTF_V2_SHAPE"))
+      ctx->env.v2_shape = std::string(v) == "8x1" ? 1 : std::string(v) == "8x2" ? 2 : 0;
+    ctx->env.hot_host = std::getenv("CMTF_HOT_HOST") != nullptr;
+    ctx->env.hot_check = std::getenv("CMTF_HOT_CHECK") != nullptr;
+  }
   auto cleanup = [&](int rc) {
     delete ctx;
     return rc;
@@ -1810,8 +1785,9 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
 // Duplicate coordinates (check_entries, src/sparse_data.cpp:44-63): the
 // reference rejects a bundle whose tensor or matrix repeats an index tuple,
 // reporting the lexicographically smallest one.  Device version: a mixed-radix
-// key per entry (exact when the dims fit 64 bits; otherwise a 64-bit hash with
-// adjacent tuples compared), a radix sort, and a scan of neighbours.
+// key per entry in a device hash set when the dims fit 64 bits; otherwise a
+// stable LSD radix sort of the entry ids by the full tuple and a scan of
+// neighbours.
 // ---------------------------------------------------------------------
 struct DupKey {
   uint32_t dims[kMaxOrder];
@@ -1819,32 +1795,27 @@ struct DupKey {
   int exact;
 };
 
-__global__ void dup_key_kernel(const uint32_t* idx, uint64_t nnz, DupKey k,
-                               unsigned long long* keys, uint32_t* ids) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    unsigned long long key = 0;
-    if (k.exact) {
-      for (int n = 0; n < k.order; ++n) key = key * k.dims[n] + idx[e * k.order + n];
-    } else {  // splitmix-style 64-bit hash of the tuple
-      key = 0x9e3779b97f4a7c15ull;
-      for (int n = 0; n < k.order; ++n) {
-        key ^= idx[e * k.order + n] + 0x9e3779b97f4a7c15ull + (key << 6) + (key >> 2);
-        key *= 0xbf58476d1ce4e5b9ull;
-        key ^= key >> 31;
-      }
-    }
-    keys[e] = key;
+__global__ void iota_u32_kernel(uint32_t* ids, uint64_t n) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x)
     ids[e] = (uint32_t)e;
-  }
 }
 
+// keys[i] = mode-n index of entry ids[i] (one LSD pass of the tuple sort)
+__global__ void mode_key_kernel(const uint32_t* idx, uint64_t nnz, int order, int n,
+                                const uint32_t* ids, uint32_t* keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = idx[(uint64_t)ids[i] * order + n];
+}
+
+// first i with tuple(ids[i]) == tuple(ids[i-1]) (keys: optional pre-filter)
 __global__ void dup_scan_kernel(const uint32_t* idx, uint64_t nnz, int order,
                                 const unsigned long long* keys, const uint32_t* ids,
                                 unsigned long long* first) {
   for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    if (keys[i] != keys[i - 1]) continue;
+    if (keys && keys[i] != keys[i - 1]) continue;
     const uint32_t* a = idx + (uint64_t)ids[i] * order;
     const uint32_t* b = idx + (uint64_t)ids[i - 1] * order;
     bool same = true;
@@ -1876,11 +1847,30 @@ __global__ void dup_hash_kernel(const uint32_t* idx, uint64_t nnz, DupKey k,
   }
 }
 
+// check_entries' first failure (src/sparse_data.cpp:29-41) from the device
+// validation's first bad entries: bad[0] = first index out of range, bad[1] =
+// first non-finite value.  The reference scans entries in order and checks an
+// entry's indices before its value; the offending tuple is read back from the
+// device staging copy (the caller's idx may be a device pointer).
+int entry_error(cmtf_gpu_ctx* ctx, const char* what, const uint32_t* d_idx, int order,
+                const uint32_t* dims, const unsigned long long* bad) {
+  if (bad[0] != ~0ull && bad[0] <= bad[1]) {
+    std::vector<uint32_t> tup(order);
+    CU(cudaMemcpy(tup.data(), d_idx + bad[0] * (uint64_t)order, order * sizeof(uint32_t),
+                  cudaMemcpyDeviceToHost));
+    for (int n = 0; n < order; ++n)
+      if (tup[n] >= dims[n])
+        return set_err(ctx, CMTF_EVALIDATION, "%s index out of range: mode %d index %u > size %u",
+                       what, n + 1, tup[n] + 1, dims[n]);
+  }
+  return set_err(ctx, CMTF_EVALIDATION, "%s value is not finite", what);
+}
+
 // 0: no duplicate; else writes the duplicated tuple (0-based) to *tuple.
-int find_duplicate(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int order,
-                   const uint32_t* dims, std::vector<uint32_t>* tuple, bool* found) {
+int find_duplicate_impl(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int order,
+                        const uint32_t* dims, std::vector<uint32_t>* tuple, bool* found) {
   *found = false;
-  if (nnz < 2 || std::getenv("CMTF_SKIP_DUP_CHECK")) return CMTF_OK;
+  if (nnz < 2) return CMTF_OK;
   DupKey k{};
   k.order = order;
   double bits = 0;
@@ -1889,7 +1879,6 @@ int find_duplicate(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int o
     bits += std::log2((double)std::max<uint32_t>(dims[n], 1));
   }
   k.exact = bits < 63.5;
-  const int end_bit = k.exact ? std::max(1, (int)std::ceil(bits + 1e-9)) : 64;
   if (k.exact) {
     uint64_t cap = 1;
     while (cap < 2 * nnz) cap <<= 1;
@@ -1912,32 +1901,56 @@ int find_duplicate(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int o
     }
     return CMTF_OK;
   }
-  TRY(ensure(ctx, &ctx->dup_keys, &ctx->dup_keys_cap, 2 * nnz));
+  // beyond 64 bits: stable LSD radix sort of the entry ids by the full tuple
+  // (one 32-bit pass per mode, last mode first), so equal tuples are adjacent
+  // and the first equal neighbour pair is the lexicographically smallest
+  // duplicate, exactly the reference's sort + scan
+  TRY(ensure(ctx, &ctx->dup_keys, &ctx->dup_keys_cap, nnz));  // 2 x u32 keys
   TRY(ensure(ctx, &ctx->dup_ids, &ctx->dup_ids_cap, 2 * nnz));
-  unsigned long long *keys = ctx->dup_keys, *keys2 = ctx->dup_keys + nnz;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ctx->dup_keys);
+  uint32_t* keys2 = keys + nnz;
   uint32_t *ids = ctx->dup_ids, *ids2 = ctx->dup_ids + nnz;
   unsigned long long* first = ctx->d_first;  // [0] is free after validation
+  iota_u32_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(ids, nnz);
   size_t tb = 0;
-  dup_key_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, k, keys, ids);
-  CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, ids2, (int)nnz, 0, end_bit,
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, ids2, nnz, 0, 32,
                                      ctx->stream));
   TRY(ensure(ctx, &ctx->dup_tmp, &ctx->dup_tmp_cap, tb));
-  CU(cub::DeviceRadixSort::SortPairs(ctx->dup_tmp, tb, keys, keys2, ids, ids2, (int)nnz, 0,
-                                     end_bit, ctx->stream));
+  for (int n = order - 1; n >= 0; --n) {
+    mode_key_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, order, n, ids, keys);
+    const int end_bit = std::max(1, (int)std::ceil(std::log2((double)dims[n] + 1.0)));
+    CU(cub::DeviceRadixSort::SortPairs(ctx->dup_tmp, tb, keys, keys2, ids, ids2, nnz, 0,
+                                       std::min(32, end_bit), ctx->stream));
+    std::swap(ids, ids2);
+  }
   CU(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ctx->stream));
-  dup_scan_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, order, keys2, ids2, first);
+  dup_scan_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, nnz, order, nullptr, ids, first);
+  CU(cudaGetLastError());
   unsigned long long f = ~0ull;
   CU(cudaMemcpyAsync(&f, first, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   if (f != ~0ull) {
     uint32_t id = 0;
-    CU(cudaMemcpy(&id, ids2 + f, sizeof id, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&id, ids + f, sizeof id, cudaMemcpyDeviceToHost));
     tuple->resize(order);
     CU(cudaMemcpy(tuple->data(), d_idx + (uint64_t)id * order, order * sizeof(uint32_t),
                   cudaMemcpyDeviceToHost));
     *found = true;
   }
   return CMTF_OK;
+}
+
+// The check's scratch (up to 16 B per entry: 16 GB at 1e9 entries) is
+// released as soon as the check is done instead of living with the context.
+int find_duplicate(cmtf_gpu_ctx* ctx, const uint32_t* d_idx, uint64_t nnz, int order,
+                   const uint32_t* dims, std::vector<uint32_t>* tuple, bool* found) {
+  const int rc = find_duplicate_impl(ctx, d_idx, nnz, order, dims, tuple, found);
+  cudaStreamSynchronize(ctx->stream);
+  dfree(ctx->dup_keys);
+  dfree(ctx->dup_ids);
+  dfree(ctx->dup_tmp);
+  ctx->dup_keys_cap = ctx->dup_ids_cap = ctx->dup_tmp_cap = 0;
+  return rc;
 }
 
 std::string dup_message(const char* what, const std::vector<uint32_t>& t) {
@@ -2035,15 +2048,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   if (bad[0] != ~0ull || bad[1] != ~0ull) {
     dfree(ctx->rec);
     ctx->rec_cap = 0;
-    if (bad[0] != ~0ull) {
-      const uint64_t e = bad[0];
-      for (int n = 0; n < N; ++n)
-        if (idx[e * N + n] >= dims[n])
-          return set_err(ctx, CMTF_EVALIDATION,
-                         "tensor index out of range: mode %d index %u > size %u", n + 1,
-                         idx[e * N + n] + 1, dims[n]);
-    }
-    return set_err(ctx, CMTF_EVALIDATION, "tensor value is not finite");
+    return entry_error(ctx, "tensor", d_idx, N, dims, bad);
   }
   {
     std::vector<uint32_t> tup;
@@ -2189,10 +2194,8 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       dfree(M.V);
       dfree(M.rec);
       dfree(M.pos);
-      if (bad[0] != ~0ull)
-        return set_err(ctx, CMTF_EVALIDATION, "matrix index out of range (entry %llu)",
-                       bad[0] + 1);
-      return set_err(ctx, CMTF_EVALIDATION, "matrix value is not finite");
+      const uint32_t mdims[2] = {rows, cols};
+      return entry_error(ctx, "matrix", d_idx, 2, mdims, bad);
     }
     {
       std::vector<uint32_t> tup;
@@ -2897,14 +2900,15 @@ __global__ void rows_to_f64_kernel(const float* U, uint64_t rows, uint32_t J, ui
   }
 }
 
-// gram[a][b] += sum_i X[i][a] X[i][b]; thread t of a block owns pair t
+// gram[a][b] += sum_i X[i][a] X[i][b]; the J*J pairs are strided over the
+// block (any J up to kMaxRank with a fixed 256-thread block)
 __global__ void gram_f64_kernel(const double* X, uint64_t rows, uint32_t J, double* gram) {
-  const uint32_t t = threadIdx.x;
-  const uint32_t a = t / J, b = t - (t / J) * J;
-  if (t >= J * J) return;
-  double acc = 0.0;
-  for (uint64_t i = blockIdx.x; i < rows; i += gridDim.x) acc += X[i * J + a] * X[i * J + b];
-  atomicAdd(gram + t, acc);
+  for (uint32_t t = threadIdx.x; t < J * J; t += blockDim.x) {
+    const uint32_t a = t / J, b = t - (t / J) * J;
+    double acc = 0.0;
+    for (uint64_t i = blockIdx.x; i < rows; i += gridDim.x) acc += X[i * J + a] * X[i * J + b];
+    atomicAdd(gram + t, acc);
+  }
 }
 
 // X <- X M (M: J x J row-major)
@@ -2925,13 +2929,17 @@ __global__ void right_mult_f64_kernel(double* X, uint64_t rows, uint32_t J, cons
 }
 
 namespace {
-// Upper R (row-major, J x J) with R^T R = A; false if A is not positive definite.
+// Upper R (row-major, J x J) with R^T R = A; false if A is not (numerically)
+// positive definite: a pivot below 1e-13 of its diagonal means the factor's
+// condition number is beyond what CholeskyQR2 resolves in f64 (~1e6.5), and
+// the caller falls back to Householder QR.
 bool cholesky_upper(const std::vector<double>& A, uint32_t J, std::vector<double>& R) {
   R.assign((size_t)J * J, 0.0);
   for (uint32_t k = 0; k < J; ++k) {
     double d = A[(size_t)k * J + k];
+    const double diag = d;
     for (uint32_t i = 0; i < k; ++i) d -= R[(size_t)i * J + k] * R[(size_t)i * J + k];
-    if (!(d > 0.0)) return false;
+    if (!(d > 1e-13 * diag)) return false;
     const double rkk = std::sqrt(d);
     R[(size_t)k * J + k] = rkk;
     for (uint32_t j = k + 1; j < J; ++j) {
@@ -2941,6 +2949,57 @@ bool cholesky_upper(const std::vector<double>& A, uint32_t J, std::vector<double
     }
   }
   return true;
+}
+
+// Householder QR of X (rows x J, row-major, f64) in place: X <- Q (thin,
+// rows x J) and R (J x J, upper), with the reference's sign fix (a negative
+// R diagonal flips that row of R and column of Q, src/tucker.cpp:250-255).
+// The host fallback of the device CholeskyQR2 for ill-conditioned or
+// rank-deficient factors, where Eigen's HouseholderQR (the reference) still
+// returns a factorisation.
+void householder_qr(std::vector<double>& X, uint64_t rows, uint32_t J, std::vector<double>& R) {
+  std::vector<std::vector<double>> V(J);
+  std::vector<double> beta(J, 0.0);
+  for (uint32_t k = 0; k < J; ++k) {
+    double nrm = 0.0;
+    for (uint64_t i = k; i < rows; ++i) nrm += X[i * J + k] * X[i * J + k];
+    nrm = std::sqrt(nrm);
+    std::vector<double>& v = V[k];
+    v.assign(rows - k, 0.0);
+    for (uint64_t i = k; i < rows; ++i) v[i - k] = X[i * J + k];
+    const double x0 = v[0];
+    const double alpha = x0 >= 0 ? -nrm : nrm;
+    v[0] = x0 - alpha;
+    double vv = 0.0;
+    for (double q : v) vv += q * q;
+    beta[k] = vv > 0.0 ? 2.0 / vv : 0.0;
+    for (uint32_t j = k; j < J; ++j) {  // A[k:, j] -= beta v (v . A[k:, j])
+      double dot = 0.0;
+      for (uint64_t i = k; i < rows; ++i) dot += v[i - k] * X[i * J + j];
+      dot *= beta[k];
+      for (uint64_t i = k; i < rows; ++i) X[i * J + j] -= dot * v[i - k];
+    }
+  }
+  R.assign((size_t)J * J, 0.0);
+  for (uint32_t a = 0; a < J; ++a)
+    for (uint32_t b = a; b < J; ++b) R[(size_t)a * J + b] = X[(uint64_t)a * J + b];
+  // Q = H_0 ... H_{J-1} [I; 0]
+  std::fill(X.begin(), X.end(), 0.0);
+  for (uint32_t k = 0; k < J; ++k) X[(uint64_t)k * J + k] = 1.0;
+  for (int k = (int)J - 1; k >= 0; --k) {
+    const std::vector<double>& v = V[k];
+    for (uint32_t j = 0; j < J; ++j) {
+      double dot = 0.0;
+      for (uint64_t i = k; i < rows; ++i) dot += v[i - k] * X[i * J + j];
+      dot *= beta[k];
+      for (uint64_t i = k; i < rows; ++i) X[i * J + j] -= dot * v[i - k];
+    }
+  }
+  for (uint32_t k = 0; k < J; ++k)
+    if (R[(size_t)k * J + k] < 0) {
+      for (uint32_t b = 0; b < J; ++b) R[(size_t)k * J + b] = -R[(size_t)k * J + b];
+      for (uint64_t i = 0; i < rows; ++i) X[i * J + k] = -X[i * J + k];
+    }
 }
 
 // inverse of an upper-triangular R (row-major)
@@ -3048,26 +3107,46 @@ int cmtf_gpu_finalize_model(cmtf_gpu_ctx* ctx, double* core, double* const* fact
       const uint32_t J = ctx->J(n), JP = ctx->JP(n);
       const uint64_t rows = ctx->dims[n];
       rows_to_f64_kernel<<<grid_for(rows * J), 256, 0, ctx->stream>>>(ctx->U[n], rows, J, JP, X);
+      CU(cudaGetLastError());
       std::vector<double> R((size_t)J * J, 0.0);
       for (uint32_t k = 0; k < J; ++k) R[(size_t)k * J + k] = 1.0;
-      for (int pass = 0; pass < 2; ++pass) {  // CholeskyQR2
+      bool chol_ok = true;
+      for (int pass = 0; pass < 2 && chol_ok; ++pass) {  // CholeskyQR2
         CU(cudaMemsetAsync(dgram, 0, (size_t)J * J * sizeof(double), ctx->stream));
-        gram_f64_kernel<<<(unsigned)std::min<uint64_t>(rows, 4096), (J * J + 31) / 32 * 32, 0,
-                          ctx->stream>>>(X, rows, J, dgram);
+        gram_f64_kernel<<<(unsigned)std::min<uint64_t>(rows, 4096), 256, 0, ctx->stream>>>(
+            X, rows, J, dgram);
+        CU(cudaGetLastError());
         std::vector<double> A((size_t)J * J), Rk;
         CU(cudaMemcpyAsync(A.data(), dgram, A.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
-        if (!cholesky_upper(A, J, Rk))
-          return set_err(ctx, CMTF_EVALIDATION,
-                         "factor %d is rank deficient; cannot orthogonalize", n + 1);
+        if (!cholesky_upper(A, J, Rk)) {
+          chol_ok = false;
+          break;
+        }
         const std::vector<double> Ri = upper_inverse(Rk, J);
         CU(cudaMemcpyAsync(dM, Ri.data(), Ri.size() * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
         right_mult_f64_kernel<<<grid_for(rows), 128, (size_t)J * J * sizeof(double),
                                 ctx->stream>>>(X, rows, J, dM);
+        CU(cudaGetLastError());
         R = matmul(Rk, R, J);
         CU(cudaStreamSynchronize(ctx->stream));  // Ri lives on the host stack
+      }
+      if (!chol_ok) {
+        // ill-conditioned or rank-deficient factor: Householder QR on the
+        // host from the factor as trained (the reference's algorithm)
+        rows_to_f64_kernel<<<grid_for(rows * J), 256, 0, ctx->stream>>>(ctx->U[n], rows, J, JP,
+                                                                        X);
+        CU(cudaGetLastError());
+        std::vector<double> hX(rows * J);
+        CU(cudaMemcpyAsync(hX.data(), X, hX.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        householder_qr(hX, rows, J, R);
+        CU(cudaMemcpyAsync(X, hX.data(), hX.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
       }
       if (factors && factors[n]) {
         CU(cudaMemcpyAsync(factors[n], X, rows * J * sizeof(double), cudaMemcpyDeviceToHost,

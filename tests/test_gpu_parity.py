@@ -477,25 +477,6 @@ def test_config4_rmse_within_1pct_of_reference():
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
 
 
-def test_order3_tensor_core_sweep_rmse_within_1pct(monkeypatch):
-    """hog3tc (opt-in order-3 kernel with the sweep's contractions on the
-    tensor cores): config 2 at 10% scale vs the reference's own run."""
-    import json
-    import os
-    from conftest import GOLDEN
-    monkeypatch.setenv("CMTF_V3_TC", "1")
-    ref = json.load(open(os.path.join(GOLDEN, "config2_s01_reference.json")))
-    b, test, _ = synth.generate(synth.config2(0.1))
-    st = api.make_state(TrainConfig(ranks=[10, 10, 10], eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
-    for _ in range(10):
-        api.run_epoch(st)
-    assert st.kernel_info()["kernel"] == "order3tc"
-    tr = api.epoch_stats(st, 0.01).train_rmse
-    te = api.test_rmse(st, test)
-    assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
-    assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
-
-
 @pytest.mark.parametrize("which", ["config1", "config2"])
 def test_device_hot_selection_matches_host(which, monkeypatch):
     """The device-side hot-row selection (radix sort of (count, array, row)
