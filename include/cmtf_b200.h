@@ -182,6 +182,17 @@ int cmtf_gpu_entry_grads(cmtf_gpu_ctx *ctx, const uint64_t *ids, uint64_t n,
                          double *xhat, double *residual, double *grow,
                          double *gcore);
 
+/* The product epoch kernel's own arithmetic at the frozen device model
+ * (order 3, opt kernel, tcgen05 path): one sweep with eta = 0 -- the model is
+ * unchanged -- recording for every training entry (caller order) x_hat, the
+ * residual and the row gradients [nnz][3 J] (compute_gradient_opt,
+ * src/gradients.cpp:130-223, as computed inside the epoch kernel's tensor-core
+ * tiles), plus the summed data term of the core gradient,
+ * sum_e -r_e u1 (x) u2 (x) u3 [J^3].  Any output may be NULL.
+ * CMTF_EUNSUPPORTED when the epoch does not run that kernel. */
+int cmtf_gpu_kernel_probe(cmtf_gpu_ctx *ctx, double *xhat, double *residual,
+                          double *grow, double *gcore_data);
+
 /* Stateless batched form of compute_gradient / compute_gradient_opt
  * (include/cmtf/gradients.hpp:59-74): n independent entries, each with its
  * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core. */

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("cmtf_gpu_matrix_rmse", C.c_int, [P, C.c_int32, f64p]),
     ("cmtf_gpu_train", C.c_int, [P, f64p, C.c_int32, i32p]),
     ("cmtf_gpu_entry_grads", C.c_int, [P, u64p, C.c_uint64, f64p, f64p, f64p, f64p]),
+    ("cmtf_gpu_kernel_probe", C.c_int, [P, f64p, f64p, f64p, f64p]),
     ("cmtf_gpu_compute_gradient", C.c_int,
      [C.c_int32, C.c_int32, u32p, f64p, C.c_uint64, f64p, f64p, u32p, C.c_double,
       C.c_uint64, C.c_int32, f64p, f64p, f64p, C.c_int32]),

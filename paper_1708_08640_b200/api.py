@@ -406,6 +406,22 @@ def entry_grads(state: TrainState, ids, with_core: bool = True):
     return xhat, r, grow, gcore
 
 
+def kernel_probe(state: TrainState):
+    """The epoch kernel's own per-entry arithmetic at the frozen device model
+    (order 3 opt, tcgen05 kernel): one eta = 0 sweep; returns x_hat [nnz],
+    r [nnz], the row gradients [nnz, 3 J] and the summed core-gradient data
+    term sum_e -r_e u1 (x) u2 (x) u3 [J, J, J].  Entries in caller order."""
+    ranks = [int(r) for r in state.config.ranks]
+    n = int(state.bundle.tensor.nnz)
+    xhat, r = np.zeros(n), np.zeros(n)
+    grow = np.zeros((n, sum(ranks)))
+    gcore = np.zeros(ranks)
+    state._check(state._L.cmtf_gpu_kernel_probe(
+        state._h, _ptr(xhat, C.c_double), _ptr(r, C.c_double), _ptr(grow, C.c_double),
+        _ptr(gcore, C.c_double)))
+    return xhat, r, grow, gcore
+
+
 def _compute_gradient(kernel: int, x, core, rows, lambda_reg, counts, nnz_total,
                       with_core=True, device=0):
     core = np.ascontiguousarray(core, dtype=np.float64)

@@ -211,6 +211,8 @@ struct cmtf_gpu_ctx {
   double last_ms[4] = {0, 0, 0, 0};
   int32_t last_launches = 0;
   int kernel_which = 0;
+  float* probe = nullptr;       // kernel probe outputs (cmtf_gpu_kernel_probe)
+  float* probe_core = nullptr;
   // test / experiment switches, read once when the context is created
   struct Env {
     bool v4_tc = true;     // CMTF_V4_TC=0: order-4 CUDA-core sweep
@@ -1419,6 +1421,8 @@ bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint6
   a.flush_every = F;
   a.core_every = FG;
   a.nonneg = ctx->cfg.nonnegative;
+  a.probe = ctx->probe;
+  a.probe_core = ctx->probe_core;
   ctx->hog_threads_used = (int)W;
   return true;
 }
@@ -3288,6 +3292,60 @@ int cmtf_gpu_entry_grads(cmtf_gpu_ctx* ctx, const uint64_t* ids, uint64_t n,
   if (gcore)
     for (uint64_t q = 0; q < hc.size(); ++q) gcore[q] = hc[q];
   return CMTF_OK;
+}
+
+// The product epoch kernel's own per-entry arithmetic at the frozen device
+// model: one hog3tm sweep with eta = 0 (every step and push is zero, so the
+// model does not change) that records each tensor entry's x_hat, residual and
+// row gradients (compute_gradient_opt, src/gradients.cpp:130-223) and the
+// summed data term sum_e -r_e u1 (x) u2 (x) u3 of the core gradient, as the
+// kernel computed them inside its tensor-core tiles.
+int cmtf_gpu_kernel_probe(cmtf_gpu_ctx* ctx, double* xhat, double* residual, double* grow,
+                          double* gcore_data) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  int J = 0;
+  if (ctx->cfg.exec_mode == CMTF_EXEC_SERIAL || ctx->order != 3 || !v2_supported(ctx, &J) ||
+      !v3_tm(ctx))
+    return set_err(ctx, CMTF_EUNSUPPORTED,
+                   "kernel probe: the epoch does not run the order-3 tcgen05 kernel");
+  const uint64_t nnz = ctx->nnz, rec_len = 2 + 3 * (uint64_t)J, csz = ctx->core_size();
+  float *d_p = nullptr, *d_c = nullptr;
+  TRY(dalloc(ctx, &d_p, nnz * rec_len));
+  TRY(dalloc(ctx, &d_c, csz));
+  int rc = CMTF_OK;
+  auto run = [&]() -> int {
+    CU(cudaMemsetAsync(d_c, 0, csz * sizeof(float), ctx->stream));
+    TRY(normalize_pos(ctx));
+    ctx->probe = d_p;
+    ctx->probe_core = d_c;
+    const int r = v2_sweep(ctx, J, 0.f, 0, nnz, nullptr, nullptr);
+    ctx->probe = ctx->probe_core = nullptr;
+    TRY(r);
+    std::vector<float> hp(nnz * rec_len), hc(csz);
+    std::vector<uint32_t> pos(nnz);
+    CU(cudaMemcpyAsync(hp.data(), d_p, hp.size() * sizeof(float), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(hc.data(), d_c, hc.size() * sizeof(float), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(pos.data(), ctx->pos, nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t k = 0; k < nnz; ++k) {
+      const float* q = hp.data() + (uint64_t)pos[k] * rec_len;
+      if (xhat) xhat[k] = q[0];
+      if (residual) residual[k] = q[1];
+      if (grow)
+        for (uint64_t t = 0; t < 3 * (uint64_t)J; ++t) grow[k * 3 * J + t] = q[2 + t];
+    }
+    if (gcore_data)
+      for (uint64_t t = 0; t < csz; ++t) gcore_data[t] = hc[t];
+    return CMTF_OK;
+  };
+  rc = run();
+  cudaFree(d_p);
+  cudaFree(d_c);
+  return rc;
 }
 
 int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ranks,

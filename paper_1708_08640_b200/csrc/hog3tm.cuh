@@ -1,6 +1,6 @@
 // hog3tm.cuh -- order-3 S^3CMTF epoch kernel with the per-entry core
 // contractions AND the core gradient on the 5th-generation tensor cores
-// (tcgen05.mma, accumulators in tensor memory).
+// (tcgen05.mma, accumulators in tensor memory), at fp32-level accuracy.
 //
 // Same epoch contract as hog3v2 (one launch = one epoch over the tensor and
 // the coupled matrices, hot-row replicas with damped merges, interleaved
@@ -14,19 +14,28 @@
 //   V[e][(a,c)] = sum_b u2_e[b] G[a,b,c]      MMA  A = U2 tile, B = G (ac x b)
 //   W1[a] = sum_b T[ab] u2[b],  g2[b] = sum_a T[ab] u1[a],  g3[c] = sum_a V[ac] u1[a],
 //   x_hat = sum_a W1[a] u1[a]                 FP32, 3 J^2 FMAs per entry
-//   dG[(a,b)][c] += sum_e P^T[ab][e] S[e][c]  MMA  A = P^T (u1[a] u2[b] per entry),
-//                                                  B = S^T (-r u3 per entry), fp16
+//   dG[(a,b)][c] += sum_e P[e][ab] S[e][c]    MMA  A = P (u1[a] u2[b] per entry),
+//                                                  B = S (-r u3 per entry)
 //
-// so an entry costs ~3J^2 FP32 FMAs instead of hog3v2's 2J^3 + 3J^2, and the
-// core gradient accumulates in tensor memory across the tile's 128 entries.
-// All operands are K-major, no-swizzle canonical layouts (umma.cuh): the
-// factor rows gathered with cp.async land directly in the U2/U3 operand tiles
-// (row e = 16-byte chunks at stride 2048 B), P^T and S^T are written as
-// transposed columns (one 4-byte store per element, bank-conflict-free).
-// The sweep MMAs take TF32 operands (the gathered fp32 rows as they are); the
-// core-gradient operands are fp16 (the same 10-bit mantissa as TF32, half the
-// shared memory: it goes to hot-row replicas), S^T pre-scaled by 2^8 so small
-// residuals stay normal; fp32 accumulation everywhere.
+// so an entry costs ~3J^2 FP32 FMAs instead of hog3v2's 2J^3 + 3J^2.
+//
+// Accuracy: every operand is split x = hi + lo into two fp16 values (after a
+// power-of-two scale that keeps both in range) and each product is formed as
+// hi*hi + hi*lo + lo*hi in three kind::f16 MMAs accumulating in fp32 -- about
+// 22 mantissa bits per product (5e-7 relative on the B200,
+// scripts/micro/umma_prec.cu), i.e. the north_star's 1e-5 per-entry bound
+// holds for the kernel's own arithmetic (tests/test_gpu_parity.py,
+// test_hog3tm_kernel_probe_*).
+//
+// Operand layouts (umma.cuh): the sweep operands are K-major (entry rows of
+// 16 bytes, so the cp.async row gathers land in the tile and the owning
+// thread rewrites its row as fp16 hi/lo with 16-byte stores); the core
+// gradient's P and S are MN-major, so thread e writes its own P row (J^2
+// values) and S row with 16-byte stores.  The core gradient runs per warp: a
+// warp's 32 entries are K = 32 of the MMA, the warpgroup's 4 warps share two
+// operand slots (warps 0/2 and 1/3 take turns: the second waits for the
+// first's MMA to finish reading) with one TMEM accumulator per slot, summed
+// at the push.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -56,43 +65,75 @@ namespace cmtfb {
 __host__ __device__ constexpr int round_up8(int x) { return (x + 7) & ~7; }
 __host__ __device__ constexpr int round_up16(int x) { return (x + 15) & ~15; }
 
+// Operand scales (powers of two, exact) keeping the fp16 splits in range:
+// |u| < 511 and |g| < 511 in the sweep, |u1 u2| < 255 and |r u3| < 255 in the
+// core gradient (beyond that the split clamps, which only a diverged model
+// reaches; the epoch's non-finite scan reports those).
+constexpr float kSU = 128.f, kSG = 128.f, kSP = 256.f, kSS = 256.f;
+
 template <int J>
 struct TMLayout {
   static constexpr int JP = round_up4(J);
-  static constexpr int KT = round_up8(J);      // K of the sweep MMAs (c or b, zero padded)
   static constexpr int AB = J * J;
-  static constexpr int NT = round_up16(AB);    // N of the sweep MMAs ((a,b) or (a,c))
-  static constexpr int MR = round_up8(AB);     // stored rows of P^T (the MMA reads 128)
-  static constexpr int KC = 16;                // N of the core-gradient MMA (c, zero padded)
-  // byte strides between 4-column groups (K direction); rows are 16 B apart
-  static constexpr int G_KS = NT * 16;
-  static constexpr int U_KS = 128 * 16;
-  // fp16 core-gradient operands: 8 entries per 16-byte row chunk
-  static constexpr int PT_KS = MR * 16 + 16;   // +16: column writes hit distinct banks
-  // S^T column-group stride: holds the 16 c rows, makes a warp's 4 column
-  // groups (its own slab) big enough for its push transpose (32 x J floats),
-  // and keeps the column writes conflict-free ((ST_KS / 4) mod 8 == 4)
-  static constexpr int st_ks(int v) { return (v % 16 == 0 && (v / 4) % 8 == 4) ? v : st_ks(v + 16); }
-  static constexpr int ST_KS = st_ks(KC * 16 > 32 * J ? KC * 16 : 32 * J);
-  static constexpr int G_BYTES = (KT / 4) * G_KS;
-  static constexpr int U_BYTES = (KT / 4) * U_KS;
-  static constexpr int U1_BYTES = 128 * JP * 4;
-  static constexpr int PT_BYTES = 16 * PT_KS;  // 128 entries = 16 groups of 8
-  // S^T also serves as the core push's transpose scratch (4 warps x 32 rows x J)
-  static constexpr int ST_BYTES = 16 * ST_KS;
-  // per warpgroup: P^T first (the M = 128 MMA reads rows MR..127 of the last
-  // column group past its end: they land in S^T / U tiles, and only feed the
-  // ignored core-gradient rows ab >= J^2)
-  static constexpr int WG_BYTES = PT_BYTES + ST_BYTES + 2 * U_BYTES + U1_BYTES;
-  static constexpr int FIXED_BYTES = 2 * G_BYTES + 2 * WG_BYTES;
+  static constexpr int NT = round_up16(AB);  // N of the sweep MMAs ((a,b) or (a,c))
+  static constexpr int NCH = (AB + 7) / 8;   // 8-wide (a,b) chunks of a P row
+  // sweep operands, fp16 K-major, K = 16 (c or b, zero padded): rows 16 B
+  // apart in 8-row groups of 128 B (SBO), the two K groups LBO apart
+  static constexpr int U_LBO = 128 * 16;
+  static constexpr int U_TILE = 2 * U_LBO;  // one hi or lo tile of 128 entries
+  static constexpr int G_LBO = NT * 16;
+  static constexpr int G_TILE = 2 * G_LBO;
+  // core-gradient slot: 32 entries (K) of P (M = (a,b)) and S (N = c),
+  // MN-major: 16-byte chunks of 8 (a,b) / c values, the 4 K groups of 8
+  // entries 128 B apart (LBO), chunks 512 B apart (SBO)
+  static constexpr int P_LBO = 128, P_SBO = 512;
+  static constexpr int P_BYTES = NCH * P_SBO;
+  static constexpr int S_BYTES = 2 * P_SBO;
+  static constexpr int SLOT = 2 * P_BYTES + 2 * S_BYTES;  // P hi, P lo, S hi, S lo
+  static constexpr int U1_BYTES = 128 * JP * 4;            // fp32 staging of u1
+  // per warpgroup: the two slots first (the M = 128 core MMA reads 16 (a,b)
+  // chunks of P; those past NCH land in the following buffers and only feed
+  // the ignored accumulator rows ab >= J^2)
+  static constexpr int WG_BYTES = 2 * SLOT + 4 * U_TILE + U1_BYTES;
+  static constexpr int G_BYTES = 4 * G_TILE;  // G (ab x c) hi, lo; G (ac x b) hi, lo
+  static constexpr int FIXED_BYTES = G_BYTES + 2 * WG_BYTES;
   static constexpr int FIXED_FLOATS = FIXED_BYTES / 4;
-  // tensor memory per warpgroup: T [0, NT), V [NT, 2 NT), dG [2 NT, 2 NT + KC)
-  static constexpr int TM_COLS = 2 * NT + KC;
+  // tensor memory per warpgroup: T [0, NT), V [NT, 2 NT), dG of slot 0 / 1
+  static constexpr int TM_COLS = 2 * NT + 32;
   static_assert(TM_COLS <= 256, "two warpgroups must fit in 512 TMEM columns");
   static_assert(AB <= 128, "core-gradient MMA has M = 128 rows (a,b)");
-  // the staged hot-row merge fits a warp's P^T slice (J >= 8)
-  static constexpr bool FSTAGE = 2 * 32 * 2 * JP * 4 <= 4 * PT_KS;
+  // while the slots are free (after the iteration's core MMAs), each of the
+  // two warps sharing a slot owns one half of it: its push transpose scratch
+  // (32 rows x J floats) and its staged hot-row merge buffer (2 stages x 32
+  // lanes x 2 JP floats) both live there
+  static constexpr int HALF = SLOT / 2;
+  static_assert(32 * J * 4 <= HALF, "push transpose scratch fits half a slot");
+  static constexpr int STAGE_WARP = 2 * 32 * 2 * JP * 4;
+  static constexpr bool FSTAGE = STAGE_WARP <= HALF;
 };
+
+// x -> hi + lo, two fp16 values (x already scaled; clamped to the fp16 range)
+__device__ __forceinline__ void split_h(float x, __half& h, __half& l) {
+  x = fminf(fmaxf(x, -65504.f), 65504.f);
+  h = __float2half_rn(x);
+  l = __float2half_rn(x - __half2float(h));
+}
+// 8 values * s -> one 16-byte chunk of hi halves and one of lo halves
+__device__ __forceinline__ void split8(const float* v, float s, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float x0 = fminf(fmaxf(v[2 * q] * s, -65504.f), 65504.f);
+    const float x1 = fminf(fmaxf(v[2 * q + 1] * s, -65504.f), 65504.f);
+    const __half2 hh = __floats2half2_rn(x0, x1);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    h[q] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[q] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
 
 // Hot-row merge (flush_hot's arithmetic, hog3v2.cuh) with the two global reads
 // of each row -- its current value and this block's base -- staged through
@@ -179,42 +220,55 @@ __device__ __forceinline__ void flush_all_hot_staged(const Args& a, float* sm, i
 template <int J>
 __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   using L = TMLayout<J>;
-  constexpr int JP = L::JP, KT = L::KT, AB = L::AB, NT = L::NT;
+  constexpr int JP = L::JP, AB = L::AB, NT = L::NT, NCH = L::NCH;
   constexpr int NW = 8;
   extern __shared__ __align__(1024) float sm[];
   uint8_t* smb = reinterpret_cast<uint8_t*>(sm);
-  uint8_t* Gc = smb;                 // B of T:  rows (a,b), K = c
-  uint8_t* Gb = smb + L::G_BYTES;    // B of V:  rows (a,c), K = b
+  uint8_t* Gch = smb;                  // B of T: rows (a,b), K = c
+  uint8_t* Gcl = Gch + L::G_TILE;
+  uint8_t* Gbh = Gcl + L::G_TILE;      // B of V: rows (a,c), K = b
+  uint8_t* Gbl = Gbh + L::G_TILE;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = threadIdx.x >> 7;    // warpgroup
-  const int e = threadIdx.x & 127;   // tile row = TMEM lane
-  uint8_t* wgb = smb + 2 * L::G_BYTES + g * L::WG_BYTES;
-  uint8_t* PT = wgb;
-  uint8_t* ST = PT + L::PT_BYTES;
-  uint8_t* tU2 = ST + L::ST_BYTES;
-  uint8_t* tU3 = tU2 + L::U_BYTES;
-  float* sU1 = reinterpret_cast<float*>(tU3 + L::U_BYTES);
-  __shared__ uint64_t mbar[2][2];    // [warpgroup][sweep MMAs done, core MMA done]
-  __shared__ uint32_t st_arrive[2];  // warps done with their S^T columns (monotonic)
+  const int g = threadIdx.x >> 7;      // warpgroup
+  const int e = threadIdx.x & 127;     // tile row = TMEM lane
+  const int wk = w & 3;                // warp within the warpgroup
+  const int slot = wk & 1, turn = wk >> 1;
+  uint8_t* wgb = smb + L::G_BYTES + g * L::WG_BYTES;
+  uint8_t* myslot = wgb + slot * L::SLOT;
+  uint8_t* tU2h = wgb + 2 * L::SLOT;
+  uint8_t* tU2l = tU2h + L::U_TILE;
+  uint8_t* tU3h = tU2l + L::U_TILE;
+  uint8_t* tU3l = tU3h + L::U_TILE;
+  float* sU1 = reinterpret_cast<float*>(tU3l + L::U_TILE);
+  __shared__ uint64_t mbar[2][3];      // [warpgroup][sweep MMAs, slot 0 MMA, slot 1 MMA]
   __shared__ uint32_t tmem_base;
 
-  auto gc_off = [](int ab, int c) { return (c >> 2) * L::G_KS + ab * 16 + (c & 3) * 4; };
+  // core element (a,b,c) into the four fp16 copies
+  auto put_g = [&](int ab, int c, float v) {
+    __half h, l;
+    split_h(v * kSG, h, l);
+    const int ia = ab / J, ib = ab - (ab / J) * J;
+    const int oc = (ab >> 3) * 128 + (ab & 7) * 16 + (c >> 3) * L::G_LBO + (c & 7) * 2;
+    const int rb = ia * J + c;
+    const int ob = (rb >> 3) * 128 + (rb & 7) * 16 + (ib >> 3) * L::G_LBO + (ib & 7) * 2;
+    *reinterpret_cast<__half*>(Gch + oc) = h;
+    *reinterpret_cast<__half*>(Gcl + oc) = l;
+    *reinterpret_cast<__half*>(Gbh + ob) = h;
+    *reinterpret_cast<__half*>(Gbl + ob) = l;
+  };
+  auto get_g = [&](int ab, int c) {
+    const int oc = (ab >> 3) * 128 + (ab & 7) * 16 + (c >> 3) * L::G_LBO + (c & 7) * 2;
+    return (__half2float(*reinterpret_cast<const __half*>(Gch + oc)) +
+            __half2float(*reinterpret_cast<const __half*>(Gcl + oc))) * (1.f / kSG);
+  };
 
   // ---- prologue: zero the operand tiles, core copies, TMEM, hot replicas ----
   for (int q = threadIdx.x; q < L::FIXED_FLOATS; q += blockDim.x) sm[q] = 0.f;
   __syncthreads();
-  for (int q = threadIdx.x; q < AB * J; q += blockDim.x) {
-    const int ab = q / J, c = q - (q / J) * J, ia = ab / J, ib = ab - (ab / J) * J;
-    const float v = __ldcg(a.G + q);
-    *reinterpret_cast<float*>(Gc + gc_off(ab, c)) = v;
-    *reinterpret_cast<float*>(Gb + gc_off(ia * J + c, ib)) = v;
-  }
+  for (int q = threadIdx.x; q < AB * J; q += blockDim.x) put_g(q / J, q % J, __ldcg(a.G + q));
   if (threadIdx.x == 0) {
-    umma::mbar_init(&mbar[0][0], 1);
-    umma::mbar_init(&mbar[0][1], 1);
-    umma::mbar_init(&mbar[1][0], 1);
-    umma::mbar_init(&mbar[1][1], 1);
-    st_arrive[0] = st_arrive[1] = 0u;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) umma::mbar_init(&mbar[k / 3][k % 3], 1);
     umma::fence_mbar_init();
   }
   if (w == 0) umma::tmem_alloc<512>(&tmem_base);
@@ -230,13 +284,16 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = tmem_base + (uint32_t)(g * 256);
-  const uint32_t tm_lane = (uint32_t)(32 * (w & 3)) << 16;
-  const uint32_t sPT = umma::smem_u32(PT), sST = umma::smem_u32(ST);
-  const uint32_t sU2 = umma::smem_u32(tU2), sU3 = umma::smem_u32(tU3);
-  const uint32_t sGc = umma::smem_u32(Gc), sGb = umma::smem_u32(Gb);
-  constexpr uint32_t ID_SWEEP = umma::idesc_tf32(128, NT, false, false);
-  constexpr uint32_t ID_CORE = umma::idesc_f16(128, L::KC);
-  constexpr float kSScale = 256.f;  // S^T = -r u3 * 2^8 in fp16
+  const uint32_t tm_lane = (uint32_t)(32 * wk) << 16;
+  const uint32_t sU2h = umma::smem_u32(tU2h), sU2l = umma::smem_u32(tU2l);
+  const uint32_t sU3h = umma::smem_u32(tU3h), sU3l = umma::smem_u32(tU3l);
+  const uint32_t sGch = umma::smem_u32(Gch), sGcl = umma::smem_u32(Gcl);
+  const uint32_t sGbh = umma::smem_u32(Gbh), sGbl = umma::smem_u32(Gbl);
+  const uint32_t sPh = umma::smem_u32(myslot), sPl = sPh + L::P_BYTES;
+  const uint32_t sSh = sPl + L::P_BYTES, sSl = sSh + L::S_BYTES;
+  constexpr uint32_t ID_SWEEP = umma::idesc_f16(128, NT);
+  constexpr uint32_t ID_CORE = umma::idesc_f16(128, 16, true, true);
+  constexpr float kInvT = 1.f / (kSU * kSG), kInvD = 1.f / (kSP * kSS);
   constexpr uint32_t kRefresh = CMTF_TM_REFRESH;
 
   const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
@@ -260,13 +317,18 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     rep[n] = sm + a.hot[n].off;
     stat[n] = sm + a.hot[n].stat_off;
   }
-  // core row (a,b) = e of this thread in the two shared core copies
-  const int ia_e = e / J, ib_e = e - (e / J) * J;
-  const int gb_row = (ib_e >> 2) * L::G_KS + (ib_e & 3) * 4;
   uint32_t npush = 0;
   float* myU1 = sU1 + e * JP;
-  uint8_t* myU2 = tU2 + e * 16;  // chunk k4 at + k4 * U_KS
-  uint8_t* myU3 = tU3 + e * 16;
+  // this thread's row in the sweep tiles: K group k at + k * U_LBO
+  uint8_t* myU2h = tU2h + e * 16;
+  uint8_t* myU2l = tU2l + e * 16;
+  uint8_t* myU3h = tU3h + e * 16;
+  uint8_t* myU3l = tU3l + e * 16;
+  // fp32 landing place of gathered row chunk q (4 floats): hi K group 0,
+  // hi K group 1, lo K group 0 -- rewritten as fp16 hi/lo before the MMA
+  auto land = [&](uint8_t* th, uint8_t* tl, int q) -> float* {
+    return reinterpret_cast<float*>(q == 0 ? th : q == 1 ? th + L::U_LBO : tl);
+  };
 
   // records two ahead, slots and coefficients one ahead; the next entry's
   // cold rows are copied (cp.async) straight into the operand tiles once the
@@ -281,17 +343,28 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       if (slx[1] < 0) {
         const float* src = a.U[1] + (uint64_t)r.y * JP;
 #pragma unroll
-        for (int k = 0; k < JP; k += 4)
-          cp_async16(reinterpret_cast<float*>(myU2 + (k >> 2) * L::U_KS), src + k);
+        for (int k = 0; k < JP; k += 4) cp_async16(land(myU2h, myU2l, k >> 2), src + k);
       }
       if (slx[2] < 0) {
         const float* src = a.U[2] + (uint64_t)r.z * JP;
 #pragma unroll
-        for (int k = 0; k < JP; k += 4)
-          cp_async16(reinterpret_cast<float*>(myU3 + (k >> 2) * L::U_KS), src + k);
+        for (int k = 0; k < JP; k += 4) cp_async16(land(myU3h, myU3l, k >> 2), src + k);
       }
     }
     cp_async_commit();
+  };
+  // a row (JP floats, zero padded to K = 16) as fp16 hi/lo into this thread's tile rows
+  auto put_row = [&](uint8_t* th, uint8_t* tl, const float* u) {
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = k < J ? u[k] : 0.f;
+    uint4 h0, l0, h1, l1;
+    split8(v, kSU, h0, l0);
+    split8(v + 8, kSU, h1, l1);
+    *reinterpret_cast<uint4*>(th) = h0;
+    *reinterpret_cast<uint4*>(th + L::U_LBO) = h1;
+    *reinterpret_cast<uint4*>(tl) = l0;
+    *reinterpret_cast<uint4*>(tl + L::U_LBO) = l1;
   };
   uint4 rc = lo < hi ? __ldg(a.rec + lo) : make_uint4(0, 0, 0, 0);
   uint4 rc1 = lo + 1 < hi ? __ldg(a.rec + lo + 1) : make_uint4(0, 0, 0, 0);
@@ -306,7 +379,6 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
   }
   issue_rows(rc, sl, lo < hi);
-  cp_async_commit();  // (empty) core-refresh group
 
 #if CMTF_TM_PROF
   long long tprof[14] = {0};
@@ -332,33 +404,19 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       }
     }
 
-    // ---- this entry's rows (cold ones landed in the tiles) ----
-    cp_async_wait_group<1>();
+    // ---- this entry's rows (cold ones landed in the tiles) -> fp16 hi/lo ----
+    cp_async_wait_group<0>();
     float u1[JP], u2[JP], u3[JP];
     if (active) {
       const float* s1 = sl[0] >= 0 ? rep[0] + sl[0] * JP : myU1;
 #pragma unroll
       for (int k = 0; k < JP; k += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(s1 + k);
-        u1[k] = q.x; u1[k + 1] = q.y; u1[k + 2] = q.z; u1[k + 3] = q.w;
-      }
-#pragma unroll
-      for (int k = 0; k < JP; k += 4) {
-        float4* d2 = reinterpret_cast<float4*>(myU2 + (k >> 2) * L::U_KS);
-        float4* d3 = reinterpret_cast<float4*>(myU3 + (k >> 2) * L::U_KS);
-        float4 q2, q3;
-        if (sl[1] >= 0) {
-          q2 = *reinterpret_cast<const float4*>(rep[1] + sl[1] * JP + k);
-          *d2 = q2;
-        } else {
-          q2 = *d2;
-        }
-        if (sl[2] >= 0) {
-          q3 = *reinterpret_cast<const float4*>(rep[2] + sl[2] * JP + k);
-          *d3 = q3;
-        } else {
-          q3 = *d3;
-        }
+        const float4 q1 = *reinterpret_cast<const float4*>(s1 + k);
+        const float4 q2 = sl[1] >= 0 ? *reinterpret_cast<const float4*>(rep[1] + sl[1] * JP + k)
+                                     : *reinterpret_cast<const float4*>(land(myU2h, myU2l, k >> 2));
+        const float4 q3 = sl[2] >= 0 ? *reinterpret_cast<const float4*>(rep[2] + sl[2] * JP + k)
+                                     : *reinterpret_cast<const float4*>(land(myU3h, myU3l, k >> 2));
+        u1[k] = q1.x; u1[k + 1] = q1.y; u1[k + 2] = q1.z; u1[k + 3] = q1.w;
         u2[k] = q2.x; u2[k + 1] = q2.y; u2[k + 2] = q2.z; u2[k + 3] = q2.w;
         u3[k] = q3.x; u3[k + 1] = q3.y; u3[k + 2] = q3.z; u3[k + 3] = q3.w;
       }
@@ -366,31 +424,24 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #pragma unroll
       for (int k = 0; k < JP; ++k) u1[k] = u2[k] = u3[k] = 0.f;
     }
-
-    // ---- P^T column (the previous tile's core MMA must be done with it) ----
-    if (it > 0) umma::mbar_wait(&mbar[g][1], par ^ 1u);
-    {
-      uint8_t* pcol = PT + (e >> 3) * L::PT_KS + (e & 7) * 2;
-#pragma unroll
-      for (int ia = 0; ia < J; ++ia)
-#pragma unroll
-        for (int ib = 0; ib < J; ++ib)
-          *reinterpret_cast<__half*>(pcol + (ia * J + ib) * 16) = __float2half_rn(u1[ia] * u2[ib]);
-    }
+    put_row(myU2h, myU2l, u2);
+    put_row(myU3h, myU3l, u3);
     umma::fence_async_smem();
+    umma::fence_before();
     TMP(0);
-    // a hardware barrier here (the last-warp-issues scheme used for the core
-    // MMA measured 2% slower: the early warps then spin on the mbarrier)
     umma::bar_sync(1 + g, 128);
     if (e == 0) {
       umma::fence_after();
-#pragma unroll
-      for (int ks = 0; ks < KT / 8; ++ks) {
-        umma::mma_tf32(tm, umma::desc(sU3 + ks * 2 * L::U_KS, L::U_KS, 128),
-                       umma::desc(sGc + ks * 2 * L::G_KS, L::G_KS, 128), ID_SWEEP, ks > 0);
-        umma::mma_tf32(tm + NT, umma::desc(sU2 + ks * 2 * L::U_KS, L::U_KS, 128),
-                       umma::desc(sGb + ks * 2 * L::G_KS, L::G_KS, 128), ID_SWEEP, ks > 0);
-      }
+      const uint64_t dU3h = umma::desc(sU3h, L::U_LBO, 128), dU3l = umma::desc(sU3l, L::U_LBO, 128);
+      const uint64_t dU2h = umma::desc(sU2h, L::U_LBO, 128), dU2l = umma::desc(sU2l, L::U_LBO, 128);
+      const uint64_t dGch = umma::desc(sGch, L::G_LBO, 128), dGcl = umma::desc(sGcl, L::G_LBO, 128);
+      const uint64_t dGbh = umma::desc(sGbh, L::G_LBO, 128), dGbl = umma::desc(sGbl, L::G_LBO, 128);
+      umma::mma_f16(tm, dU3h, dGch, ID_SWEEP, 0u);
+      umma::mma_f16(tm, dU3h, dGcl, ID_SWEEP, 1u);
+      umma::mma_f16(tm, dU3l, dGch, ID_SWEEP, 1u);
+      umma::mma_f16(tm + NT, dU2h, dGbh, ID_SWEEP, 0u);
+      umma::mma_f16(tm + NT, dU2h, dGbl, ID_SWEEP, 1u);
+      umma::mma_f16(tm + NT, dU2l, dGbh, ID_SWEEP, 1u);
       umma::commit(&mbar[g][0]);
     }
 
@@ -414,8 +465,9 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         const int col = c0 + q;
         if (col < AB) {
           const int ia = col / J, ib = col % J;
-          w1[ia] = fmaf(v[q], u2[ib], w1[ia]);
-          g2[ib] = fmaf(v[q], u1[ia], g2[ib]);
+          const float t = v[q] * kInvT;
+          w1[ia] = fmaf(t, u2[ib], w1[ia]);
+          g2[ib] = fmaf(t, u1[ia], g2[ib]);
         }
       }
     }
@@ -431,29 +483,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         const int col = c0 + q;
         if (col < AB) {
           const int ia = col / J, ic = col % J;
-          g3[ic] = fmaf(v[q], u1[ia], g3[ic]);
+          g3[ic] = fmaf(v[q] * kInvT, u1[ia], g3[ic]);
         }
       }
     }
-#if CMTF_TM_EXACT  // diagnostics: the contractions in FP32 from the shared core copy
-#pragma unroll
-    for (int k = 0; k < J; ++k) w1[k] = g2[k] = g3[k] = 0.f;
-#pragma unroll 1
-    for (int ia = 0; ia < J; ++ia)
-#pragma unroll
-      for (int ib = 0; ib < J; ++ib) {
-        float tab = 0.f;
-        const float p = u1[ia] * u2[ib];
-#pragma unroll
-        for (int c = 0; c < J; ++c) {
-          const float gv = *reinterpret_cast<const float*>(Gc + gc_off(ia * J + ib, c));
-          tab = fmaf(gv, u3[c], tab);
-          g3[c] = fmaf(gv, p, g3[c]);
-        }
-        w1[ia] = fmaf(tab, u2[ib], w1[ia]);
-        g2[ib] = fmaf(tab, u1[ia], g2[ib]);
-      }
-#endif
     float xh = 0.f;
 #pragma unroll
     for (int k = 0; k < J; ++k) xh = fmaf(w1[k], u1[k], xh);
@@ -461,6 +494,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     TMP(3);
     // ---- residual, row steps ----
     const float r = active ? __uint_as_float(rc.w) - xh : 0.f;
+    float* pr = a.probe && active ? a.probe + e0 * (uint64_t)(2 + 3 * J) : nullptr;
+    if (pr) {
+      pr[0] = xh;
+      pr[1] = r;
+    }
     {
       float n1 = 0.f, n2 = 0.f, n3 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
 #pragma unroll
@@ -475,14 +513,23 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       float gr[J];
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, w1[k], rg[0] * u1[k]);
+      if (pr)
+#pragma unroll
+        for (int k = 0; k < J; ++k) pr[2 + k] = gr[k];
       step_row_warp<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0],
                            (int)a.hot[0].off, active, u1, gr, a.eta, a.nonneg, c1, lane);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], rg[1] * u2[k]);
+      if (pr)
+#pragma unroll
+        for (int k = 0; k < J; ++k) pr[2 + J + k] = gr[k];
       step_row_warp<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1],
                            (int)a.hot[1].off, active, u2, gr, a.eta, a.nonneg, c2, lane);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], rg[2] * u3[k]);
+      if (pr)
+#pragma unroll
+        for (int k = 0; k < J; ++k) pr[2 + 2 * J + k] = gr[k];
       step_row_warp<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2],
                            (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
     }
@@ -500,34 +547,62 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       lamG = 0.f;
     }
 
-    // ---- S^T column (-r u3 at pre-update values), core-gradient MMA ----
+    // ---- core gradient: this warp's P and S rows (pre-update values) into
+    // its slot, then one warp-issued MMA (K = 32 entries) into the slot's
+    // accumulator.  Slot completions per iteration: turn 0 (#2it), turn 1 (#2it+1) ----
+    if (turn == 0) {
+      if (it > 0) umma::mbar_wait(&mbar[g][1 + slot], 1u);
+    } else {
+      umma::mbar_wait(&mbar[g][1 + slot], 0u);
+    }
     {
-      uint8_t* scol = ST + (e >> 3) * L::ST_KS + (e & 7) * 2;
+      uint8_t* Ph = myslot + lane * 16;
 #pragma unroll
-      for (int c = 0; c < J; ++c)
-        *reinterpret_cast<__half*>(scol + c * 16) =
-            __float2half_rn(fminf(fmaxf(-r * kSScale * u3[c], -65504.f), 65504.f));
+      for (int j = 0; j < NCH; ++j) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int ab = 8 * j + q;
+          v[q] = ab < AB ? u1[ab / J] * u2[ab % J] : 0.f;
+        }
+        uint4 h, l;
+        split8(v, kSP, h, l);
+        *reinterpret_cast<uint4*>(Ph + j * L::P_SBO) = h;
+        *reinterpret_cast<uint4*>(Ph + L::P_BYTES + j * L::P_SBO) = l;
+      }
+      uint8_t* Sh = myslot + 2 * L::P_BYTES + lane * 16;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = 8 * j + q;
+          v[q] = c < J ? -r * u3[c] : 0.f;
+        }
+        uint4 h, l;
+        split8(v, kSS, h, l);
+        *reinterpret_cast<uint4*>(Sh + j * L::P_SBO) = h;
+        *reinterpret_cast<uint4*>(Sh + L::S_BYTES + j * L::P_SBO) = l;
+      }
     }
     umma::fence_async_smem();
-    umma::fence_before();
-    // no barrier: the last of the warpgroup's 4 warps to finish its S^T
-    // columns issues the core MMA; nobody waits
     __syncwarp();
-    bool issue_core = false;
     if (lane == 0) {
-      __threadfence_block();
-      issue_core = (atomicAdd(&st_arrive[g], 1u) & 3u) == 3u;
-      __threadfence_block();
-    }
-    if (issue_core) {
       umma::fence_after();
-      const uint32_t acc0 = (it % (uint64_t)a.core_every) != 0 ? 1u : 0u;
+      const uint32_t d = tm + 2 * NT + 16 * slot;
+      const uint32_t acc0 = (turn == 1 || (it % (uint64_t)a.core_every) != 0) ? 1u : 0u;
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        umma::mma_f16(tm + 2 * NT, umma::desc(sPT + ks * 2 * L::PT_KS, L::PT_KS, 128),
-                      umma::desc(sST + ks * 2 * L::ST_KS, L::ST_KS, 128), ID_CORE,
-                      ks > 0 ? 1u : acc0);
-      umma::commit(&mbar[g][1]);
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t ko = ks * 2 * L::P_LBO;
+        const uint64_t dPh = umma::desc(sPh + ko, L::P_LBO, L::P_SBO);
+        const uint64_t dPl = umma::desc(sPl + ko, L::P_LBO, L::P_SBO);
+        const uint64_t dSh = umma::desc(sSh + ko, L::P_LBO, L::P_SBO);
+        const uint64_t dSl = umma::desc(sSl + ko, L::P_LBO, L::P_SBO);
+        umma::mma_f16(d, dPh, dSh, ID_CORE, ks > 0 ? 1u : acc0);
+        umma::mma_f16(d, dPh, dSl, ID_CORE, 1u);
+        umma::mma_f16(d, dPl, dSh, ID_CORE, 1u);
+      }
+      umma::commit(&mbar[g][1 + slot]);
     }
 
     TMP(5);
@@ -554,21 +629,29 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
 
     TMP(8);
+    const bool flush = (it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters;
+    if (push || flush) {
+      // every core MMA of this iteration is done with its slot (the slots are
+      // free until the next barrier: push scratch and merge staging)
+      umma::mbar_wait(&mbar[g][1], 1u);
+      umma::mbar_wait(&mbar[g][2], 1u);
+    }
     // ---- periodic core push / refresh (per warpgroup, no block barrier).
-    // TMEM lane e holds core row (a,b) = e; each warp transposes its 32 rows
-    // through its slice of the S^T buffer (free until the next barrier) so the
-    // REDs to the global core are coalesced ----
+    // TMEM lane e holds core row (a,b) = e of both slot accumulators; each
+    // warp transposes its 32 rows through its part of a slot so the REDs to
+    // the global core are coalesced ----
     if (push) {
-      umma::mbar_wait(&mbar[g][1], par);
       TMP(11);
       umma::fence_after();
-      float v[16];
-      umma::ld16(tm + tm_lane + 2 * NT, v);
+      float v0[16], v1[16];
+      umma::ld16(tm + tm_lane + 2 * NT, v0);
+      umma::ld16(tm + tm_lane + 2 * NT + 16, v1);
       umma::ld_wait();
-      umma::ld_fence_regs<16>(v);
+      umma::ld_fence_regs<16>(v0);
+      umma::ld_fence_regs<16>(v1);
       TMP(12);
-      float* scr = reinterpret_cast<float*>(ST + (w & 3) * 4 * L::ST_KS);  // own slab
-      const int row0 = 32 * (w & 3);
+      float* scr = reinterpret_cast<float*>(myslot + turn * L::HALF);
+      const int row0 = 32 * wk;
       if (kb > 0.f && row0 < AB) {
         const float q = a.eta * (lb / kb) * a.nhat_core;
         const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
@@ -576,26 +659,24 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         const float creg = kb * a.core_reg;
         float* Grow = a.G + e * J;
         // the shared copies follow the global core every kRefresh pushes
-        // (and right away in nonnegative mode)
+        // (and right away in nonnegative mode); the refresh read is issued
+        // before this push's REDs and gets this push's own delta added
         const bool refresh = ++npush % kRefresh == 0;
         if (e < AB) {
-          // row owner: the gradient of its row plus the regulariser, and the
-          // refresh of its row in both shared copies
+          float gnew[J];
+          if (refresh && !a.nonneg)
+#pragma unroll
+            for (int c = 0; c < J; ++c) gnew[c] = __ldcg(Grow + c);
 #pragma unroll
           for (int c = 0; c < J; ++c) {
-            float* gc = reinterpret_cast<float*>(Gc + gc_off(e, c));
-            float* gb = reinterpret_cast<float*>(Gb + gb_row + (ia_e * J + c) * 16);
-            const float gr = fmaf(creg, *gc, v[c] * (1.f / kSScale));
+            const float dat = (v0[c] + v1[c]) * kInvD;
+            if (a.probe_core) atomicAdd(a.probe_core + e * J + c, dat);
+            const float gr = fmaf(creg, get_g(e, c), dat);
             if (a.nonneg) {
-              const float nv = atomic_add_clamp0(Grow + c, s * gr);
-              *gc = nv;
-              *gb = nv;
+              put_g(e, c, atomic_add_clamp0(Grow + c, s * gr));
             } else {
               scr[lane * J + c] = gr;
-              if (refresh) {
-                cp_async4(gc, Grow + c);
-                cp_async4(gb, Grow + c);
-              }
+              if (refresh) put_g(e, c, gnew[c] + s * gr);
             }
           }
         }
@@ -603,7 +684,6 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         if (!a.nonneg) {  // coalesced REDs of the warp's 32 rows
           const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
           float* Gw = a.G + row0 * J;
-          // vector REDs: 4 consecutive core elements per request
           for (int m4 = lane; m4 < nval / 4; m4 += 32) {
             const float4 d = *reinterpret_cast<const float4*>(scr + 4 * m4);
             red_add_v4(Gw + 4 * m4, make_float4(s * d.x, s * d.y, s * d.z, s * d.w));
@@ -611,17 +691,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
           for (int m = (nval & ~3) + lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
         }
       }
-      umma::fence_before();
+      __syncwarp();
     }
     TMP(9);
-    cp_async_commit();  // core refresh group (possibly empty)
-    if ((it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters) {
+    if (flush) {
       if (CMTF_TM_FSTAGE && L::FSTAGE) {
-        // staging: this warp's 4 column groups of its P^T buffer (only its
-        // own threads write them; the core MMA that read them is complete)
-        umma::mbar_wait(&mbar[g][1], par);
         flush_all_hot_staged<J, JP, NW>(
-            a, sm, w, lane, reinterpret_cast<float*>(PT + (w & 3) * 4 * L::PT_KS));
+            a, sm, w, lane, reinterpret_cast<float*>(myslot + turn * L::HALF));
       } else {
         flush_all_hot<J, JP, NW>(a, sm, w, lane);
       }
@@ -640,8 +716,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   if (w == 0) umma::tmem_free<512>(tmem_base);
 #if CMTF_TM_PROF
   if (blockIdx.x == 0 && (threadIdx.x & 127) == 0)
-    printf("prof wg%d iters %llu: wait+tiles+PT %lld | bar1+issue %lld | mma wait %lld | contract %lld | "
-           "rowsteps %lld | ST+bar2+issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld | push.mbar %lld | push.tmem %lld\n",
+    printf("prof wg%d iters %llu: wait+tiles %lld | bar1+issue %lld | mma wait %lld | contract %lld | "
+           "rowsteps %lld | P,S+core issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld | slot waits %lld | push.tmem %lld\n",
            g, (unsigned long long)iters, tprof[0], tprof[1], tprof[2], tprof[3], tprof[4], tprof[5],
            tprof[6], tprof[7], tprof[8], tprof[9], tprof[10], tprof[11], tprof[12]);
 #endif

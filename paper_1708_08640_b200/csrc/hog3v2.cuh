@@ -87,6 +87,10 @@ struct Hog3v2Args {
   int flush_every;  // iterations between hot-row flushes
   int core_every;   // iterations between core pushes
   int nonneg;
+  // kernel probe (hog3tm, eta = 0): per record {x_hat, r, grad u1[J], grad u2[J],
+  // grad u3[J]} and the summed data term of the core gradient (null: off)
+  float* probe;
+  float* probe_core;
 };
 
 // ---------------------------------------------------------------------

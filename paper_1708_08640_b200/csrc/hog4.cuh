@@ -48,6 +48,8 @@ struct Hog4Args {
   int flush_every;
   int core_every;
   int nonneg;
+  float* probe;       // unused (hog3tm only)
+  float* probe_core;
 };
 
 template <int J, int NW, bool TC = false>

@@ -40,9 +40,17 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool 
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// Instruction descriptor, kind::f16 with fp16 operands and an fp32 accumulator.
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
-  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor, kind::f16 with fp16 operands and an fp32
+// accumulator; a_mn / b_mn select MN-major operands (bits 15 / 16).  MN-major
+// no-swizzle layout (CUTLASS SWIZZLE_NONE convention, checked on the B200 by
+// scripts/micro/umma_prec.cu): a core matrix is 8 K-rows x 16 bytes of M (or
+// N); LBO = byte distance between K-adjacent core matrices, SBO = between
+// MN-adjacent ones.  K-major: a core matrix is 8 M-rows x 16 bytes of K; LBO
+// = K direction, SBO = M direction.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn = false,
+                                                 bool b_mn = false) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // D[tmem] (+)= A[smem] * B[smem] (fp16 operands, K = 16 per instruction).

@@ -571,3 +571,91 @@ def test_tcgen05_kernel_ranks_within_1pct_of_oracle(J):
     gpu_train = api.epoch_stats(st, 0.01).train_rmse
     assert abs(gpu_train - ref_train) <= 0.01 * ref_train, (gpu_train, ref_train)
     assert abs(gpu_test - ref_test) <= 0.01 * ref_test, (gpu_test, ref_test)
+
+
+# ----------------------------------------------------------------------
+# the product epoch kernel's own arithmetic (hog3tm, tcgen05 split-fp16)
+# ----------------------------------------------------------------------
+def _hog3tm_probe_check(st, bundle, ranks, lam, n_oracle=400, tol=1e-5):
+    """x_hat, r and the row gradients of every training entry, and the summed
+    core-gradient data term, as the epoch kernel computes them inside its
+    tensor-core tiles, against the f64 oracle at the same (fp32) model.
+    Bound: |got - ref| <= tol * (forward-error scale of the sum), i.e. the
+    sum of the absolute values of the terms (scale-aware 1e-5)."""
+    m = st.model
+    before = [m.core.copy()] + [f.copy() for f in m.factors]
+    xh, r, grow, gdat = api.kernel_probe(st)
+    after = st.model
+    assert np.array_equal(after.core, before[0])  # eta = 0: nothing moves
+    for n in range(3):
+        assert np.array_equal(after.factors[n], before[1 + n])
+    t = bundle.tensor
+    idx = np.asarray(t.indices, dtype=np.int64).reshape(-1, 3)
+    x = f32(t.values)
+    G, U = m.core, m.factors
+    aG = np.abs(G)
+    u = [U[n][idx[:, n]] for n in range(3)]
+    au = [np.abs(q) for q in u]
+    T = np.einsum("abc,ec->eab", G, u[2])
+    aT = np.einsum("abc,ec->eab", aG, au[2])
+    c1 = np.einsum("eab,eb->ea", T, u[1])
+    a1 = np.einsum("eab,eb->ea", aT, au[1])
+    c2 = np.einsum("eab,ea->eb", T, u[0])
+    a2 = np.einsum("eab,ea->eb", aT, au[0])
+    c3 = np.einsum("abc,ea,eb->ec", G, u[0], u[1])
+    a3 = np.einsum("abc,ea,eb->ec", aG, au[0], au[1])
+    xref = np.einsum("ea,ea->e", c1, u[0])
+    sabs = np.einsum("ea,ea->e", a1, au[0])
+    rref = x - xref
+    counts = O.count_modes(bundle, ranks)
+    offs = np.cumsum([0] + list(t.dims))
+    # x_hat and r: the sum's own scale
+    scale_close(xh, xref, sabs, tol)
+    scale_close(r, rref, sabs, tol)
+    J = ranks[0]
+    for n, (c, ac) in enumerate(((c1, a1), (c2, a2), (c3, a3))):
+        cnt = counts[offs[n] + idx[:, n]].astype(np.float64)
+        reg = np.float32(lam) / cnt.astype(np.float32)
+        gref = -rref[:, None] * c + reg.astype(np.float64)[:, None] * u[n]
+        # error of r propagates through c; error of c through r
+        sc = sabs[:, None] * np.abs(c) + np.abs(rref)[:, None] * ac + reg[:, None] * au[n]
+        scale_close(grow[:, n * J:(n + 1) * J], gref, sc, tol)
+    # the C oracle (compute_gradient_opt restated) on a sample of entries
+    rng = np.random.default_rng(1)
+    for e in rng.choice(len(x), size=min(n_oracle, len(x)), replace=False):
+        rows = [u[n][e] for n in range(3)]
+        cn = [counts[offs[n] + idx[e, n]] for n in range(3)]
+        g_o, _, r_o = O.compute_gradient(1, float(x[e]), G, rows, lam, cn, len(x), with_core=False)
+        sc = np.concatenate([sabs[e] * np.abs(c[e]) + abs(rref[e]) * ac[e] + lam / cn[k] * au[k][e]
+                             for k, (c, ac) in enumerate(((c1, a1), (c2, a2), (c3, a3)))])
+        scale_close([r[e]], [r_o], sabs[e], tol)
+        scale_close(grow[e], g_o, sc, tol)
+    # core gradient: sum_e -r_e u1 (x) u2 (x) u3 (the tile MMAs' accumulations)
+    D = np.einsum("e,ea,eb,ec->abc", -rref, u[0], u[1], u[2])
+    aD = np.einsum("e,ea,eb,ec->abc", np.abs(rref) + sabs, au[0], au[1], au[2])
+    scale_close(gdat, D, aD, tol)
+
+
+@pytest.mark.parametrize("J", [4, 5, 8, 10])
+def test_hog3tm_kernel_probe_matches_oracle(J):
+    """north_star: the per-entry prediction and gradient pass within 1e-5 --
+    checked on the product kernel itself (every training entry, at the initial
+    model and after 3 epochs), not on a separate probe kernel."""
+    b, _, _ = synth.generate(synth.config1(literal=False))
+    ranks = [J] * 3
+    st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
+    _hog3tm_probe_check(st, b, ranks, 0.01)
+    assert st.kernel_info()["kernel"] == "order3tm"
+    for _ in range(3):
+        api.run_epoch(st)
+    _hog3tm_probe_check(st, b, ranks, 0.01)
+
+
+def test_hog3tm_kernel_probe_config2_tile_shapes():
+    """Config-2 shape at 10% scale (Zipf heads in hot-row replicas, J = 10,
+    all 148 SMs, full 128-entry tiles): the kernel's arithmetic at 1e-5."""
+    b, _, _ = synth.generate(synth.config2(0.1))
+    ranks = [10, 10, 10]
+    st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
+    api.run_epoch(st)
+    _hog3tm_probe_check(st, b, ranks, 0.01, n_oracle=200)
