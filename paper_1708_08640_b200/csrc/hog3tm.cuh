@@ -65,11 +65,11 @@ namespace cmtfb {
 __host__ __device__ constexpr int round_up8(int x) { return (x + 7) & ~7; }
 __host__ __device__ constexpr int round_up16(int x) { return (x + 15) & ~15; }
 
-// Operand scales (powers of two, exact) keeping the fp16 splits in range:
-// |u| < 511 and |g| < 511 in the sweep, |u1 u2| < 255 and |r u3| < 255 in the
-// core gradient (beyond that the split clamps, which only a diverged model
-// reaches; the epoch's non-finite scan reports those).
-constexpr float kSU = 128.f, kSG = 128.f, kSP = 256.f, kSS = 256.f;
+// Operand scales (powers of two, exact) that keep the fp16 hi/lo parts of
+// ordinary values in the normal range; a value beyond 1023 overflows to inf
+// in fp16, which -- like a diverged model -- surfaces as a non-finite
+// parameter (DivergenceError) rather than as a silently clamped result.
+constexpr float kSU = 64.f, kSG = 64.f, kSP = 64.f, kSS = 64.f;
 
 template <int J>
 struct TMLayout {
@@ -91,10 +91,15 @@ struct TMLayout {
   static constexpr int S_BYTES = 2 * P_SBO;
   static constexpr int SLOT = 2 * P_BYTES + 2 * S_BYTES;  // P hi, P lo, S hi, S lo
   static constexpr int U1_BYTES = 128 * JP * 4;            // fp32 staging of u1
+  // the warpgroup's fp32 view of the core, row (a,b) = thread (a,b) (odd
+  // stride: conflict-free); the push's regulariser reads it and the refresh
+  // lands in it with cp.async before it is converted into the fp16 copies
+  static constexpr int JG = J | 1;
+  static constexpr int G32_BYTES = (AB * JG * 4 + 15) / 16 * 16;
   // per warpgroup: the two slots first (the M = 128 core MMA reads 16 (a,b)
   // chunks of P; those past NCH land in the following buffers and only feed
   // the ignored accumulator rows ab >= J^2)
-  static constexpr int WG_BYTES = 2 * SLOT + 4 * U_TILE + U1_BYTES;
+  static constexpr int WG_BYTES = 2 * SLOT + 4 * U_TILE + U1_BYTES + G32_BYTES;
   static constexpr int G_BYTES = 4 * G_TILE;  // G (ab x c) hi, lo; G (ac x b) hi, lo
   static constexpr int FIXED_BYTES = G_BYTES + 2 * WG_BYTES;
   static constexpr int FIXED_FLOATS = FIXED_BYTES / 4;
@@ -112,22 +117,23 @@ struct TMLayout {
   static constexpr bool FSTAGE = STAGE_WARP <= HALF;
 };
 
-// x -> hi + lo, two fp16 values (x already scaled; clamped to the fp16 range)
+// x -> hi + lo, two fp16 values (x already scaled): hi keeps x's top 11
+// significant bits (exactly an fp16 for |x| >= 2^-14), lo = x - hi is exact
+// in fp32 and rounded to fp16; hi + lo carries ~21 bits
 __device__ __forceinline__ void split_h(float x, __half& h, __half& l) {
-  x = fminf(fmaxf(x, -65504.f), 65504.f);
-  h = __float2half_rn(x);
-  l = __float2half_rn(x - __half2float(h));
+  const float hx = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  h = __float2half_rn(hx);
+  l = __float2half_rn(x - hx);
 }
-// 8 values * s -> one 16-byte chunk of hi halves and one of lo halves
-__device__ __forceinline__ void split8(const float* v, float s, uint4& hi, uint4& lo) {
+// 8 scaled values -> one 16-byte chunk of hi halves and one of lo halves
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float x0 = fminf(fmaxf(v[2 * q] * s, -65504.f), 65504.f);
-    const float x1 = fminf(fmaxf(v[2 * q + 1] * s, -65504.f), 65504.f);
-    const __half2 hh = __floats2half2_rn(x0, x1);
-    const float2 hf = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+    const float h0 = __uint_as_float(__float_as_uint(v[2 * q]) & 0xffffe000u);
+    const float h1 = __uint_as_float(__float_as_uint(v[2 * q + 1]) & 0xffffe000u);
+    const __half2 hh = __floats2half2_rn(h0, h1);
+    const __half2 ll = __floats2half2_rn(v[2 * q] - h0, v[2 * q + 1] - h1);
     h[q] = *reinterpret_cast<const uint32_t*>(&hh);
     l[q] = *reinterpret_cast<const uint32_t*>(&ll);
   }
@@ -240,6 +246,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   uint8_t* tU3h = tU2l + L::U_TILE;
   uint8_t* tU3l = tU3h + L::U_TILE;
   float* sU1 = reinterpret_cast<float*>(tU3l + L::U_TILE);
+  float* myG32 = reinterpret_cast<float*>(tU3l + L::U_TILE + L::U1_BYTES) + e * L::JG;
   __shared__ uint64_t mbar[2][3];      // [warpgroup][sweep MMAs, slot 0 MMA, slot 1 MMA]
   __shared__ uint32_t tmem_base;
 
@@ -256,16 +263,15 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     *reinterpret_cast<__half*>(Gbh + ob) = h;
     *reinterpret_cast<__half*>(Gbl + ob) = l;
   };
-  auto get_g = [&](int ab, int c) {
-    const int oc = (ab >> 3) * 128 + (ab & 7) * 16 + (c >> 3) * L::G_LBO + (c & 7) * 2;
-    return (__half2float(*reinterpret_cast<const __half*>(Gch + oc)) +
-            __half2float(*reinterpret_cast<const __half*>(Gcl + oc))) * (1.f / kSG);
-  };
 
   // ---- prologue: zero the operand tiles, core copies, TMEM, hot replicas ----
   for (int q = threadIdx.x; q < L::FIXED_FLOATS; q += blockDim.x) sm[q] = 0.f;
   __syncthreads();
   for (int q = threadIdx.x; q < AB * J; q += blockDim.x) put_g(q / J, q % J, __ldcg(a.G + q));
+  if (e < AB)
+#pragma unroll
+    for (int c = 0; c < J; ++c) myG32[c] = __ldcg(a.G + e * J + c);
+  bool g32_fresh = false;  // a refresh landed in myG32: convert it
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) umma::mbar_init(&mbar[k / 3][k % 3], 1);
@@ -357,10 +363,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   auto put_row = [&](uint8_t* th, uint8_t* tl, const float* u) {
     float v[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = k < J ? u[k] : 0.f;
+    for (int k = 0; k < 16; ++k) v[k] = k < J ? u[k] * kSU : 0.f;
     uint4 h0, l0, h1, l1;
-    split8(v, kSU, h0, l0);
-    split8(v + 8, kSU, h1, l1);
+    split8(v, h0, l0);
+    split8(v + 8, h1, l1);
     *reinterpret_cast<uint4*>(th) = h0;
     *reinterpret_cast<uint4*>(th + L::U_LBO) = h1;
     *reinterpret_cast<uint4*>(tl) = l0;
@@ -387,6 +393,88 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #else
 #define TMP(k) do {} while (0)
 #endif
+  // the previous iteration's core push and hot-row merges, run at the top of
+  // the next iteration (or after the last): every core MMA of that iteration
+  // is done first, so the slots are free (until this iteration's barrier) for
+  // the push transpose and the merge staging
+  bool pend_push = false, pend_flush = false;
+  float pkb = 0.f, plb = 0.f;
+  auto push_flush = [&]() {
+    umma::mbar_wait(&mbar[g][1], 1u);
+    umma::mbar_wait(&mbar[g][2], 1u);
+    TMP(10);
+    if (pend_push) {
+      // TMEM lane e holds core row (a,b) = e of both slot accumulators; each
+      // warp transposes its 32 rows through its half of a slot so the REDs to
+      // the global core are coalesced
+      umma::fence_after();
+      float v0[16], v1[16];
+      umma::ld16(tm + tm_lane + 2 * NT, v0);
+      umma::ld16(tm + tm_lane + 2 * NT + 16, v1);
+      umma::ld_wait();
+      umma::ld_fence_regs<16>(v0);
+      umma::ld_fence_regs<16>(v1);
+      TMP(11);
+      float* scr = reinterpret_cast<float*>(myslot + turn * L::HALF);
+      const int row0 = 32 * wk;
+      if (pkb > 0.f && row0 < AB) {
+        const float q = a.eta * (plb / pkb) * a.nhat_core;
+        const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
+        const float s = -a.eta * alpha;
+        const float creg = pkb * a.core_reg;
+        float* Grow = a.G + e * J;
+        // the shared copies follow the global core every kRefresh pushes
+        // (and right away in nonnegative mode); the refresh read is issued
+        // before this push's REDs and gets this push's own delta added
+        const bool refresh = ++npush % kRefresh == 0;
+        if (e < AB) {
+#pragma unroll
+          for (int c = 0; c < J; ++c) {
+            const float dat = (v0[c] + v1[c]) * kInvD;
+            if (a.probe_core) atomicAdd(a.probe_core + e * J + c, dat);
+            const float gr = fmaf(creg, myG32[c], dat);
+            if (a.nonneg) {
+              const float nv = atomic_add_clamp0(Grow + c, s * gr);
+              myG32[c] = nv;
+              put_g(e, c, nv);
+            } else {
+              scr[lane * J + c] = gr;
+            }
+          }
+        }
+        __syncwarp();
+        if (!a.nonneg) {  // coalesced REDs of the warp's 32 rows
+          const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
+          float* Gw = a.G + row0 * J;
+          for (int m4 = lane; m4 < nval / 4; m4 += 32) {
+            const float4 d = *reinterpret_cast<const float4*>(scr + 4 * m4);
+            red_add_v4(Gw + 4 * m4, make_float4(s * d.x, s * d.y, s * d.z, s * d.w));
+          }
+          for (int m = (nval & ~3) + lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
+          if (refresh && e < AB) {
+            // the global row (with this push) lands in the fp32 view; it is
+            // converted into the fp16 copies at the top of the next iteration
+#pragma unroll
+            for (int c = 0; c < J; ++c) cp_async4(myG32 + c, Grow + c);
+            g32_fresh = true;
+          }
+        }
+      }
+      __syncwarp();
+      TMP(12);
+    }
+    if (pend_flush) {
+      if (CMTF_TM_FSTAGE && L::FSTAGE) {
+        flush_all_hot_staged<J, JP, NW>(
+            a, sm, w, lane, reinterpret_cast<float*>(myslot + turn * L::HALF));
+      } else {
+        flush_all_hot<J, JP, NW>(a, sm, w, lane);
+      }
+    }
+    pend_push = pend_flush = false;
+    TMP(13);
+  };
+
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e0 = lo + it;
     const bool active = e0 < hi;
@@ -406,6 +494,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     // ---- this entry's rows (cold ones landed in the tiles) -> fp16 hi/lo ----
     cp_async_wait_group<0>();
+    if (g32_fresh) {
+#pragma unroll
+      for (int c = 0; c < J; ++c) put_g(e, c, myG32[c]);
+      g32_fresh = false;
+    }
     float u1[JP], u2[JP], u3[JP];
     if (active) {
       const float* s1 = sl[0] >= 0 ? rep[0] + sl[0] * JP : myU1;
@@ -426,9 +519,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
     put_row(myU2h, myU2l, u2);
     put_row(myU3h, myU3l, u3);
+    TMP(0);
+    if (pend_push || pend_flush) push_flush();
     umma::fence_async_smem();
     umma::fence_before();
-    TMP(0);
+    TMP(9);
     umma::bar_sync(1 + g, 128);
     if (e == 0) {
       umma::fence_after();
@@ -447,9 +542,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     TMP(1);
     // ---- contractions out of tensor memory (FP32) ----
-    float w1[J], g2[J], g3[J];
+    float w1[J], g2[J], g3[J], u1t[J], u2t[J];  // u * 2^-12 undoes the operand scales
 #pragma unroll
-    for (int k = 0; k < J; ++k) w1[k] = g2[k] = g3[k] = 0.f;
+    for (int k = 0; k < J; ++k) {
+      w1[k] = g2[k] = g3[k] = 0.f;
+      u1t[k] = u1[k] * kInvT;
+      u2t[k] = u2[k] * kInvT;
+    }
     umma::mbar_wait(&mbar[g][0], par);
     TMP(2);
     umma::fence_after();
@@ -465,9 +564,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         const int col = c0 + q;
         if (col < AB) {
           const int ia = col / J, ib = col % J;
-          const float t = v[q] * kInvT;
-          w1[ia] = fmaf(t, u2[ib], w1[ia]);
-          g2[ib] = fmaf(t, u1[ia], g2[ib]);
+          w1[ia] = fmaf(v[q], u2t[ib], w1[ia]);
+          g2[ib] = fmaf(v[q], u1t[ia], g2[ib]);
         }
       }
     }
@@ -483,7 +581,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         const int col = c0 + q;
         if (col < AB) {
           const int ia = col / J, ic = col % J;
-          g3[ic] = fmaf(v[q] * kInvT, u1[ia], g3[ic]);
+          g3[ic] = fmaf(v[q], u1t[ia], g3[ic]);
         }
       }
     }
@@ -535,27 +633,33 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     }
 
     TMP(4);
-    // push statistics of this warpgroup; they cross the barrier below
-    // (per warp: the warpgroup's count and curvature sum are taken as 4x the
-    // warp's -- the damping only needs their ratio, the regulariser the count)
-    const bool push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
-    float kb = 0.f, lb = 0.f;
-    if (push) {
-      kb = 4.f * warp_sum(kw);
-      lb = 4.f * warp_sum(lamG);
+    // push statistics of this warpgroup (per warp: the warpgroup's count and
+    // curvature sum are taken as 4x the warp's -- the damping only needs
+    // their ratio, the regulariser the count); the push itself runs at the
+    // top of the next iteration
+    pend_push = (it + 1) % (uint64_t)a.core_every == 0 || it + 1 == iters;
+    pend_flush = (it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters;
+    if (pend_push) {
+      pkb = 4.f * warp_sum(kw);
+      plb = 4.f * warp_sum(lamG);
       kw = 0.f;
       lamG = 0.f;
     }
 
     // ---- core gradient: this warp's P and S rows (pre-update values) into
     // its slot, then one warp-issued MMA (K = 32 entries) into the slot's
-    // accumulator.  Slot completions per iteration: turn 0 (#2it), turn 1 (#2it+1) ----
-    if (turn == 0) {
-      if (it > 0) umma::mbar_wait(&mbar[g][1 + slot], 1u);
-    } else {
-      umma::mbar_wait(&mbar[g][1 + slot], 0u);
-    }
-    {
+    // accumulator.  Slot completions per iteration: turn 0 (#2it), turn 1
+    // (#2it+1).  Turn-0 warps do it right away; turn-1 warps first issue their
+    // row gathers and matrix entries, so the turn-0 MMA is long done ----
+    auto core_phase = [&]() {
+      if (turn == 0) {
+        if (it > 0) umma::mbar_wait(&mbar[g][1 + slot], 1u);
+      } else {
+        umma::mbar_wait(&mbar[g][1 + slot], 0u);
+      }
+      float u1s[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) u1s[k] = u1[k] * kSP;
       uint8_t* Ph = myslot + lane * 16;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
@@ -563,47 +667,49 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int ab = 8 * j + q;
-          v[q] = ab < AB ? u1[ab / J] * u2[ab % J] : 0.f;
+          v[q] = ab < AB ? u1s[ab / J] * u2[ab % J] : 0.f;
         }
         uint4 h, l;
-        split8(v, kSP, h, l);
+        split8(v, h, l);
         *reinterpret_cast<uint4*>(Ph + j * L::P_SBO) = h;
         *reinterpret_cast<uint4*>(Ph + L::P_BYTES + j * L::P_SBO) = l;
       }
       uint8_t* Sh = myslot + 2 * L::P_BYTES + lane * 16;
+      const float rs = -r * kSS;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         float v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int c = 8 * j + q;
-          v[q] = c < J ? -r * u3[c] : 0.f;
+          v[q] = c < J ? rs * u3[c] : 0.f;
         }
         uint4 h, l;
-        split8(v, kSS, h, l);
+        split8(v, h, l);
         *reinterpret_cast<uint4*>(Sh + j * L::P_SBO) = h;
         *reinterpret_cast<uint4*>(Sh + L::S_BYTES + j * L::P_SBO) = l;
       }
-    }
-    umma::fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      umma::fence_after();
-      const uint32_t d = tm + 2 * NT + 16 * slot;
-      const uint32_t acc0 = (turn == 1 || (it % (uint64_t)a.core_every) != 0) ? 1u : 0u;
+      umma::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        umma::fence_after();
+        const uint32_t d = tm + 2 * NT + 16 * slot;
+        const uint32_t acc0 = (turn == 1 || (it % (uint64_t)a.core_every) != 0) ? 1u : 0u;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint32_t ko = ks * 2 * L::P_LBO;
-        const uint64_t dPh = umma::desc(sPh + ko, L::P_LBO, L::P_SBO);
-        const uint64_t dPl = umma::desc(sPl + ko, L::P_LBO, L::P_SBO);
-        const uint64_t dSh = umma::desc(sSh + ko, L::P_LBO, L::P_SBO);
-        const uint64_t dSl = umma::desc(sSl + ko, L::P_LBO, L::P_SBO);
-        umma::mma_f16(d, dPh, dSh, ID_CORE, ks > 0 ? 1u : acc0);
-        umma::mma_f16(d, dPh, dSl, ID_CORE, 1u);
-        umma::mma_f16(d, dPl, dSh, ID_CORE, 1u);
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ko = ks * 2 * L::P_LBO;
+          const uint64_t dPh = umma::desc(sPh + ko, L::P_LBO, L::P_SBO);
+          const uint64_t dPl = umma::desc(sPl + ko, L::P_LBO, L::P_SBO);
+          const uint64_t dSh = umma::desc(sSh + ko, L::P_LBO, L::P_SBO);
+          const uint64_t dSl = umma::desc(sSl + ko, L::P_LBO, L::P_SBO);
+          umma::mma_f16(d, dPh, dSh, ID_CORE, ks > 0 ? 1u : acc0);
+          umma::mma_f16(d, dPh, dSl, ID_CORE, 1u);
+          umma::mma_f16(d, dPl, dSh, ID_CORE, 1u);
+        }
+        umma::commit(&mbar[g][1 + slot]);
       }
-      umma::commit(&mbar[g][1 + slot]);
-    }
+    };
+    if (turn == 0) core_phase();
 
     TMP(5);
     // ---- next entry's rows into the tiles (the sweep MMAs are done) ----
@@ -618,8 +724,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
                                 lane);
 #endif
-
     TMP(7);
+    if (turn == 1) core_phase();
+
+    TMP(8);
     rc = rc1;
     rc1 = rc2;
 #pragma unroll
@@ -627,99 +735,27 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       sl[n] = nsl[n];
       rg[n] = nrg[n];
     }
-
-    TMP(8);
-    const bool flush = (it + 1) % (uint64_t)a.flush_every == 0 || it + 1 == iters;
-    if (push || flush) {
-      // every core MMA of this iteration is done with its slot (the slots are
-      // free until the next barrier: push scratch and merge staging)
-      umma::mbar_wait(&mbar[g][1], 1u);
-      umma::mbar_wait(&mbar[g][2], 1u);
-    }
-    // ---- periodic core push / refresh (per warpgroup, no block barrier).
-    // TMEM lane e holds core row (a,b) = e of both slot accumulators; each
-    // warp transposes its 32 rows through its part of a slot so the REDs to
-    // the global core are coalesced ----
-    if (push) {
-      TMP(11);
-      umma::fence_after();
-      float v0[16], v1[16];
-      umma::ld16(tm + tm_lane + 2 * NT, v0);
-      umma::ld16(tm + tm_lane + 2 * NT + 16, v1);
-      umma::ld_wait();
-      umma::ld_fence_regs<16>(v0);
-      umma::ld_fence_regs<16>(v1);
-      TMP(12);
-      float* scr = reinterpret_cast<float*>(myslot + turn * L::HALF);
-      const int row0 = 32 * wk;
-      if (kb > 0.f && row0 < AB) {
-        const float q = a.eta * (lb / kb) * a.nhat_core;
-        const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
-        const float s = -a.eta * alpha;
-        const float creg = kb * a.core_reg;
-        float* Grow = a.G + e * J;
-        // the shared copies follow the global core every kRefresh pushes
-        // (and right away in nonnegative mode); the refresh read is issued
-        // before this push's REDs and gets this push's own delta added
-        const bool refresh = ++npush % kRefresh == 0;
-        if (e < AB) {
-          float gnew[J];
-          if (refresh && !a.nonneg)
-#pragma unroll
-            for (int c = 0; c < J; ++c) gnew[c] = __ldcg(Grow + c);
-#pragma unroll
-          for (int c = 0; c < J; ++c) {
-            const float dat = (v0[c] + v1[c]) * kInvD;
-            if (a.probe_core) atomicAdd(a.probe_core + e * J + c, dat);
-            const float gr = fmaf(creg, get_g(e, c), dat);
-            if (a.nonneg) {
-              put_g(e, c, atomic_add_clamp0(Grow + c, s * gr));
-            } else {
-              scr[lane * J + c] = gr;
-              if (refresh) put_g(e, c, gnew[c] + s * gr);
-            }
-          }
-        }
-        __syncwarp();
-        if (!a.nonneg) {  // coalesced REDs of the warp's 32 rows
-          const int nval = (AB - row0 < 32 ? AB - row0 : 32) * J;
-          float* Gw = a.G + row0 * J;
-          for (int m4 = lane; m4 < nval / 4; m4 += 32) {
-            const float4 d = *reinterpret_cast<const float4*>(scr + 4 * m4);
-            red_add_v4(Gw + 4 * m4, make_float4(s * d.x, s * d.y, s * d.z, s * d.w));
-          }
-          for (int m = (nval & ~3) + lane; m < nval; m += 32) red_add_f32(Gw + m, s * scr[m]);
-        }
-      }
-      __syncwarp();
-    }
-    TMP(9);
-    if (flush) {
-      if (CMTF_TM_FSTAGE && L::FSTAGE) {
-        flush_all_hot_staged<J, JP, NW>(
-            a, sm, w, lane, reinterpret_cast<float*>(myslot + turn * L::HALF));
-      } else {
-        flush_all_hot<J, JP, NW>(a, sm, w, lane);
-      }
-    }
-    TMP(10);
   }
 #if CMTF_TM_MPF
   matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mhi, mhi, lane);
 #else
   matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
 #endif
+  if (pend_push || pend_flush) push_flush();
   cp_async_wait_all();
   umma::fence_before();
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);
   if (w == 0) umma::tmem_free<512>(tmem_base);
 #if CMTF_TM_PROF
-  if (blockIdx.x == 0 && (threadIdx.x & 127) == 0)
-    printf("prof wg%d iters %llu: wait+tiles %lld | bar1+issue %lld | mma wait %lld | contract %lld | "
-           "rowsteps %lld | P,S+core issue %lld | issue_rows %lld | matrix %lld | misc %lld | push %lld | flush %lld | slot waits %lld | push.tmem %lld\n",
-           g, (unsigned long long)iters, tprof[0], tprof[1], tprof[2], tprof[3], tprof[4], tprof[5],
-           tprof[6], tprof[7], tprof[8], tprof[9], tprof[10], tprof[11], tprof[12]);
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+    printf("prof wg%d w%d iters %llu: wait+tiles %lld | push+flush %lld | bar+issue %lld | mma wait %lld | "
+           "contract %lld | rowsteps %lld | core(turn0) %lld | issue_rows %lld | matrix %lld | core(turn1) %lld\n",
+           g, w, (unsigned long long)iters, tprof[0], tprof[9], tprof[1], tprof[2], tprof[3], tprof[4],
+           tprof[5], tprof[6], tprof[7], tprof[8]);
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+    printf("prof wg%d w%d push/flush: slot wait %lld | tmem ld %lld | push %lld | flush %lld\n", g, w,
+           tprof[10], tprof[11], tprof[12], tprof[13]);
 #endif
 }
 
