@@ -1,17 +1,23 @@
 """S^3CMTF SGD epoch benchmark (BASELINE.json metric: tensor+matrix nonzero SGD
 updates/sec per epoch; % roofline).
 
-Workload at N=1: BASELINE configs[1] ("config2"): 1e5 x 1e5 x 1e3 tensor,
-1e7 Zipf(1.2) nonzeros (90/10 split -> 9e6 training entries), planted core
-10^3 + noise clipped to [1,5], coupled 1e5 x 1e5 symmetric (1e6 nnz, mode 1)
-and 1e5 x 200 (2e6 nnz, mode 2); rank 10, S^3CMTF-opt.  Synthetic, seeded.
+Workload at N=1 (default): BASELINE configs[4] ("config5") at its largest
+point, the largest single-GPU configuration: a 1e7 x 1e7 x 1e7 tensor with
+1e9 uniform nonzeros (90/10 split -> 9e8 training entries), planted core
+10^3 + N(0, 0.1) noise, coupled 1e7 x 1e6 matrix on mode 1 with 1e8
+nonzeros; rank 10, S^3CMTF-opt.  Synthetic, seeded, generated on the device.
+Other configs are behind --config (config2 = configs[1], config3 =
+configs[2], config4 = configs[3]; config5 --nnz/--rank for the sweep points).
 
 A "step" = one run_epoch (tensor sweep + matrix sweeps + non-finite scan)
 over the device-resident bundle.  `value` = updates/s on the device (CUDA
-events on the launching stream); `e2e` = the same through the C ABI with host
-buffers (bundle upload + epoch + stats read back each step, wall clock).
+events on the launching stream); `e2e` = the same through the C ABI with
+host buffers (bundle upload + epoch + stats read back each step).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+With --gpus N > 1 outside torchrun, the script launches itself under
+torch.distributed.run (one process per GPU) so the DSGD path runs.
 """
 from __future__ import annotations
 
@@ -30,6 +36,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP32_FMA_PER_SM_CLK = 128  # Blackwell SM: 4 x 32 FP32 lanes
+# arithmetic type of each epoch kernel (the parameters and accumulators are
+# fp32 everywhere; the tcgen05 kernel forms its products from split fp16
+# operands, hi*hi + hi*lo + lo*hi, ~22 mantissa bits -- fp32-level accuracy)
+DTYPE = {"order3tm": "f32 (tcgen05 MMAs on split-fp16 x3 operands, fp32 accumulate)",
+         "order3v2": "f32 (core gradient: tf32 mma.sync)",
+         "order4": "f32 (tf32 mma.sync contractions)",
+         "order3": "f32", "generic": "f32"}
 CONFIG_INDEX = {"config1": "BASELINE configs[0]", "config2": "BASELINE configs[1]",
                 "config3": "BASELINE configs[2]", "config4": "BASELINE configs[3]",
                 "config5": "BASELINE configs[4]"}
@@ -41,24 +54,61 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="config2")
+    p.add_argument("--config", default="config5")
     p.add_argument("--scale", type=float, default=1.0)
-    p.add_argument("--nnz", type=float, default=1e8, help="config5 tensor nonzeros")
+    p.add_argument("--nnz", type=float, default=1e9, help="config5 tensor nonzeros")
     p.add_argument("--rank", type=int, default=10, help="config5 rank")
     p.add_argument("--kernel", default="opt", choices=["opt", "naive"])
     p.add_argument("--hog-threads", type=int, default=0)
     p.add_argument("--order", default="random", choices=["sorted", "random"])
     p.add_argument("--uniform", action="store_true",
                    help="diagnostic: uniform instead of Zipf indices")
-    p.add_argument("--cpu-sample", type=int, default=600_000,
+    p.add_argument("--cpu-sample", type=int, default=1_000_000,
                    help="tensor entries in the bounded CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-naive", action="store_true")
     p.add_argument("--strong", action="store_true",
                    help="DSGD (N > 1): fixed total workload instead of weak scaling")
     p.add_argument("--dsgd", action="store_true",
                    help="use the DSGD/NCCL path even with one rank (testing)")
     return p.parse_args()
+
+
+def physical_cores():
+    """Physical cores counted the way the reference's acceptance test does
+    (tests/acceptance.cpp:52-73): distinct (physical id, core id) pairs in
+    /proc/cpuinfo, else the hardware concurrency."""
+    ids, phys, core = set(), -1, -1
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in list(f) + [""]:
+                line = line.rstrip("\n")
+                if not line:
+                    if core >= 0:
+                        ids.add((0 if phys < 0 else phys, core))
+                    phys = core = -1
+                elif line.startswith("physical id"):
+                    phys = int(line.split(":", 1)[1])
+                elif line.startswith("core id"):
+                    core = int(line.split(":", 1)[1])
+    except OSError:
+        pass
+    return len(ids) if ids else (os.cpu_count() or 1)
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N processes (one per GPU) and return its exit
+    code, so the DSGD path engages whichever way the driver launches us."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -166,10 +216,11 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "NVML, 5 ms polling"}
 
 
-def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None):
+def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None,
+                 kernel_opt=True):
     """The reference's own multi-threaded run_epoch (oracle/_ref) on a bounded
     sample of the workload: the first `sample` training entries plus the same
-    fraction of every coupled matrix."""
+    fraction of every coupled matrix, workers = physical cores."""
     from oracle import oracle as O
     from paper_1708_08640_b200.api import CoupledMatrix, DataBundle, SparseTensor
     bundle = host_bundle(bundle, 0, min(sample, bundle.tensor.nnz))
@@ -179,9 +230,9 @@ def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None
     ms = [CoupledMatrix(m.coupled_mode, m.rows, m.cols, m.indices[: int(m.nnz * frac)],
                         m.values[: int(m.nnz * frac)], m.weight) for m in bundle.matrices]
     sb = DataBundle(st, ms)
-    cores = threads or os.cpu_count() or 1
+    cores = threads or physical_cores()
     run = O.RefRun(sb, ranks, seed=0, eta0=lr, mu=0.1, lambda_reg=lam, workers=cores,
-                   kernel_opt=True)
+                   kernel_opt=kernel_opt)
     for _ in range(warmup):
         run.run_epoch()
     times = []
@@ -194,29 +245,52 @@ def cpu_baseline(bundle, ranks, lr, lam, sample, steps=2, warmup=1, threads=None
     return n_upd / min(times), n_upd, cores, times
 
 
+def sample_text(n_sample, nt, nsamp, cores, kernel):
+    return (f"first {n_sample} of {nt} training entries ({100.0 * n_sample / max(1, nt):.3g}%) "
+            f"+ the same fraction of each matrix ({nsamp} updates per epoch); the reference's "
+            f"run_epoch (oracle/_ref, kernel {kernel}) with workers = {cores} physical cores, "
+            "best of the timed epochs after 1 warm-up")
+
+
 def fp32_peak_tflops(sms, mhz):
     return sms * FP32_FMA_PER_SM_CLK * 2 * mhz * 1e6 / 1e12
 
 
+def workload_name(args):
+    return (f"{args.config} ({CONFIG_INDEX.get(args.config, '?')})"
+            + (f", nnz {args.nnz:g}, rank {args.rank}" if args.config == "config5"
+               else f", scale {args.scale:g}"))
+
+
 def run_reference(args):
+    """The reference arm: the reference's own CPU run_epoch (oracle/_ref, the
+    unmodified sources compiled here) with all physical cores, on a bounded
+    sample of the same workload (each step = one epoch over the sample).
+    Rank 0 alone runs under torchrun."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     spec, bundle, test, ranks, lr, lam = make_workload(args)
+    nt = bundle.tensor.nnz
+    n_sample = min(args.cpu_sample, nt)
     ups, n_upd, cores, times = cpu_baseline(bundle, ranks, lr, lam, args.cpu_sample,
                                             steps=max(1, args.steps), warmup=args.warmup)
+    nups, _, _, ntimes = cpu_baseline(bundle, ranks, lr, lam, args.cpu_sample, steps=1,
+                                      warmup=0, kernel_opt=False)
     line = {
         "metric": "tensor+matrix nonzero SGD updates/sec per epoch", "impl": "reference",
         "value": ups, "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * min(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}) bounded sample",
-                   "sample_tensor_entries": min(args.cpu_sample, bundle.tensor.nnz),
-                   "updates_per_step": n_upd, "ranks": ranks},
+        "config": {"workload": workload_name(args) + f" -- bounded sample: {n_sample} of {nt} "
+                               "training entries per step",
+                   "sample_tensor_entries": n_sample, "updates_per_step": n_upd,
+                   "ranks": ranks, "kernel": "opt"},
         "cpu_baseline": {"value": ups, "unit": "updates/s", "cores": cores,
                          "kind": "reference",
-                         "sample": f"first {min(args.cpu_sample, bundle.tensor.nnz)} training "
-                                   f"entries + same fraction of each matrix; run_epoch workers={cores}"},
+                         "sample": sample_text(n_sample, nt, n_upd, cores, "opt"),
+                         "naive": {"value": nups, "unit": "updates/s",
+                                   "ms_per_step": 1e3 * min(ntimes)}},
         "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -294,10 +368,19 @@ def run_ours(args):
     # DRAM traffic per launch of the dominant kernel, from the committed ncu
     # --set full capture of the same command (profiles/ncu_r1_metrics.json)
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_r1_metrics.json")))
+        prof = {}
+        for fn in ("ncu_r1_metrics.json", "ncu_r2_metrics.json"):  # later rounds override
+            fp = os.path.join(ROOT, "profiles", fn)
+            if os.path.exists(fp):
+                prof.update(json.load(open(fp)))
         key = {"order3v2": "hog3v2", "order3tm": "hog3tm", "order4": "hog4"}.get(info["kernel"])
         for k, v in prof.items():
-            scale_ok = (f"scale {args.scale:g}" in k) if "scale" in k else args.scale == 1.0
+            # keys: "<kernel> <config> [scale s | nnz n rank j] (...)"
+            if args.config == "config5":
+                want = f"nnz {args.nnz:g} rank {args.rank}"
+                scale_ok = want in k
+            else:
+                scale_ok = (f"scale {args.scale:g}" in k) if "scale" in k else args.scale == 1.0
             if key and k.startswith(key) and args.config in k.replace("(", " ").split() and scale_ok:
                 roof["traffic"] = (v["dram__bytes_read.sum"]["value"]
                                    + v["dram__bytes_write.sum"]["value"]) * 1e6
@@ -325,15 +408,13 @@ def run_ours(args):
         "metric": "tensor+matrix nonzero SGD updates/sec per epoch", "value": value,
         "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}), "
-                               f"scale {args.scale}" + (f", nnz {args.nnz:g}, rank {args.rank}"
-                                                         if args.config == "config5" else ""),
+        "vs_baseline": None, "dtype": DTYPE.get(info["kernel"], "f32"), "data": "synthetic",
+        "config": {"workload": workload_name(args),
                    "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
                    "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
                    "hog_threads": info["hog_threads"], "tensor_kernel": info["kernel"],
                    "sort_mode": info["sort_mode"], "l2": "flushed between epochs (256 MiB "
-                   "write); COO inputs (180 MB) also exceed L2",
+                   f"write); the COO records ({nt * 16 / 1e6:.0f} MB) also exceed L2",
                    "parallelism": f"dp{world}" if world > 1 else "single"},
         "breakdown_ms": {"tensor": ten_ms, "matrix": mat_ms,
                          "scan": sum(p["scan_ms"] for p in per) / len(per)},
@@ -393,12 +474,33 @@ def run_ours(args):
                        "includes": "set_tensor+add_matrix (H2D, validate, sort), run_epoch, "
                                    "epoch_stats"}
     if rank == 0 and not args.no_cpu_baseline:
+        n_sample = min(args.cpu_sample, nt)
         ups, nsamp, cores, times = cpu_baseline(bundle, ranks, lr, lam, args.cpu_sample)
-        line["cpu_baseline"] = {
-            "value": ups, "unit": "updates/s", "cores": cores, "kind": "reference",
-            "sample": f"first {min(args.cpu_sample, nt)} training entries + same fraction of "
-                      f"each matrix ({nsamp} updates), reference run_epoch workers={cores}, "
-                      "best of 2 after 1 warm-up"}
+        line["cpu_baseline"] = {"value": ups, "unit": "updates/s", "cores": cores,
+                                "kind": "reference",
+                                "sample": sample_text(n_sample, nt, nsamp, cores, "opt")}
+    if not args.no_naive and args.kernel == "opt":
+        # S^3CMTF-naive beside opt (BASELINE configs[1]: "naive vs cached-opt"),
+        # same bundle, a fresh state
+        st.close()
+        del st
+        torch.cuda.empty_cache()
+        cfgn = api.TrainConfig(ranks=ranks, seed=rank, eta0=lr, lambda_reg=lam, kernel="naive",
+                               device=local, hog_threads=args.hog_threads,
+                               order_policy=args.order)
+        stn = api.make_state(cfgn, bundle)
+        api.run_epoch(stn)
+        pn = []
+        for _ in range(2):
+            flush.zero_()
+            torch.cuda.synchronize()
+            api.run_epoch(stn)
+            pn.append(stn.last_epoch_timing())
+        ms_n = sum(p["total_ms"] for p in pn) / len(pn)
+        line["naive"] = {"value": n_upd * world / (ms_n * 1e-3), "unit": "updates/s",
+                         "ms_per_step": ms_n, "tensor_kernel": stn.kernel_info()["kernel"],
+                         "steps": 2, "warmup": 1}
+        stn.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -528,6 +630,8 @@ def run_dsgd(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     elif dist_env()[1] > 1 or args.dsgd:

@@ -17,7 +17,8 @@
  *    factors are row-major I_n x J_n, coupled factors cols x J_mode.
  *
  * Return codes: 0 ok, 1 validation (ValidationError), 2 divergence
- * (DivergenceError), 3 CUDA error, 4 NCCL error, 5 unsupported.
+ * (DivergenceError), 3 CUDA error, 4 NCCL error, 5 unsupported,
+ * 6 parse (ParseError).
  * The message of the last failure is available from cmtf_gpu_last_error()
  * (per calling thread) and cmtf_gpu_ctx_error(ctx).  A context is not
  * thread-safe, as TrainState is not (include/cmtf/trainer.hpp:49-56).
@@ -37,6 +38,7 @@ extern "C" {
 #define CMTF_ECUDA 3
 #define CMTF_ENCCL 4
 #define CMTF_EUNSUPPORTED 5
+#define CMTF_EPARSE 6 /* ParseError (include/cmtf/errors.hpp): text formats */
 
 /* GradientKernel (include/cmtf/trainer.hpp:14) */
 #define CMTF_KERNEL_NAIVE 0
@@ -84,7 +86,8 @@ typedef struct cmtf_gpu_config {
                             the row's expected concurrent updates in other
                             blocks; 0 = default (0.5)                   */
   int32_t flush_every;   /* sweep iterations between hot-row replica
-                            merges; 0 = default (16)                    */
+                            merges; 0 = default (32 on the tcgen05
+                            kernel, 16 on the others)                   */
   int32_t kernel_version;/* 0 = auto (v2 where specialised), 1 = v1     */
   int32_t core_flush_every; /* sweep iterations between block-level core
                             pushes; 0 = default (1)                     */
@@ -110,8 +113,9 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx *ctx);
  * SparseTensor (:17-40) and CoupledMatrix list (:44-70); counts as
  * count_mode_occurrences (src/sparse_data.cpp:344-362) are derived on the
  * device.  Range and finiteness are validated as check_entries
- * (src/sparse_data.cpp:19-64); duplicate detection is the caller's
- * (the reference rejects duplicates when the SparseTensor is constructed).
+ * (src/sparse_data.cpp:19-64) on the device: indices in range, finite
+ * values, and no duplicate index tuples -- rejected with the reference's
+ * message for the lexicographically smallest duplicated tuple.
  * idx/vals may be host (pageable or pinned) or device pointers (UVA). */
 int cmtf_gpu_set_tensor(cmtf_gpu_ctx *ctx, const uint32_t *dims,
                         const uint32_t *idx, const double *vals, uint64_t nnz);
@@ -261,6 +265,80 @@ int cmtf_gpu_last_epoch_timing(cmtf_gpu_ctx *ctx, double *kernel_ms,
  * 2 specialised N=4; hog_threads actually used. */
 int cmtf_gpu_kernel_info(cmtf_gpu_ctx *ctx, int32_t *which,
                          int32_t *hog_threads, int32_t *sort_mode);
+
+/* ---- text formats and host-side data preparation ----
+ * Host C++ (io.cpp), all host threads; no device is needed except for
+ * cmtf_gpu_check_entries. */
+
+/* parse_coo_file + infer_dims (src/sparse_data.cpp:124-227): the reference's
+ * text format -- an optional dims header (detected from the first two data
+ * lines), then one entry per line, 1-based indices and the value; '#'
+ * comments and blank lines ignored.  expected_order 0 = any (load_tensor),
+ * 2 = a matrix file (load_matrix).  Errors: CMTF_EPARSE with the reference's
+ * ParseError message (line numbers included).  The parsed object owns
+ * 0-based AoS indices and f64 values; dims = the header or the per-mode
+ * maximum index.  threads <= 0: all hardware threads. */
+typedef struct cmtf_coo cmtf_coo;
+int cmtf_coo_parse(const char *path, int32_t expected_order, int32_t threads,
+                   cmtf_coo **out);
+int32_t cmtf_coo_order(const cmtf_coo *c);
+uint64_t cmtf_coo_nnz(const cmtf_coo *c);
+int32_t cmtf_coo_has_header(const cmtf_coo *c);
+const uint32_t *cmtf_coo_dims(const cmtf_coo *c);
+const uint32_t *cmtf_coo_indices(const cmtf_coo *c);
+const double *cmtf_coo_values(const cmtf_coo *c);
+void cmtf_coo_free(cmtf_coo *c);
+
+/* write_coo (src/sparse_data.cpp:279-302) behind save_tensor / save_matrix:
+ * the dims line, then "i1 .. iN %.17g" per entry (1-based). */
+int cmtf_coo_write(const char *path, int32_t order, const uint32_t *dims,
+                   const uint32_t *idx, const double *vals, uint64_t nnz,
+                   int32_t threads);
+
+/* check_entries (src/sparse_data.cpp:19-64), the validation of the
+ * SparseTensor (is_matrix 0) and CoupledMatrix (is_matrix 1) constructors,
+ * on the device: order >= 2 for tensors, positive dims, indices in range,
+ * finite values, no duplicate tuples -- the reference's ValidationError
+ * messages.  idx/vals: host or device pointers. */
+int cmtf_gpu_check_entries(int32_t device, int32_t order, const uint32_t *dims,
+                           const uint32_t *idx, const double *vals,
+                           uint64_t nnz, int32_t is_matrix);
+
+/* split_train_test (src/sparse_data.cpp:311-342): Fisher-Yates over the
+ * entry ids with make_rng(seed, Split); test = the first
+ * round(test_fraction * nnz) shuffled ids, train = the rest, both in
+ * shuffled order.  Output buffers hold (nnz - n_test) / n_test entries; all
+ * four NULL = size query (*n_test_out only). */
+int cmtf_split_train_test(int32_t order, const uint32_t *idx, const double *vals,
+                          uint64_t nnz, double test_fraction, uint64_t seed,
+                          uint32_t *train_idx, double *train_vals,
+                          uint32_t *test_idx, double *test_vals,
+                          uint64_t *n_test_out, int32_t threads);
+
+/* save_model (src/model_io.cpp:94-126): CORE (ranks line, row-major
+ * values, J_N per line; a CP core -- its ranks[0] superdiagonal values --
+ * is written densely), FACTOR n (rows cols, values), COUPLED m (rows cols,
+ * values), 17 significant digits.  validate_model's checks
+ * (src/tucker.cpp:208-224). */
+int cmtf_model_save(const char *path, int32_t order, const uint32_t *ranks,
+                    int32_t cp, const double *core, const uint32_t *factor_rows,
+                    const double *const *factors, int32_t n_coupled,
+                    const int32_t *coupled_modes, const uint32_t *coupled_rows,
+                    const double *const *couplings);
+
+/* load_model (src/model_io.cpp:128-179); the core is dense. */
+typedef struct cmtf_model_file cmtf_model_file;
+int cmtf_model_load(const char *path, cmtf_model_file **out);
+int32_t cmtf_model_order(const cmtf_model_file *m);
+const uint32_t *cmtf_model_ranks(const cmtf_model_file *m);
+const double *cmtf_model_core(const cmtf_model_file *m);
+uint32_t cmtf_model_factor_rows(const cmtf_model_file *m, int32_t n);
+const double *cmtf_model_factor(const cmtf_model_file *m, int32_t n);
+int32_t cmtf_model_n_coupled(const cmtf_model_file *m);
+int32_t cmtf_model_coupled_mode(const cmtf_model_file *m, int32_t c);
+uint32_t cmtf_model_coupled_rows(const cmtf_model_file *m, int32_t c);
+const double *cmtf_model_coupled(const cmtf_model_file *m, int32_t c);
+void cmtf_model_free(cmtf_model_file *m);
 
 #ifdef __cplusplus
 }

@@ -532,3 +532,88 @@ def run_epoch_counts(bundle, model: OracleModel, schedule, eta, lambda_reg, coun
         C.c_double(eta), C.c_double(lambda_reg), C.c_int32(int(kernel_opt)), C.c_int32(1),
         C.c_int32(0), C.c_int32(0), _p(cc, C.c_uint32), C.c_uint64(nnz_global),
         C.c_uint64(len(schedule)))
+
+
+# ----------------------------------------------------------------------
+# The reference's text formats (test infrastructure: golden fixtures)
+# ----------------------------------------------------------------------
+def ref_load(path, is_matrix=False, coupled_mode=1, weight=10.0, dims=None):
+    """load_tensor / load_matrix of the reference.  Returns ("ok", dims,
+    idx, vals) or (kind, message) with kind ParseError / ValidationError."""
+    L = ref()
+    code = C.c_int32()
+    if is_matrix:
+        d = np.ascontiguousarray(dims, dtype=np.uint32)
+        L.ref_load_matrix.restype = C.c_void_p
+        L.ref_load_matrix.argtypes = [C.c_char_p, C.c_int32, C.c_double, C.c_int32, u32p,
+                                      C.POINTER(C.c_int32)]
+        h = L.ref_load_matrix(os.fsencode(str(path)), coupled_mode, weight, len(d),
+                              _p(d, C.c_uint32), C.byref(code))
+    else:
+        L.ref_load_tensor.restype = C.c_void_p
+        L.ref_load_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int32)]
+        h = L.ref_load_tensor(os.fsencode(str(path)), C.byref(code))
+    if not h:
+        kind = {1: "ParseError", 2: "ValidationError"}.get(code.value, "Error")
+        return kind, L.ref_last_error().decode()
+    order = C.c_int32()
+    dd = np.zeros(64, dtype=np.uint32)
+    nnz = C.c_uint64()
+    L.ref_coo_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), u32p,
+                               C.POINTER(C.c_uint64)]
+    L.ref_coo_info(h, int(is_matrix), C.byref(order), _p(dd, C.c_uint32), C.byref(nnz))
+    idx = np.zeros(max(1, nnz.value * order.value), dtype=np.uint32)
+    vals = np.zeros(max(1, nnz.value))
+    L.ref_coo_get.argtypes = [C.c_void_p, C.c_int32, u32p, f64p]
+    L.ref_coo_get(h, int(is_matrix), _p(idx, C.c_uint32), _p(vals, C.c_double))
+    L.ref_coo_free.argtypes = [C.c_void_p, C.c_int32]
+    L.ref_coo_free(h, int(is_matrix))
+    n = nnz.value
+    return ("ok", [int(x) for x in dd[: order.value]],
+            idx[: n * order.value].reshape(n, order.value), vals[:n])
+
+
+def ref_save_tensor(path, dims, idx, vals):
+    L = ref()
+    d = np.ascontiguousarray(dims, dtype=np.uint32)
+    i = np.ascontiguousarray(idx, dtype=np.uint32)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    L.ref_save_tensor.argtypes = [C.c_char_p, C.c_int32, u32p, C.c_uint64, u32p, f64p]
+    rc = L.ref_save_tensor(os.fsencode(str(path)), len(d), _p(d, C.c_uint32), v.shape[0],
+                           _p(i, C.c_uint32), _p(v, C.c_double))
+    if rc:
+        raise ValueError(L.ref_last_error().decode())
+
+
+def ref_save_model(path, core, factors, couplings=(), coupling_modes=(), cp=False):
+    L = ref()
+    ranks = np.ascontiguousarray([f.shape[1] for f in factors], dtype=np.uint32)
+    c = np.ascontiguousarray(core, dtype=np.float64).reshape(-1)
+    fs = [np.ascontiguousarray(f, dtype=np.float64) for f in factors]
+    rows = np.ascontiguousarray([f.shape[0] for f in fs], dtype=np.uint32)
+    fp = (f64p * len(fs))(*[_p(f, C.c_double) for f in fs])
+    cs = [np.ascontiguousarray(v, dtype=np.float64) for v in couplings]
+    cm = np.ascontiguousarray(list(coupling_modes), dtype=np.int32)
+    cr = np.ascontiguousarray([v.shape[0] for v in cs], dtype=np.uint32)
+    cpp = (f64p * max(1, len(cs)))(*[_p(v, C.c_double) for v in cs])
+    L.ref_save_model.argtypes = [C.c_char_p, C.c_int32, u32p, C.c_int32, f64p, u32p,
+                                 C.POINTER(f64p), C.c_int32, C.POINTER(C.c_int32), u32p,
+                                 C.POINTER(f64p)]
+    rc = L.ref_save_model(os.fsencode(str(path)), len(ranks), _p(ranks, C.c_uint32), int(cp),
+                          _p(c, C.c_double), _p(rows, C.c_uint32), fp, len(cs),
+                          _p(cm, C.c_int32), _p(cr, C.c_uint32), cpp)
+    if rc:
+        raise ValueError(L.ref_last_error().decode())
+
+
+def ref_load_model(path):
+    """load_model of the reference: ("ok", order, n_factors, n_coupled) or
+    (kind, message)."""
+    L = ref()
+    o, nf, nc = C.c_int32(), C.c_int32(), C.c_int32()
+    L.ref_load_model.argtypes = [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32)]
+    rc = L.ref_load_model(os.fsencode(str(path)), C.byref(o), C.byref(nf), C.byref(nc))
+    if rc:
+        return {1: "ParseError", 2: "ValidationError"}.get(rc, "Error"), L.ref_last_error().decode()
+    return "ok", o.value, nf.value, nc.value

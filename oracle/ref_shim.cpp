@@ -14,6 +14,7 @@
 #include "cmtf/errors.hpp"
 #include "cmtf/eval.hpp"
 #include "cmtf/gradients.hpp"
+#include "cmtf/model_io.hpp"
 #include "cmtf/sparse_data.hpp"
 #include "cmtf/synth.hpp"
 #include "cmtf/trainer.hpp"
@@ -354,6 +355,121 @@ void ref_bundle_get(void* bundle, uint32_t* idx, double* vals,
     if (mat_vals)
       std::memcpy(mat_vals[m], b->matrices[m].values().data(),
                   b->matrices[m].nnz() * sizeof(double));
+  }
+}
+
+// ---- text formats (src/sparse_data.cpp:124-311, src/model_io.cpp) ----
+// error code: 1 ParseError, 2 ValidationError, 3 anything else
+static int classify(const std::exception& e) {
+  if (dynamic_cast<const ParseError*>(&e)) return 1;
+  if (dynamic_cast<const ValidationError*>(&e)) return 2;
+  return 3;
+}
+
+void* ref_load_tensor(const char* path, int32_t* code) {
+  try {
+    *code = 0;
+    return new SparseTensor(load_tensor(path));
+  } catch (const std::exception& e) {
+    *code = fail(e, classify(e));
+    return nullptr;
+  }
+}
+
+void* ref_load_matrix(const char* path, int32_t coupled_mode, double weight, int32_t order,
+                      const uint32_t* dims, int32_t* code) {
+  try {
+    *code = 0;
+    SparseTensor t(std::vector<uint32_t>(dims, dims + order), {}, {});
+    return new CoupledMatrix(load_matrix(path, coupled_mode, weight, t));
+  } catch (const std::exception& e) {
+    *code = fail(e, classify(e));
+    return nullptr;
+  }
+}
+
+void ref_coo_info(void* obj, int32_t is_matrix, int32_t* order, uint32_t* dims, uint64_t* nnz) {
+  if (is_matrix) {
+    auto* m = static_cast<CoupledMatrix*>(obj);
+    *order = 2;
+    dims[0] = m->rows();
+    dims[1] = m->cols();
+    *nnz = m->nnz();
+  } else {
+    auto* t = static_cast<SparseTensor*>(obj);
+    *order = t->order();
+    for (int n = 0; n < t->order(); ++n) dims[n] = t->dims()[n];
+    *nnz = t->nnz();
+  }
+}
+
+void ref_coo_get(void* obj, int32_t is_matrix, uint32_t* idx, double* vals) {
+  const std::vector<uint32_t>& i = is_matrix ? static_cast<CoupledMatrix*>(obj)->indices()
+                                             : static_cast<SparseTensor*>(obj)->indices();
+  const std::vector<double>& v = is_matrix ? static_cast<CoupledMatrix*>(obj)->values()
+                                           : static_cast<SparseTensor*>(obj)->values();
+  std::memcpy(idx, i.data(), i.size() * sizeof(uint32_t));
+  std::memcpy(vals, v.data(), v.size() * sizeof(double));
+}
+
+void ref_coo_free(void* obj, int32_t is_matrix) {
+  if (is_matrix) delete static_cast<CoupledMatrix*>(obj);
+  else delete static_cast<SparseTensor*>(obj);
+}
+
+int ref_save_tensor(const char* path, int32_t order, const uint32_t* dims, uint64_t nnz,
+                    const uint32_t* idx, const double* vals) {
+  try {
+    SparseTensor t(std::vector<uint32_t>(dims, dims + order),
+                   std::vector<uint32_t>(idx, idx + nnz * order),
+                   std::vector<double>(vals, vals + nnz));
+    save_tensor(path, t);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, classify(e));
+  }
+}
+
+// load_model: 0 ok (ranks / number of factors / couplings returned), else the
+// error class with the message in ref_last_error()
+int ref_load_model(const char* path, int32_t* order, int32_t* n_factors, int32_t* n_coupled) {
+  try {
+    FactorModel m = load_model(path);
+    *order = m.core.order();
+    *n_factors = (int32_t)m.factors.size();
+    *n_coupled = (int32_t)m.couplings.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, classify(e));
+  }
+}
+
+int ref_save_model(const char* path, int32_t order, const uint32_t* ranks, int32_t cp,
+                   const double* core, const uint32_t* factor_rows, const double* const* factors,
+                   int32_t n_coupled, const int32_t* coupled_modes, const uint32_t* coupled_rows,
+                   const double* const* couplings) {
+  try {
+    std::vector<uint32_t> rk(ranks, ranks + order);
+    size_t cs = 1;
+    for (auto j : rk) cs *= j;
+    const size_t stored = cp ? rk[0] : cs;
+    FactorModel m{CoreTensor(rk, cp ? CoreStructure::HyperDiagonalCp : CoreStructure::DenseTucker,
+                             std::vector<double>(core, core + stored)),
+                  {}, {}};
+    for (int n = 0; n < order; ++n)
+      m.factors.emplace_back(factor_rows[n], rk[n],
+                             std::vector<double>(factors[n], factors[n] + (size_t)factor_rows[n] * rk[n]));
+    for (int c = 0; c < n_coupled; ++c) {
+      const uint32_t J = rk[coupled_modes[c]];
+      m.couplings.push_back(Coupling{coupled_modes[c],
+                                     FactorMatrix(coupled_rows[c], J,
+                                                  std::vector<double>(couplings[c],
+                                                                      couplings[c] + (size_t)coupled_rows[c] * J))});
+    }
+    save_model(path, m);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, classify(e));
   }
 }
 

@@ -13,3 +13,6 @@ from .api import (  # noqa: F401
     make_bundle, make_state, matrix_entry_gradients, matrix_rmse, run_epoch,
     test_rmse, train)
 from ._abi import build, lib  # noqa: F401
+from .io import (  # noqa: F401
+    check_entries, load_matrix, load_model, load_tensor, save_matrix, save_model, save_tensor,
+    split_train_test)

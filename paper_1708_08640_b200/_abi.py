@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("CMTF_B200_LIB") or os.path.join(_HERE, "libcmtf_b200.
 _lock = threading.Lock()
 _lib = None
 
-OK, EVALIDATION, EDIVERGENCE, ECUDA, ENCCL, EUNSUPPORTED = 0, 1, 2, 3, 4, 5
+OK, EVALIDATION, EDIVERGENCE, ECUDA, ENCCL, EUNSUPPORTED, EPARSE = 0, 1, 2, 3, 4, 5, 6
 KERNEL_NAIVE, KERNEL_OPT = 0, 1
 EXEC_HOGWILD, EXEC_SERIAL = 0, 1
 
@@ -102,6 +102,34 @@ SIGNATURES = [
     ("cmtf_gpu_elapsed_ms", C.c_int, [P, C.c_int32, C.c_int32, f64p]),
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
+    # text formats and host-side data preparation (io.cpp)
+    ("cmtf_coo_parse", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(P)]),
+    ("cmtf_coo_order", C.c_int32, [P]),
+    ("cmtf_coo_nnz", C.c_uint64, [P]),
+    ("cmtf_coo_has_header", C.c_int32, [P]),
+    ("cmtf_coo_dims", u32p, [P]),
+    ("cmtf_coo_indices", u32p, [P]),
+    ("cmtf_coo_values", f64p, [P]),
+    ("cmtf_coo_free", None, [P]),
+    ("cmtf_coo_write", C.c_int, [C.c_char_p, C.c_int32, u32p, u32p, f64p, C.c_uint64,
+                                 C.c_int32]),
+    ("cmtf_gpu_check_entries", C.c_int, [C.c_int32, C.c_int32, u32p, u32p, f64p, C.c_uint64,
+                                         C.c_int32]),
+    ("cmtf_split_train_test", C.c_int, [C.c_int32, u32p, f64p, C.c_uint64, C.c_double,
+                                        C.c_uint64, u32p, f64p, u32p, f64p, u64p, C.c_int32]),
+    ("cmtf_model_save", C.c_int, [C.c_char_p, C.c_int32, u32p, C.c_int32, f64p, u32p, f64pp,
+                                  C.c_int32, i32p, u32p, f64pp]),
+    ("cmtf_model_load", C.c_int, [C.c_char_p, C.POINTER(P)]),
+    ("cmtf_model_order", C.c_int32, [P]),
+    ("cmtf_model_ranks", u32p, [P]),
+    ("cmtf_model_core", f64p, [P]),
+    ("cmtf_model_factor_rows", C.c_uint32, [P, C.c_int32]),
+    ("cmtf_model_factor", f64p, [P, C.c_int32]),
+    ("cmtf_model_n_coupled", C.c_int32, [P]),
+    ("cmtf_model_coupled_mode", C.c_int32, [P, C.c_int32]),
+    ("cmtf_model_coupled_rows", C.c_uint32, [P, C.c_int32]),
+    ("cmtf_model_coupled", f64p, [P, C.c_int32]),
+    ("cmtf_model_free", None, [P]),
 ]
 
 

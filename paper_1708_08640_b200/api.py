@@ -50,6 +50,7 @@ def _raise(rc: int, msg: str):
         _abi.ECUDA: CudaError,
         _abi.ENCCL: CudaError,
         _abi.EUNSUPPORTED: UnsupportedError,
+        _abi.EPARSE: ParseError,
     }.get(rc, CmtfError)
     raise cls(msg)
 
@@ -145,9 +146,9 @@ class TrainConfig:
     sort_mode: int = -1
     force_generic: bool = False
     order_policy: str = "random"  # "random" | "sorted" | "caller"
-    hot_tau: float = 0.0  # 0 = default 2.0, < 0 disables hot-row replicas
+    hot_tau: float = 0.0  # 0 = default 0.5, < 0 disables hot-row replicas
     kappa: float = 0.0  # 0 = default 0.5
-    flush_every: int = 0  # 0 = default 8
+    flush_every: int = 0  # 0 = default: 32 (tcgen05 kernel), 16 (others)
     kernel_version: int = 0  # 0 = auto (v2), 1 = v1
     core_flush_every: int = 0  # 0 = default 1
     kappa_core: float = 0.0  # 0 = default 2.0
@@ -184,10 +185,11 @@ class FactorModel:
     core: np.ndarray
     factors: List[np.ndarray]
     couplings: List[np.ndarray] = field(default_factory=list)
+    coupling_modes: List[int] = field(default_factory=list)  # Coupling::mode (0-based)
 
     def copy(self) -> "FactorModel":
         return FactorModel(self.core.copy(), [f.copy() for f in self.factors],
-                           [c.copy() for c in self.couplings])
+                           [c.copy() for c in self.couplings], list(self.coupling_modes))
 
 
 @dataclass
@@ -256,7 +258,8 @@ class TrainState:
         fp = (f64p_t * max(1, len(F)))(*[_ptr(f, C.c_double) for f in F])
         vp = (f64p_t * max(1, len(V)))(*[_ptr(v, C.c_double) for v in V])
         self._check(self._L.cmtf_gpu_get_model(self._h, _ptr(core, C.c_double), fp, vp))
-        return FactorModel(core.reshape(ranks), F, V)
+        return FactorModel(core.reshape(ranks), F, V,
+                           [m.coupled_mode for m in self.bundle.matrices])
 
     def finalized_model(self) -> FactorModel:
         """The tail of train() (src/trainer.cpp:342-345) on the current model:
@@ -269,7 +272,8 @@ class TrainState:
         fp = (f64p_t * max(1, len(F)))(*[_ptr(f, C.c_double) for f in F])
         vp = (f64p_t * max(1, len(V)))(*[_ptr(v, C.c_double) for v in V])
         self._check(self._L.cmtf_gpu_finalize_model(self._h, _ptr(core, C.c_double), fp, vp))
-        return FactorModel(core.reshape(ranks), F, V)
+        return FactorModel(core.reshape(ranks), F, V,
+                           [m.coupled_mode for m in self.bundle.matrices])
 
     @model.setter
     def model(self, m: FactorModel):

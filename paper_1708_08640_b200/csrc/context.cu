@@ -27,6 +27,8 @@
 #include "hog4.cuh"
 #include "hog3tm.cuh"
 
+#include "host_rng.hpp"
+
 using namespace cmtfb;
 
 namespace {
@@ -260,29 +262,7 @@ int set_err(cmtf_gpu_ctx* ctx, int code, const char* fmt, ...) {
     if (rc_ != CMTF_OK) return rc_; \
   } while (0)
 
-// splitmix-mixed mt19937_64 streams (src/rng.cpp:8-26, rng.hpp:11-36).
-uint64_t splitmix64(uint64_t& s) {
-  s += 0x9e3779b97f4a7c15ULL;
-  uint64_t z = s;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
-}
-std::mt19937_64 make_rng(uint64_t seed, uint64_t stream, uint64_t index) {
-  uint64_t state = seed;
-  uint64_t mixed = splitmix64(state);
-  state ^= stream * 0xd1b54a32d192ed03ULL;
-  mixed ^= splitmix64(state);
-  state ^= index * 0x9e3779b97f4a7c15ULL;
-  mixed ^= splitmix64(state);
-  return std::mt19937_64(mixed);
-}
-inline double uniform01(std::mt19937_64& g) {
-  return static_cast<double>(g() >> 11) * 0x1.0p-53;
-}
-inline uint64_t bounded(std::mt19937_64& g, uint64_t n) {
-  return static_cast<uint64_t>((static_cast<unsigned __int128>(g()) * n) >> 64);
-}
+// splitmix-mixed mt19937_64 streams: host_rng.hpp (src/rng.cpp:8-26).
 
 template <typename T>
 int dalloc(cmtf_gpu_ctx* ctx, T** p, size_t n) {
@@ -1703,6 +1683,15 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
   if (cudaSetDevice(ctx->device) != cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "cudaSetDevice failed"));
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  // L2 fill granularity for misses: the epoch's row gathers and regulariser
+  // lookups are random 16-48 byte accesses, so a wider fill only adds DRAM
+  // traffic (CMTF_L2_FETCH overrides; 0 keeps the driver default)
+  {
+    int g = 32;
+    if (const char* v = std::getenv("CMTF_L2_FETCH")) g = std::atoi(v);
+    if (g > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)g);
+    cudaGetLastError();
+  }
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(set_err(nullptr, CMTF_ECUDA, "stream creation failed"));
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
@@ -1961,6 +1950,79 @@ std::string dup_message(const char* what, const std::vector<uint32_t>& t) {
   std::string msg = std::string("duplicate ") + what + " index (";
   for (size_t n = 0; n < t.size(); ++n) msg += (n ? " " : "") + std::to_string(t[n] + 1);
   return msg + ")";
+}
+
+// check_entries' range and finiteness pass (src/sparse_data.cpp:29-41):
+// first entry with an index out of range / a non-finite value
+__global__ void check_entries_kernel(const uint32_t* idx, const double* vals, uint64_t nnz,
+                                     DupKey k, unsigned long long* bad) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    for (int n = 0; n < k.order; ++n)
+      if (idx[e * k.order + n] >= k.dims[n]) atomicMin(&bad[0], (unsigned long long)e);
+    if (!isfinite(vals[e])) atomicMin(&bad[1], (unsigned long long)e);
+  }
+}
+
+int cmtf_gpu_check_entries(int32_t device, int32_t order, const uint32_t* dims,
+                           const uint32_t* idx, const double* vals, uint64_t nnz,
+                           int32_t is_matrix) {
+  const char* what = is_matrix ? "matrix" : "tensor";
+  if (!dims || order < 1 || order > kMaxOrder)
+    return set_err(nullptr, CMTF_EVALIDATION, "invalid arguments");
+  if (order < 2 && !is_matrix)
+    return set_err(nullptr, CMTF_EVALIDATION, "tensor order must be at least 2");
+  for (int n = 0; n < order; ++n)
+    if (dims[n] == 0) return set_err(nullptr, CMTF_EVALIDATION, "mode sizes must be positive");
+  if (nnz == 0) return CMTF_OK;
+  cmtf_gpu_config cfg;
+  cmtf_gpu_config_default(&cfg);
+  std::vector<uint32_t> ones(order, 1u);
+  cfg.order = order;
+  cfg.ranks = ones.data();
+  cfg.device = device;
+  cmtf_gpu_ctx* ctx = nullptr;
+  TRY(cmtf_gpu_create(&cfg, &ctx));
+  auto run = [&]() -> int {
+    uint32_t* d_idx = nullptr;
+    double* d_vals = nullptr;
+    TRY(dalloc(ctx, &d_idx, nnz * (uint64_t)order));
+    TRY(dalloc(ctx, &d_vals, nnz));
+    auto cleanup = [&](int rc) {
+      dfree(d_idx);
+      dfree(d_vals);
+      return rc;
+    };
+    if (cudaMemcpyAsync(d_idx, idx, nnz * order * sizeof(uint32_t), cudaMemcpyDefault,
+                        ctx->stream) != cudaSuccess ||
+        cudaMemcpyAsync(d_vals, vals, nnz * sizeof(double), cudaMemcpyDefault, ctx->stream) !=
+            cudaSuccess)
+      return cleanup(set_err(ctx, CMTF_ECUDA, "copy of the entries failed"));
+    DupKey k{};
+    k.order = order;
+    for (int n = 0; n < order; ++n) k.dims[n] = dims[n];
+    cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream);
+    check_entries_kernel<<<grid_for(nnz), 256, 0, ctx->stream>>>(d_idx, d_vals, nnz, k,
+                                                                 ctx->d_first);
+    unsigned long long bad[2];
+    if (cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      return cleanup(set_err(ctx, CMTF_ECUDA, "entry check failed"));
+    if (bad[0] != ~0ull || bad[1] != ~0ull)
+      return cleanup(entry_error(ctx, what, d_idx, order, dims, bad));
+    std::vector<uint32_t> tup;
+    bool dup = false;
+    const int rc = find_duplicate(ctx, d_idx, nnz, order, dims, &tup, &dup);
+    if (rc) return cleanup(rc);
+    if (dup) return cleanup(set_err(ctx, CMTF_EVALIDATION, "%s", dup_message(what, tup).c_str()));
+    return cleanup(CMTF_OK);
+  };
+  const int rc = run();
+  const std::string msg = ctx->err;
+  cmtf_gpu_destroy(ctx);
+  if (rc) g_last_error = msg;
+  return rc;
 }
 
 int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
@@ -3520,3 +3582,11 @@ int cmtf_gpu_kernel_info(cmtf_gpu_ctx* ctx, int32_t* which, int32_t* hog_threads
 }
 
 }  // extern "C"
+
+// io.cpp's error hook (the thread's last error, as set_err)
+namespace cmtfb {
+int io_fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+}  // namespace cmtfb

@@ -223,3 +223,17 @@ def config4(scale: float = 1.0) -> PlantedSpec:
                        matrices=[MatrixSpec(0, 10_000, int(3e7 * scale)),
                                  MatrixSpec(1, 10_000, int(3e7 * scale))],
                        test_fraction=0.1, seed=0)
+
+
+def config3(scale: float = 1.0) -> PlantedSpec:
+    """configs[2] on the host (numpy): 1e6 x 1e6 x 1e4, 1e8 * scale nonzeros
+    with Zipf(1.1) mode-1/mode-2 indices and uniform mode 3, planted 10^3 core
+    + N(0, 0.1) noise (no clipping is stated); one coupled 1e6 x 1e4 matrix on
+    mode 1 with 1e7 * scale nonzeros.  The full-size run of the reference
+    (scripts/oracle_config2.py --config config3) pins the GPU's 10-epoch RMSE;
+    the bench generates the same laws on the device (synth_gpu.config3)."""
+    return PlantedSpec(dims=[1_000_000, 1_000_000, 10_000], nnz=int(1e8 * scale),
+                       ranks=[10, 10, 10], laws=[("zipf", 1.1), ("zipf", 1.1), "uniform"],
+                       factor_law="ref", noise=0.1,
+                       matrices=[MatrixSpec(0, 10_000, int(1e7 * scale))],
+                       test_fraction=0.1, seed=0)
