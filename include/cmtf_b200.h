@@ -61,7 +61,9 @@ typedef struct cmtf_gpu_config {
   double rel_tol;        /* default 1e-4 */
   uint64_t seed;
   int32_t kernel;         /* CMTF_KERNEL_* */
-  int32_t core_structure; /* 0 dense Tucker; 1 CP (not yet on device)   */
+  int32_t core_structure; /* 0 dense Tucker; 1 CP / hyper-diagonal (equal
+                            ranks; model transfers carry its ranks[0]
+                            superdiagonal values as the core)           */
   int32_t nonnegative;    /* per-step clamp at 0 (src/trainer.cpp:185) */
   double init_scale;      /* default 1.0 */
   /* ---- device fields ---- */
@@ -199,14 +201,17 @@ int cmtf_gpu_kernel_probe(cmtf_gpu_ctx *ctx, double *xhat, double *residual,
 
 /* Stateless batched form of compute_gradient / compute_gradient_opt
  * (include/cmtf/gradients.hpp:59-74): n independent entries, each with its
- * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core. */
+ * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core.
+ * core_structure 0: dense core (prod J values); 1: CP / hyper-diagonal
+ * (src/gradients.cpp:108-115,145-152,192-205): core and each entry's core
+ * gradient hold the ranks[0] superdiagonal values, all ranks equal. */
 int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order,
-                              const uint32_t *ranks, const double *core,
-                              uint64_t n, const double *x, const double *rows,
-                              const uint32_t *counts, double lambda_reg,
-                              uint64_t nnz_total, int32_t with_core,
-                              double *grow, double *gcore, double *residual,
-                              int32_t device);
+                              const uint32_t *ranks, int32_t core_structure,
+                              const double *core, uint64_t n, const double *x,
+                              const double *rows, const uint32_t *counts,
+                              double lambda_reg, uint64_t nnz_total,
+                              int32_t with_core, double *grow, double *gcore,
+                              double *residual, int32_t device);
 
 /* Batched matrix_entry_gradients (include/cmtf/gradients.hpp:83-86). */
 int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double *y,

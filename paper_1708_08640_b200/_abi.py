@@ -84,7 +84,7 @@ SIGNATURES = [
     ("cmtf_gpu_entry_grads", C.c_int, [P, u64p, C.c_uint64, f64p, f64p, f64p, f64p]),
     ("cmtf_gpu_kernel_probe", C.c_int, [P, f64p, f64p, f64p, f64p]),
     ("cmtf_gpu_compute_gradient", C.c_int,
-     [C.c_int32, C.c_int32, u32p, f64p, C.c_uint64, f64p, f64p, u32p, C.c_double,
+     [C.c_int32, C.c_int32, u32p, C.c_int32, f64p, C.c_uint64, f64p, f64p, u32p, C.c_double,
       C.c_uint64, C.c_int32, f64p, f64p, f64p, C.c_int32]),
     ("cmtf_gpu_matrix_entry_gradients", C.c_int,
      [C.c_uint64, C.c_uint32, f64p, f64p, f64p, C.c_double, C.c_double, u32p, f64p,

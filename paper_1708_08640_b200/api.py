@@ -250,15 +250,21 @@ class TrainState:
         return ranks, fac, cpl
 
     @property
+    def _cp(self) -> bool:
+        return self.config.core_structure != "dense"
+
+    @property
     def model(self) -> FactorModel:
+        """The model; a CP core comes back as its ranks[0] superdiagonal
+        values (CoreTensor::stored() of a HyperDiagonalCp core)."""
         ranks, fac, cpl = self._shapes()
-        core = np.zeros(int(np.prod(ranks)), dtype=np.float64)
+        core = np.zeros(ranks[0] if self._cp else int(np.prod(ranks)), dtype=np.float64)
         F = [np.zeros(s, dtype=np.float64) for s in fac]
         V = [np.zeros(s, dtype=np.float64) for s in cpl]
         fp = (f64p_t * max(1, len(F)))(*[_ptr(f, C.c_double) for f in F])
         vp = (f64p_t * max(1, len(V)))(*[_ptr(v, C.c_double) for v in V])
         self._check(self._L.cmtf_gpu_get_model(self._h, _ptr(core, C.c_double), fp, vp))
-        return FactorModel(core.reshape(ranks), F, V,
+        return FactorModel(core if self._cp else core.reshape(ranks), F, V,
                            [m.coupled_mode for m in self.bundle.matrices])
 
     def finalized_model(self) -> FactorModel:
@@ -272,6 +278,9 @@ class TrainState:
         fp = (f64p_t * max(1, len(F)))(*[_ptr(f, C.c_double) for f in F])
         vp = (f64p_t * max(1, len(V)))(*[_ptr(v, C.c_double) for v in V])
         self._check(self._L.cmtf_gpu_finalize_model(self._h, _ptr(core, C.c_double), fp, vp))
+        if self._cp and self.config.nonnegative:  # the projection keeps the CP structure
+            return FactorModel(core[: ranks[0]].copy(), F, V,
+                               [m.coupled_mode for m in self.bundle.matrices])
         return FactorModel(core.reshape(ranks), F, V,
                            [m.coupled_mode for m in self.bundle.matrices])
 
@@ -427,20 +436,23 @@ def kernel_probe(state: TrainState):
 
 
 def _compute_gradient(kernel: int, x, core, rows, lambda_reg, counts, nnz_total,
-                      with_core=True, device=0):
+                      with_core=True, device=0, ranks=None, cp=False):
     core = np.ascontiguousarray(core, dtype=np.float64)
-    ranks = np.array(core.shape, dtype=np.uint32)
+    if ranks is None:
+        ranks = core.shape
+    ranks = np.array(ranks, dtype=np.uint32)
     x = np.ascontiguousarray(np.atleast_1d(x), dtype=np.float64)
     n = x.shape[0]
     rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(n, -1)
     counts = np.ascontiguousarray(counts, dtype=np.uint32).reshape(n, -1)
-    sumj, size = int(ranks.sum()), int(np.prod(ranks))
+    sumj = int(ranks.sum())
+    size = int(ranks[0]) if cp else int(np.prod(ranks))
     grow = np.zeros((n, sumj))
     gcore = np.zeros((n, size))
     res = np.zeros(n)
     L = _abi.lib()
     rc = L.cmtf_gpu_compute_gradient(
-        kernel, len(ranks), _ptr(ranks, C.c_uint32), _ptr(core, C.c_double), n,
+        kernel, len(ranks), _ptr(ranks, C.c_uint32), int(cp), _ptr(core, C.c_double), n,
         _ptr(x, C.c_double), _ptr(rows, C.c_double), _ptr(counts, C.c_uint32),
         lambda_reg, nnz_total, int(with_core), _ptr(grow, C.c_double),
         _ptr(gcore, C.c_double), _ptr(res, C.c_double), device)
@@ -449,20 +461,21 @@ def _compute_gradient(kernel: int, x, core, rows, lambda_reg, counts, nnz_total,
 
 
 def compute_gradient(x, core, rows, lambda_reg, counts, nnz_total, with_core=True,
-                     device=0):
+                     device=0, ranks=None, cp=False):
     """Batched compute_gradient (include/cmtf/gradients.hpp:59-64).
 
     x: (n,), rows: (n, sum J) concatenated mode rows, counts: (n, N).
-    Returns (row_grads (n, sumJ), core_grads (n, prod J), residuals (n,))."""
+    cp: a CP core given as its superdiagonal (with `ranks`).
+    Returns (row_grads (n, sumJ), core_grads (n, prod J | J), residuals (n,))."""
     return _compute_gradient(_abi.KERNEL_NAIVE, x, core, rows, lambda_reg, counts,
-                             nnz_total, with_core, device)
+                             nnz_total, with_core, device, ranks, cp)
 
 
 def compute_gradient_opt(x, core, rows, lambda_reg, counts, nnz_total, with_core=True,
-                         device=0):
+                         device=0, ranks=None, cp=False):
     """Batched compute_gradient_opt (include/cmtf/gradients.hpp:69-74)."""
     return _compute_gradient(_abi.KERNEL_OPT, x, core, rows, lambda_reg, counts,
-                             nnz_total, with_core, device)
+                             nnz_total, with_core, device, ranks, cp)
 
 
 def matrix_entry_gradients(y, u, v, lambda_m, lambda_reg, col_count, device=0):

@@ -145,6 +145,15 @@ struct cmtf_gpu_ctx {
   uint64_t posA = 1, posB = 0;
   uint4* mrec_alt = nullptr;
   uint64_t mrec_alt_cap = 0;
+  // hog3tm: per record {lambda/count_1(i1), lambda/count_2(i2),
+  // lambda/count_3(i3), 0}, stored beside rec in the same order (a streamed
+  // 16-byte read instead of three random 4-byte lookups per entry: each of
+  // those costs a full L2 fill once the count arrays miss L2), permuted with
+  // rec by the per-epoch reshuffle
+  float4* rrec = nullptr;
+  float4* rrec_alt = nullptr;
+  uint64_t rrec_cap = 0, rrec_alt_cap = 0;
+  bool rrec_valid = false;
   // the next epoch's gathers run on a side stream, overlapping the current
   // sweep (they only read rec / mrec and write the spare buffers)
   cudaStream_t side = nullptr;
@@ -193,6 +202,7 @@ struct cmtf_gpu_ctx {
   int v2_nw = 8;
   int v2_e = 2;
   size_t v2_smem = 0;
+  uint32_t tm_stage_off = 0;  // hog3tm bulk row-step staging (floats; 0 = REDs)
 
   // DSGD: replicated parameters, global sizes, communicator
   uint64_t nnz_global = 0;  // 0 = local nnz
@@ -222,6 +232,7 @@ struct cmtf_gpu_ctx {
     int v2_shape = 0;      // CMTF_V2_SHAPE: 1 = "8x1", 2 = "8x2"
     bool hot_host = false; // CMTF_HOT_HOST: host hot-row selection
     bool hot_check = false;// CMTF_HOT_CHECK: compare device vs host selection
+    bool tm_red = false;   // CMTF_TM_RED=1: hog3tm cold-row steps as REDs (no bulk staging)
   } env;
   int hog_threads_used = 0;
 
@@ -438,6 +449,16 @@ __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
     reg[i] = count[i] ? lambda / (float)count[i] : 0.f;
 }
 
+// rrec[p] = the three regulariser coefficients of record p (order 3)
+__global__ void build_rrec_kernel(const uint4* rec, uint64_t n, const float* r0, const float* r1,
+                                  const float* r2, float4* out) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 r = rec[p];
+    out[p] = make_float4(__ldg(r0 + r.x), __ldg(r1 + r.y), __ldg(r2 + r.z), 0.f);
+  }
+}
+
 constexpr uint32_t kPackHistCols = 8192;
 // Entries [e_lo, e_hi) of a matrix upload; perm_n > 0: each record goes
 // straight to its place p = (pa * e + pb) mod perm_n of the entry order.
@@ -587,6 +608,12 @@ CoreShape core_shape(const cmtf_gpu_ctx* ctx) {
   }
   cs.off[ctx->order] = off;
   cs.size = (uint32_t)ctx->core_size();
+  cs.cp = ctx->cfg.core_structure == 1;
+  cs.dstep = 0;
+  for (int n = ctx->order - 1, st = 1; n >= 0; --n) {
+    cs.dstep += (uint32_t)st;
+    st *= (int)ctx->ranks[n];
+  }
   return cs;
 }
 
@@ -1297,6 +1324,17 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
     mrec_hot_flags_kernel<<<grid_for(ctx->mnnz), 256, 0, ctx->stream>>>(ctx->mrec, ctx->mnnz, f);
     CU(cudaGetLastError());
   }
+  // hog3tm: per-thread staging rows for the bulk asynchronous row steps
+  // (3 rows x JP floats per thread) when they fit beside the hot replicas
+  ctx->tm_stage_off = 0;
+  if (tm3 && !ctx->cfg.nonnegative && !ctx->env.tm_red) {
+    const uint32_t so = (off + 3) & ~3u;
+    const size_t need = (size_t)(so + 256 * 3 * JP) * sizeof(float);
+    if (need <= limit) {
+      ctx->tm_stage_off = so;
+      off = so + 256 * 3 * JP;
+    }
+  }
   ctx->v2_smem = (size_t)off * sizeof(float);
   // hog3tm allocates all 512 TMEM columns: keep it at one block per SM
   if (tm3) ctx->v2_smem = std::max<size_t>(ctx->v2_smem, 116 * 1024);
@@ -1416,10 +1454,23 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   Hog3v2Args a{};
   a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
   if (!fill_sweep_args<3>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
+  if (v3_tm(ctx) && !ctx->rrec_valid) {
+    // built from this epoch's record order (no gather of the next order is
+    // pending here; from now on the reshuffle keeps rrec aligned with rec)
+    TRY(ensure(ctx, &ctx->rrec, &ctx->rrec_cap, ctx->nnz));
+    build_rrec_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const uint4*>(ctx->rec), ctx->nnz, ctx->reg[0], ctx->reg[1],
+        ctx->reg[2], ctx->rrec);
+    CU(cudaGetLastError());
+    ctx->rrec_valid = true;
+    ctx->last_launches += 1;
+  }
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
   if (v3_tm(ctx)) {
+    a.rrec = ctx->rrec + t_lo;
+    a.stage_off = ctx->tm_stage_off;
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
@@ -1595,9 +1646,13 @@ int validate_config(const cmtf_gpu_config* c) {
     return set_err(nullptr, CMTF_EUNSUPPORTED,
                    "core of %llu elements exceeds device limit %d",
                    (unsigned long long)size, kMaxCore);
-  if (c->core_structure != 0)
-    return set_err(nullptr, CMTF_EUNSUPPORTED,
-                   "CP core structure is not implemented on the device yet");
+  if (c->core_structure != 0 && c->core_structure != 1)
+    return set_err(nullptr, CMTF_EVALIDATION, "unknown core structure %d", c->core_structure);
+  // validate_config (src/trainer.cpp:69-72)
+  if (c->core_structure == 1)
+    for (int n = 1; n < c->order; ++n)
+      if (c->ranks[n] != c->ranks[0])
+        return set_err(nullptr, CMTF_EVALIDATION, "CP mode requires equal ranks on every mode");
   // src/trainer.cpp:79-91
   if (!(c->eta0 >= 0)) return set_err(nullptr, CMTF_EVALIDATION, "eta0 must be nonnegative");
   if (!(c->mu >= 0)) return set_err(nullptr, CMTF_EVALIDATION, "mu must be nonnegative");
@@ -1643,7 +1698,7 @@ const char* cmtf_gpu_last_error(void) { return g_last_error.c_str(); }
 const char* cmtf_gpu_ctx_error(const cmtf_gpu_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();
 }
-int32_t cmtf_gpu_abi_version(void) { return 1; }
+int32_t cmtf_gpu_abi_version(void) { return 2; }
 
 int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
   cmtf_gpu_ctx* ctx = nullptr;
@@ -1659,6 +1714,8 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
     return set_err(nullptr, CMTF_EVALIDATION, "device %d out of range", cfg->device);
   ctx = new cmtf_gpu_ctx();
   ctx->cfg = *cfg;
+  // CP cores run on the generic kernels (dense storage, superdiagonal steps)
+  if (cfg->core_structure == 1) ctx->cfg.force_generic = 1;
   ctx->order = cfg->order;
   ctx->ranks.assign(cfg->ranks, cfg->ranks + cfg->order);
   ctx->cfg.ranks = ctx->ranks.data();
@@ -1675,6 +1732,10 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.v2_shape = std::string(v) == "8x1" ? 1 : std::string(v) == "8x2" ? 2 : 0;
     ctx->env.hot_host = std::getenv("CMTF_HOT_HOST") != nullptr;
     ctx->env.hot_check = std::getenv("CMTF_HOT_CHECK") != nullptr;
+    {
+      const char* v = std::getenv("CMTF_TM_RED");
+      ctx->env.tm_red = v && v[0] == '1';
+    }
   }
   auto cleanup = [&](int rc) {
     delete ctx;
@@ -1717,6 +1778,8 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->pos);
   dfree(ctx->rec_alt);
   dfree(ctx->mrec_alt);
+  dfree(ctx->rrec);
+  dfree(ctx->rrec_alt);
   dfree(ctx->s_idx);
   dfree(ctx->s_vals);
   dfree(ctx->s_rec);
@@ -1857,6 +1920,31 @@ int entry_error(cmtf_gpu_ctx* ctx, const char* what, const uint32_t* d_idx, int 
                        what, n + 1, tup[n] + 1, dims[n]);
   }
   return set_err(ctx, CMTF_EVALIDATION, "%s value is not finite", what);
+}
+
+// An upload source that already lives on this context's device is read in
+// place (no staging copy); host (pageable or pinned) and other devices' memory
+// goes through the chunked staging copy.
+bool on_device(const cmtf_gpu_ctx* ctx, const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device == ctx->device;
+}
+
+// The upload staging (up to ~45 bytes per entry: 45 GB at 1e9 entries) is
+// released after every upload instead of living with the context.
+void release_staging(cmtf_gpu_ctx* ctx) {
+  cudaStreamSynchronize(ctx->side);
+  cudaStreamSynchronize(ctx->stream);
+  dfree(ctx->s_idx);
+  dfree(ctx->s_vals);
+  dfree(ctx->s_rec);
+  dfree(ctx->s_keys);
+  dfree(ctx->s_ids);
+  ctx->s_idx_cap = ctx->s_vals_cap = ctx->s_rec_cap = ctx->s_keys_cap = ctx->s_ids_cap = 0;
 }
 
 // 0: no duplicate; else writes the duplicated tuple (0-based) to *tuple.
@@ -2044,6 +2132,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   const bool same_shape =
       ctx->dims.size() == (size_t)N && std::equal(ctx->dims.begin(), ctx->dims.end(), dims);
   drain_side(ctx);  // a pending reshuffle reads rec
+  ctx->rrec_valid = false;
   ctx->dims.assign(dims, dims + N);
   ctx->nnz = nnz;
   ctx->v2_dirty = true;
@@ -2056,26 +2145,34 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   ctx->sort_mode = sm;
 
-  TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * N));
-  TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
-  TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * (N + 1)));
-  TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
-  TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
-  uint32_t* d_idx = ctx->s_idx;
-  double* d_vals = ctx->s_vals;
+  const bool in_place = on_device(ctx, idx) && on_device(ctx, vals);
+  const bool sorted_order = ctx->cfg.order_policy == 0;  // sorted order needs keys + a gather
+  if (!in_place) {
+    TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * N));
+    TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
+  }
+  if (sorted_order) {
+    TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * (N + 1)));
+    TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
+    TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
+  }
+  const uint32_t* d_idx = in_place ? idx : ctx->s_idx;
+  const double* d_vals = in_place ? vals : ctx->s_vals;
   uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
-  // cudaMemcpyDefault: host (pageable or pinned) or device source (UVA).
-  // The copies run in chunks on the side stream; each chunk is packed on the
-  // main stream as soon as it lands (H2D overlaps validation and packing).
+  // Host (pageable or pinned) or another device's memory: the copies run in
+  // chunks on the side stream; each chunk is packed on the main stream as
+  // soon as it lands (H2D overlaps validation and packing).
   constexpr int kChunks = 4;
   const uint64_t chunk = (nnz + kChunks - 1) / kChunks;
   for (int k = 0; k < kChunks; ++k) {
     const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
     if (c0 >= c1) break;
-    CU(cudaMemcpyAsync(d_idx + c0 * N, idx + c0 * N, (c1 - c0) * N * sizeof(uint32_t),
-                       cudaMemcpyDefault, ctx->side));
-    CU(cudaMemcpyAsync(d_vals + c0, vals + c0, (c1 - c0) * sizeof(double), cudaMemcpyDefault,
-                       ctx->side));
+    if (!in_place) {
+      CU(cudaMemcpyAsync(ctx->s_idx + c0 * N, idx + c0 * N, (c1 - c0) * N * sizeof(uint32_t),
+                         cudaMemcpyDefault, ctx->side));
+      CU(cudaMemcpyAsync(ctx->s_vals + c0, vals + c0, (c1 - c0) * sizeof(double),
+                         cudaMemcpyDefault, ctx->side));
+    }
     CU(cudaEventRecord(ctx->cev[k], ctx->side));
   }
   for (int n = 0; n < N; ++n) {
@@ -2114,15 +2211,19 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   if (bad[0] != ~0ull || bad[1] != ~0ull) {
     dfree(ctx->rec);
     ctx->rec_cap = 0;
-    return entry_error(ctx, "tensor", d_idx, N, dims, bad);
+    const int rc = entry_error(ctx, "tensor", d_idx, N, dims, bad);
+    release_staging(ctx);
+    return rc;
   }
   {
     std::vector<uint32_t> tup;
     bool dup = false;
-    TRY(find_duplicate(ctx, d_idx, nnz, N, dims, &tup, &dup));
-    if (dup) {
+    const int rc = find_duplicate(ctx, d_idx, nnz, N, dims, &tup, &dup);
+    if (rc || dup) {
       dfree(ctx->rec);
       ctx->rec_cap = 0;
+      release_staging(ctx);
+      if (rc) return rc;
       return set_err(ctx, CMTF_EVALIDATION, "%s", dup_message("tensor", tup).c_str());
     }
   }
@@ -2143,6 +2244,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->stream));
   if (sorted_ids) cudaFree(sorted_ids);
+  release_staging(ctx);
   // model buffers (allocated with the bundle's shapes; kept on re-upload of a
   // same-shaped bundle, as run_epoch(state, bundle) keeps the state's model)
   if (!same_shape || !ctx->G) {
@@ -2211,13 +2313,18 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
   M.weight = weight;
   CU(cudaMemsetAsync(M.count, 0, cols * sizeof(uint32_t), ctx->stream));
   if (nnz > 0) {
-    TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * 2));
-    TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
-    TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * 3));
-    TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
-    TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
-    uint32_t* d_idx = ctx->s_idx;
-    double* d_vals = ctx->s_vals;
+    const bool in_place = on_device(ctx, idx) && on_device(ctx, vals);
+    if (!in_place) {
+      TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * 2));
+      TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
+    }
+    if (ctx->cfg.order_policy == 0) {
+      TRY(ensure(ctx, &ctx->s_rec, &ctx->s_rec_cap, nnz * 3));
+      TRY(ensure(ctx, &ctx->s_keys, &ctx->s_keys_cap, nnz));
+      TRY(ensure(ctx, &ctx->s_ids, &ctx->s_ids_cap, nnz));
+    }
+    const uint32_t* d_idx = in_place ? idx : ctx->s_idx;
+    const double* d_vals = in_place ? vals : ctx->s_vals;
     uint32_t *d_rec = ctx->s_rec, *d_keys = ctx->s_keys, *d_ids = ctx->s_ids;
     // chunked H2D on the side stream, each chunk packed as it lands; random
     // and caller orders pack straight into the entry order (no scatter pass)
@@ -2232,10 +2339,12 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     for (int k = 0; k < kChunks; ++k) {
       const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
       if (c0 >= c1) break;
-      CU(cudaMemcpyAsync(d_idx + 2 * c0, idx + 2 * c0, (c1 - c0) * 2 * sizeof(uint32_t),
-                         cudaMemcpyDefault, ctx->side));
-      CU(cudaMemcpyAsync(d_vals + c0, vals + c0, (c1 - c0) * sizeof(double), cudaMemcpyDefault,
-                         ctx->side));
+      if (!in_place) {
+        CU(cudaMemcpyAsync(ctx->s_idx + 2 * c0, idx + 2 * c0, (c1 - c0) * 2 * sizeof(uint32_t),
+                           cudaMemcpyDefault, ctx->side));
+        CU(cudaMemcpyAsync(ctx->s_vals + c0, vals + c0, (c1 - c0) * sizeof(double),
+                           cudaMemcpyDefault, ctx->side));
+      }
       CU(cudaEventRecord(ctx->cev[k], ctx->side));
     }
     CU(cudaMemsetAsync(ctx->d_first, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
@@ -2261,19 +2370,23 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
       dfree(M.rec);
       dfree(M.pos);
       const uint32_t mdims[2] = {rows, cols};
-      return entry_error(ctx, "matrix", d_idx, 2, mdims, bad);
+      const int rc = entry_error(ctx, "matrix", d_idx, 2, mdims, bad);
+      release_staging(ctx);
+      return rc;
     }
     {
       std::vector<uint32_t> tup;
       bool dup = false;
       const uint32_t mdims[2] = {rows, cols};
-      TRY(find_duplicate(ctx, d_idx, nnz, 2, mdims, &tup, &dup));
-      if (dup) {
+      const int rc = find_duplicate(ctx, d_idx, nnz, 2, mdims, &tup, &dup);
+      if (rc || dup) {
         dfree(M.count);
         dfree(M.vreg);
         dfree(M.V);
         dfree(M.rec);
         dfree(M.pos);
+        release_staging(ctx);
+        if (rc) return rc;
         return set_err(ctx, CMTF_EVALIDATION, "%s", dup_message("matrix", tup).c_str());
       }
     }
@@ -2286,6 +2399,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));
     if (sorted_ids) cudaFree(sorted_ids);
+    release_staging(ctx);
   }
   reg_kernel<<<grid_for(cols), 256, 0, ctx->stream>>>(
       M.count, cols, (float)(weight * ctx->cfg.lambda_reg), M.vreg);
@@ -2296,16 +2410,57 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
   return CMTF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// The core as the caller sees it (CoreTensor::stored(), include/cmtf/tucker.hpp):
+// dense, or for a CP core its ranks[0] superdiagonal values; on the device
+// it is always dense (off-diagonal zeros).
+uint64_t stored_core_size(const cmtf_gpu_ctx* ctx) {
+  return ctx->cfg.core_structure == 1 ? ctx->ranks[0] : ctx->core_size();
+}
+uint64_t cp_step(const cmtf_gpu_ctx* ctx) {
+  uint64_t step = 0, st = 1;
+  for (int n = ctx->order - 1; n >= 0; --n) {
+    step += st;
+    st *= ctx->ranks[n];
+  }
+  return step;
+}
+std::vector<float> dense_core(const cmtf_gpu_ctx* ctx, const double* stored) {
+  std::vector<float> c(ctx->core_size(), 0.f);
+  if (ctx->cfg.core_structure == 1) {
+    const uint64_t step = cp_step(ctx);
+    for (uint32_t k = 0; k < ctx->ranks[0]; ++k) c[k * step] = (float)stored[k];
+  } else {
+    for (size_t d = 0; d < c.size(); ++d) c[d] = (float)stored[d];
+  }
+  return c;
+}
+void stored_core(const cmtf_gpu_ctx* ctx, const std::vector<float>& dense, double* out) {
+  if (ctx->cfg.core_structure == 1) {
+    const uint64_t step = cp_step(ctx);
+    for (uint32_t k = 0; k < ctx->ranks[0]; ++k) out[k] = dense[k * step];
+  } else {
+    for (size_t d = 0; d < dense.size(); ++d) out[d] = dense[d];
+  }
+}
+}  // namespace
+
+extern "C" {
+
 // random_model (src/trainer.cpp:30-58) with make_rng(seed, Init)
-// (src/trainer.cpp:100); uploaded as f32 with zeroed row padding.
+// (src/trainer.cpp:100); uploaded as f32 with zeroed row padding.  The core
+// draws cover its stored values (a CP core: ranks[0] of them).
 int cmtf_gpu_make_state(cmtf_gpu_ctx* ctx) {
   if (!ctx) return set_err(nullptr, CMTF_EVALIDATION, "null context");
   if (!ctx->rec) return set_err(ctx, CMTF_EVALIDATION, "no training tensor set");
   CU(cudaSetDevice(ctx->device));
   auto rng = make_rng(ctx->cfg.seed, 0x01, 0);
   const double scale = ctx->cfg.init_scale;
-  std::vector<float> core(ctx->core_size());
-  for (auto& g : core) g = (float)(0.0 + (scale - 0.0) * uniform01(rng));
+  std::vector<double> drawn(stored_core_size(ctx));
+  for (auto& g : drawn) g = (double)(float)(0.0 + (scale - 0.0) * uniform01(rng));
+  const std::vector<float> core = dense_core(ctx, drawn.data());
   CU(cudaMemcpyAsync(ctx->G, core.data(), core.size() * sizeof(float),
                      cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -2336,8 +2491,7 @@ int cmtf_gpu_set_model(cmtf_gpu_ctx* ctx, const double* core,
   // the context streams are non-blocking: no kernel may still read the model
   CU(cudaStreamSynchronize(ctx->stream));
   CU(cudaStreamSynchronize(ctx->side));
-  std::vector<float> c(ctx->core_size());
-  for (size_t d = 0; d < c.size(); ++d) c[d] = (float)core[d];
+  const std::vector<float> c = dense_core(ctx, core);
   CU(cudaMemcpy(ctx->G, c.data(), c.size() * sizeof(float), cudaMemcpyHostToDevice));
   auto put = [&](float* dst, const double* src, uint32_t rows, uint32_t J,
                  uint32_t JP) -> int {
@@ -2364,7 +2518,7 @@ int cmtf_gpu_get_model(cmtf_gpu_ctx* ctx, double* core, double* const* factors,
   if (core) {
     std::vector<float> c(ctx->core_size());
     CU(cudaMemcpy(c.data(), ctx->G, c.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    for (size_t d = 0; d < c.size(); ++d) core[d] = c[d];
+    stored_core(ctx, c, core);
   }
   auto get = [&](double* dst, const float* src, uint32_t rows, uint32_t J,
                  uint32_t JP) -> int {
@@ -2440,6 +2594,11 @@ int launch_tensor_gather(cmtf_gpu_ctx* ctx, uint64_t epoch, cudaStream_t st, uin
     case 9: launch_reshuffle<9>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
     default: return set_err(ctx, CMTF_EUNSUPPORTED, "order %d", ctx->order);
   }
+  if (ctx->rrec_valid) {
+    TRY(ensure(ctx, &ctx->rrec_alt, &ctx->rrec_alt_cap, n));
+    launch_reshuffle<4>(reinterpret_cast<const uint32_t*>(ctx->rrec),
+                        reinterpret_cast<uint32_t*>(ctx->rrec_alt), n, *a, *b, st);
+  }
   CU(cudaGetLastError());
   return CMTF_OK;
 }
@@ -2483,6 +2642,10 @@ int take_tensor_order(cmtf_gpu_ctx* ctx) {
   }
   std::swap(ctx->rec, ctx->rec_alt);
   std::swap(ctx->rec_cap, ctx->rec_alt_cap);
+  if (ctx->rrec_valid) {  // permuted by the same gather
+    std::swap(ctx->rrec, ctx->rrec_alt);
+    std::swap(ctx->rrec_cap, ctx->rrec_alt_cap);
+  }
   // the group at old position G moves to a^-1 (G - b)
   const uint64_t ai = inv_mod(a, ng);
   ctx->posA = mulmod(ai, ctx->posA, ng);
@@ -2705,6 +2868,8 @@ int cmtf_gpu_set_counts(cmtf_gpu_ctx* ctx, int32_t which, const uint32_t* counts
   }
   CU(cudaStreamSynchronize(ctx->stream));  // non-blocking stream: prior readers done
   CU(cudaMemcpy(dst, counts, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  drain_side(ctx);
+  if (which < ctx->order) ctx->rrec_valid = false;
   reg_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(dst, n, lam, reg);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->stream));
@@ -3108,6 +3273,8 @@ int finalize_nonnegative(cmtf_gpu_ctx* ctx, double* core, double* const* factors
     vp[m] = V[m].data();
   }
   TRY(cmtf_gpu_get_model(ctx, G.data(), fp.data(), vp.empty() ? nullptr : vp.data()));
+  const bool cp = ctx->cfg.core_structure == 1;
+  if (cp) G.resize(ctx->ranks[0]);  // the stored superdiagonal (src/trainer.cpp:370-371)
   auto clamp = [](std::vector<double>& v) {
     for (double& x : v)
       if (x < 0) x = 0;
@@ -3125,9 +3292,13 @@ int finalize_nonnegative(cmtf_gpu_ctx* ctx, double* core, double* const* factors
       if (nsq == 0.0) continue;  // absorbed as norm 1
       const double norm = std::sqrt(nsq);
       for (uint64_t i = 0; i < ctx->dims[n]; ++i) F[n][i * J + k] /= norm;
-      const uint64_t block = stride * J;
-      for (uint64_t base = 0; base < G.size(); base += block)
-        for (uint64_t t = 0; t < stride; ++t) G[base + k * stride + t] *= norm;
+      if (cp) {
+        G[k] *= norm;
+      } else {
+        const uint64_t block = stride * J;
+        for (uint64_t base = 0; base < G.size(); base += block)
+          for (uint64_t t = 0; t < stride; ++t) G[base + k * stride + t] *= norm;
+      }
       for (size_t m = 0; m < ctx->mats.size(); ++m)
         if (ctx->mats[m].mode == n)
           for (uint64_t i = 0; i < ctx->mats[m].cols; ++i) V[m][i * J + k] *= norm;
@@ -3411,7 +3582,8 @@ int cmtf_gpu_kernel_probe(cmtf_gpu_ctx* ctx, double* xhat, double* residual, dou
 }
 
 int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ranks,
-                              const double* core, uint64_t n, const double* x,
+                              int32_t core_structure, const double* core, uint64_t n,
+                              const double* x,
                               const double* rows, const uint32_t* counts,
                               double lambda_reg, uint64_t nnz_total, int32_t with_core,
                               double* grow, double* gcore, double* residual,
@@ -3435,13 +3607,27 @@ int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ran
     return set_err(nullptr, CMTF_EUNSUPPORTED, "core too large for the device kernels");
   cs.off[order] = off;
   cs.size = (uint32_t)size;
+  const bool cp = core_structure == 1;
+  if (cp)
+    for (int q = 1; q < order; ++q)
+      if (ranks[q] != ranks[0])
+        return set_err(nullptr, CMTF_EVALIDATION, "CP mode requires equal ranks on every mode");
+  cs.cp = cp;
+  cs.dstep = 0;
+  for (int q = order - 1, st = 1; q >= 0; --q) {
+    cs.dstep += (uint32_t)st;
+    st *= (int)ranks[q];
+  }
+  // a CP core is passed as its stored superdiagonal (ranks[0] values) and
+  // returns its gradient the same way (src/gradients.cpp:108-115)
+  const uint64_t stored = cp ? ranks[0] : size;
   for (uint64_t e = 0; e < n * order; ++e)
     if (counts[e] == 0)
       return set_err(nullptr, CMTF_EVALIDATION, "mode counts must be >= 1");
   if (n == 0) return CMTF_OK;
   CU(cudaSetDevice(device));
-  std::vector<float> hcore(size), hrows(n * off), hx(n);
-  for (uint64_t q = 0; q < size; ++q) hcore[q] = (float)core[q];
+  std::vector<float> hcore(size, 0.f), hrows(n * off), hx(n);
+  for (uint64_t q = 0; q < stored; ++q) hcore[cp ? q * cs.dstep : q] = (float)core[q];
   for (uint64_t q = 0; q < n * off; ++q) hrows[q] = (float)rows[q];
   for (uint64_t q = 0; q < n; ++q) hx[q] = (float)x[q];
   float *d_core = nullptr, *d_rows = nullptr, *d_x = nullptr, *d_r = nullptr,
@@ -3494,7 +3680,9 @@ int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ran
     if (residual) residual[q] = hr[q];
   for (uint64_t q = 0; q < n * off; ++q) grow[q] = hg[q];
   if (with_core && gcore)
-    for (uint64_t q = 0; q < hc.size(); ++q) gcore[q] = hc[q];
+    for (uint64_t e = 0; e < n; ++e)
+      for (uint64_t q = 0; q < stored; ++q)
+        gcore[e * stored + q] = hc[e * size + (cp ? q * cs.dstep : q)];
   return CMTF_OK;
 }
 

@@ -26,7 +26,18 @@ struct CoreShape {
   uint32_t J[kMaxOrder];
   uint32_t off[kMaxOrder + 1];  // offsets of each mode's row in a concat
   uint32_t size;                // prod J
+  // CP / hyper-diagonal core (CoreStructure::HyperDiagonalCp, equal ranks):
+  // stored densely with zero off-diagonal elements -- every contraction is
+  // then exactly the CP one -- and only the superdiagonal (d % dstep == 0,
+  // dstep = 1 + J + ... + J^(N-1)) is ever updated
+  int cp;
+  uint32_t dstep;
 };
+
+// Core element d takes steps (every element; CP: the superdiagonal only).
+__device__ __forceinline__ bool core_active(const CoreShape& cs, uint32_t d) {
+  return !cs.cp || d % cs.dstep == 0;
+}
 
 // Decode a linear core index (last mode fastest) into digits.
 __device__ __forceinline__ void decode(const CoreShape& cs, uint32_t d,
@@ -271,6 +282,7 @@ __global__ void serial_epoch_kernel(SerialArgs a) {
       // core step (uses pre-update rows and core)
       uint32_t j[kMaxOrder];
       for (uint32_t d = t; d < cs.size; d += T) {
+        if (!core_active(cs, d)) continue;
         decode(cs, d, j);
         float p = 1.f;
         for (int n = 0; n < cs.order; ++n) p *= u[cs.off[n] + j[n]];
@@ -388,6 +400,7 @@ __global__ void hogwild_generic_kernel(HogArgs a) {
       // block-local core gradient accumulation (pre-update rows)
       uint32_t j[kMaxOrder];
       for (uint32_t d = l; d < cs.size; d += 32) {
+        if (!core_active(cs, d)) continue;  // CP: off-diagonal elements stay 0
         decode(cs, d, j);
         float p = 1.f;
         for (int n = 0; n < cs.order; ++n) p *= u[cs.off[n] + j[n]];

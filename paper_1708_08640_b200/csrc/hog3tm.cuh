@@ -224,6 +224,43 @@ __device__ __forceinline__ void flush_all_hot_staged(const Args& a, float* sm, i
   }
 }
 
+// Cold-row step as one asynchronous bulk reduction (cp.reduce.async.bulk
+// .add.f32) of the row's delta, staged in this thread's shared-memory row:
+// the step leaves the thread at issue (a vector RED keeps its four source
+// registers until the memory pipe takes them, which under scattered L2-missing
+// traffic stalls the next writer of those registers).  Per element the add
+// is atomic, as the RED it replaces (no lost updates on cold rows).  Hot rows
+// and nonnegative mode keep step_row.  The caller waits for the previous
+// entry's reductions to have read the staging (bulk_wait_read) before.
+template <int J, int JP>
+__device__ __forceinline__ void tm_step_row(float* U, uint32_t i, int slot, float* rep, float* stat,
+                                            bool act, const float* u, const float* grad, float eta,
+                                            int nonneg, float curv, float* stage) {
+  if (!act) return;
+  if (slot >= 0 || !stage) {
+    step_row<J, JP>(U, i, slot, rep, stat, u, grad, eta, nonneg, curv);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < JP; k += 4)
+    *reinterpret_cast<float4*>(stage + k) =
+        make_float4(k + 0 < J ? -eta * grad[k] : 0.f, k + 1 < J ? -eta * grad[k + 1] : 0.f,
+                    k + 2 < J ? -eta * grad[k + 2] : 0.f, k + 3 < J ? -eta * grad[k + 3] : 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
+               ::"l"(U + (uint64_t)i * JP), "r"(umma::smem_u32(stage)), "n"(JP * 4)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int J>
 __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   using L = TMLayout<J>;
@@ -326,6 +363,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   }
   uint32_t npush = 0;
   float* myU1 = sU1 + e * JP;
+  // bulk row-step staging: 3 rows of this thread (null: REDs)
+  float* mystage = a.stage_off ? sm + a.stage_off + threadIdx.x * 3 * JP : nullptr;
   // this thread's row in the sweep tiles: K group k at + k * U_LBO
   uint8_t* myU2h = tU2h + e * 16;
   uint8_t* myU2l = tU2l + e * 16;
@@ -382,8 +421,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #pragma unroll
     for (int n = 0; n < 3; ++n) {
       sl[n] = (lo < hi && a.hot[n].slot) ? __ldg(a.hot[n].slot + ix[n]) : -1;
-      rg[n] = lo < hi ? __ldg(a.reg[n] + ix[n]) : 0.f;
     }
+    const float4 r0 = lo < hi ? __ldg(a.rrec + lo) : make_float4(0.f, 0.f, 0.f, 0.f);
+    rg[0] = r0.x;
+    rg[1] = r0.y;
+    rg[2] = r0.z;
   }
   issue_rows(rc, sl, lo < hi);
 
@@ -488,10 +530,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       const bool nxt = e0 + 1 < hi;
       const uint32_t nx[3] = {rc1.x, rc1.y, rc1.z};
 #pragma unroll
-      for (int n = 0; n < 3; ++n) {
+      for (int n = 0; n < 3; ++n)
         nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
-        nrg[n] = __ldg(a.reg[n] + (nxt ? nx[n] : 0u));
-      }
+      // the regulariser coefficients stream beside the records (rrec)
+      const float4 rr = nxt ? __ldg(a.rrec + e0 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      nrg[0] = rr.x;
+      nrg[1] = rr.y;
+      nrg[2] = rr.z;
     }
 
     // ---- this entry's rows (cold ones landed in the tiles) -> fp16 hi/lo ----
@@ -616,22 +661,24 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       if (pr)
 #pragma unroll
         for (int k = 0; k < J; ++k) pr[2 + k] = gr[k];
-      step_row_warp<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0],
-                           (int)a.hot[0].off, active, u1, gr, a.eta, a.nonneg, c1, lane);
+      if (mystage) bulk_wait_read();  // the previous entry's reductions read their staging
+      tm_step_row<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0], active, u1, gr,
+                         a.eta, a.nonneg, c1, mystage);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], rg[1] * u2[k]);
       if (pr)
 #pragma unroll
         for (int k = 0; k < J; ++k) pr[2 + J + k] = gr[k];
-      step_row_warp<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1],
-                           (int)a.hot[1].off, active, u2, gr, a.eta, a.nonneg, c2, lane);
+      tm_step_row<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1], active, u2, gr,
+                         a.eta, a.nonneg, c2, mystage ? mystage + JP : nullptr);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], rg[2] * u3[k]);
       if (pr)
 #pragma unroll
         for (int k = 0; k < J; ++k) pr[2 + 2 * J + k] = gr[k];
-      step_row_warp<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2],
-                           (int)a.hot[2].off, active, u3, gr, a.eta, a.nonneg, c3, lane);
+      tm_step_row<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2], active, u3, gr,
+                         a.eta, a.nonneg, c3, mystage ? mystage + 2 * JP : nullptr);
+      if (mystage) bulk_commit();
     }
 
     TMP(4);
@@ -749,6 +796,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #endif
   if (pend_push || pend_flush) push_flush();
   cp_async_wait_all();
+  if (mystage) bulk_wait_all();
   umma::fence_before();
   __syncthreads();
   flush_all_hot<J, JP, NW>(a, sm, w, lane);

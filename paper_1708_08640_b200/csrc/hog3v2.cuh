@@ -67,6 +67,7 @@ struct MatDesc3 {
 
 struct Hog3v2Args {
   const uint4* rec;     // tensor records {i1, i2, i3, bits(x)}, random order
+  const float4* rrec;   // hog3tm: per record {lambda/count_n(i_n)}, n = 1..3, aligned with rec
   uint64_t nnz;
   const uint4* mrec;    // matrix records {row, col, bits(y), matrix id}
   uint64_t mnnz;        // total over the ranges below
@@ -91,6 +92,7 @@ struct Hog3v2Args {
   // grad u3[J]} and the summed data term of the core gradient (null: off)
   float* probe;
   float* probe_core;
+  uint32_t stage_off;  // hog3tm: shared-memory staging of the bulk row steps (floats; 0 = REDs)
 };
 
 // ---------------------------------------------------------------------

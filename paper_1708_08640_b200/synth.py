@@ -237,3 +237,16 @@ def config3(scale: float = 1.0) -> PlantedSpec:
                        factor_law="ref", noise=0.1,
                        matrices=[MatrixSpec(0, 10_000, int(1e7 * scale))],
                        test_fraction=0.1, seed=0)
+
+
+def config5_small(nnz: int = 1_000_000, rank: int = 10) -> PlantedSpec:
+    """A CPU-reference-sized stand-in for configs[4] (uniform indices on three
+    large modes, planted core + N(0, 0.1), one coupled matrix on mode 1 with
+    10% of the tensor nonzeros): every row has ~nnz / 50_000 observations, so
+    no row is hot and the tcgen05 epoch takes its bulk row-step path, as at
+    full size.  Pins the config-5 kernel path against the reference's own
+    threaded run (tests/golden/config5_small_reference.json)."""
+    return PlantedSpec(dims=[50_000, 50_000, 50_000], nnz=int(nnz), ranks=[rank] * 3,
+                       laws=["uniform"] * 3, factor_law="ref", noise=0.1,
+                       matrices=[MatrixSpec(0, 5_000, int(nnz) // 10)],
+                       test_fraction=0.1, seed=0)

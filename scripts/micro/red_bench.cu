@@ -10,6 +10,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef WORK
+#define WORK 64
+#endif
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16; x *= 0x7feb352d; x ^= x >> 15; x *= 0x846ca68b; x ^= x >> 16;
   return x;
@@ -22,15 +25,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256, 1) k(float* U, uint32_t rows, int per_thread, float* sink) {
-  __shared__ __align__(128) float st[2][256][12];
+template <int MODE, int DEPTH>
+__global__ void __launch_bounds__(256) k(float* U, uint32_t rows, int per_thread, float* sink) {
+  __shared__ __align__(128) float st[DEPTH + 1][256][12];
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   float acc = 0.f;
   for (int i = 0; i < per_thread; ++i) {
     const uint32_t r = hash32(t * 7919u + i * 104729u) % rows;
     float* row = U + (uint64_t)r * 12;
-    const int s = i & 1;
+    const int s = i % (DEPTH + 1);
     float d[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) d[q] = q < 10 ? 1e-6f * (float)(q + i) : 0.f;
@@ -40,7 +43,7 @@ __global__ void __launch_bounds__(256, 1) k(float* U, uint32_t rows, int per_thr
       red_v4(row + 8, make_float4(d[8], d[9], d[10], d[11]));
     } else if (MODE == 1) {
       // the staging row of two iterations ago must have been read
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(DEPTH) : "memory");
 #pragma unroll
       for (int q = 0; q < 12; q += 4)
         *reinterpret_cast<float4*>(&st[s][threadIdx.x][q]) = make_float4(d[q], d[q + 1], d[q + 2], d[q + 3]);
@@ -54,12 +57,12 @@ __global__ void __launch_bounds__(256, 1) k(float* U, uint32_t rows, int per_thr
       for (int q = 0; q < 12; q += 4)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + q * 4), "l"(row + q));
       asm volatile("cp.async.commit_group;");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      acc += st[s ^ 1][threadIdx.x][0];
+      asm volatile("cp.async.wait_group %0;" ::"n"(DEPTH) : "memory");
+      acc += st[(i + 1) % (DEPTH + 1)][threadIdx.x][0];
     }
     // a little independent work between updates (the epoch does ~1.5k instr/entry)
 #pragma unroll 4
-    for (int w = 0; w < 64; ++w) acc = fmaf(acc, 0.999f, d[w % 10]);
+    for (int w = 0; w < WORK; ++w) acc = fmaf(acc, 0.999f, d[w % 10]);
   }
   if (MODE == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (MODE == 2) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -73,26 +76,31 @@ int main() {
   cudaMalloc(&U, (size_t)rows * 48);
   cudaMalloc(&sink, 4);
   cudaMemset(U, 0, (size_t)rows * 48);
-  const int per = 2048, blocks = 148, threads = 256;
-  const double n = (double)blocks * threads * per;
+  const int threads = 256;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char* names[3] = {"red.v4 x3", "cp.reduce.async.bulk 48B", "cp.async gather 3x16B"};
-  for (int mode = 0; mode < 3; ++mode) {
+  auto run = [&](const char* name, auto kern, int bps, int depth) {
+    const int blocks = 148 * bps, per = 2048 / bps;
+    const double n = (double)blocks * threads * per;
+    float ms = 0;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      if (mode == 0) k<0><<<blocks, threads>>>(U, rows, per, sink);
-      if (mode == 1) k<1><<<blocks, threads>>>(U, rows, per, sink);
-      if (mode == 2) k<2><<<blocks, threads>>>(U, rows, per, sink);
+      kern<<<blocks, threads>>>(U, rows, per, sink);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
-      float ms;
       cudaEventElapsedTime(&ms, a, b);
-      if (rep == 2)
-        printf("%-28s %8.3f ms  %.3g rows/s  %s\n", names[mode], ms, n / (ms * 1e-3),
-               cudaGetErrorString(cudaGetLastError()));
     }
+    printf("%-26s blocks/SM %d depth %d: %8.3f ms  %.3g rows/s  %s\n", name, bps, depth, ms,
+           n / (ms * 1e-3), cudaGetErrorString(cudaGetLastError()));
+  };
+  for (int bps : {1, 2, 4}) {
+    run("red.v4 x3", k<0, 1>, bps, 0);
+    run("cp.reduce.async.bulk 48B", k<1, 1>, bps, 1);
+    run("cp.reduce.async.bulk 48B", k<1, 3>, bps, 3);
+    run("cp.async gather 3x16B", k<2, 1>, bps, 1);
+    run("cp.async gather 3x16B", k<2, 3>, bps, 3);
+    run("cp.async gather 3x16B", k<2, 2>, bps, 2);
   }
   return 0;
 }

@@ -6,14 +6,15 @@ from oracle import oracle as O
 from paper_1708_08640_b200 import synth
 p = argparse.ArgumentParser()
 p.add_argument("--scale", type=float, default=1.0)
-p.add_argument("--config", default="config2", choices=["config2", "config3"])
+p.add_argument("--config", default="config2", choices=["config2", "config3", "config5_small"])
 p.add_argument("--epochs", type=int, default=10)
 p.add_argument("--which", default="ref", choices=["ref", "orc"])
 p.add_argument("--workers", type=int, default=8)
 p.add_argument("--lr", type=float, default=1e-3)
 p.add_argument("--lam", type=float, default=0.01)
 a = p.parse_args()
-b, test, _ = synth.generate(getattr(synth, a.config)(a.scale))
+spec = synth.config5_small() if a.config == "config5_small" else getattr(synth, a.config)(a.scale)
+b, test, _ = synth.generate(spec)
 out = {"config": a.config, "scale": a.scale, "which": a.which, "workers": a.workers, "lr": a.lr, "train": [], "test": []}
 if a.which == "ref":
     run = O.RefRun(b, [10, 10, 10], seed=0, eta0=a.lr, mu=0.1, lambda_reg=a.lam, workers=a.workers)

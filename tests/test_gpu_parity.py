@@ -366,6 +366,53 @@ def test_config2_rmse_within_1pct_of_reference(tm, monkeypatch):
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
 
 
+@pytest.mark.parametrize("red", ["0", "1"])
+def test_config5_small_within_1pct_of_reference(red, monkeypatch):
+    """configs[4]'s shape (uniform indices over three large modes, no hot
+    rows, so the tcgen05 epoch steps cold rows with bulk asynchronous
+    reductions from shared memory -- red=0 -- or with vector REDs -- red=1):
+    10 epochs vs the reference's own 8-thread run on the same data
+    (tests/golden/config5_small_reference.json), final RMSE within 1%."""
+    import json
+    import os
+    from conftest import GOLDEN
+    monkeypatch.setenv("CMTF_TM_RED", red)
+    ref = json.load(open(os.path.join(GOLDEN, "config5_small_reference.json")))
+    b, test, _ = synth.generate(synth.config5_small())
+    st = api.make_state(TrainConfig(ranks=[10, 10, 10], eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
+    for _ in range(10):
+        api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == "order3tm"
+    tr = api.epoch_stats(st, 0.01).train_rmse
+    te = api.test_rmse(st, test)
+    assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
+    assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
+
+
+def test_config3_full_scale_within_1pct_of_reference():
+    """BASELINE configs[2] at its stated size: 1e8 nonzeros (Zipf 1.1 over two
+    1e6-row modes, uniform over 1e4), planted 10^3 core + noise, a 1e6 x 1e4
+    coupled matrix with 1e7 nonzeros.  10 epochs of the product kernel on the
+    GPU vs the reference's own 8-thread run on the same data
+    (tests/golden/config3_reference.json, ~25 min of host time): final train
+    and test RMSE within 1%."""
+    import json
+    import os
+    from conftest import GOLDEN
+    ref = json.load(open(os.path.join(GOLDEN, "config3_reference.json")))
+    b, test, _ = synth.generate(synth.config3(1.0))
+    assert b.tensor.nnz == 90_000_000 and b.matrices[0].nnz == 10_000_000
+    st = api.make_state(TrainConfig(ranks=[10, 10, 10], eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
+    trs = []
+    for _ in range(10):
+        api.run_epoch(st)
+    assert st.kernel_info()["kernel"] == "order3tm"
+    tr = api.epoch_stats(st, 0.01).train_rmse
+    te = api.test_rmse(st, test)
+    assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
+    assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
+
+
 @pytest.mark.parametrize("G", [2, 4])
 def test_dsgd_emulated_ranks_within_1pct(G):
     """DSGD with G ranks emulated on one GPU -- the multi-GPU
