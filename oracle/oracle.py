@@ -306,8 +306,9 @@ class RefRun:
 
     def __init__(self, bundle, ranks, seed=0, eta0=1e-3, mu=0.1, lambda_reg=0.1, workers=1,
                  kernel_opt=True, max_epochs=100, rel_tol=1e-4, init_scale=1.0,
-                 nonnegative=False, eval_threads=0):
+                 nonnegative=False, eval_threads=0, cp=False):
         L = ref()
+        self.cp = bool(cp)
         self.L = L
         self.bundle = bundle
         self._keep = _Keep()
@@ -336,7 +337,7 @@ class RefRun:
             raise ValueError(L.ref_last_error().decode())
         self.ranks = k(np.ascontiguousarray(ranks, dtype=np.uint32))
         self.cfg = RefConfig(len(ranks), _p(self.ranks, C.c_uint32), eta0, mu, lambda_reg,
-                             workers, max_epochs, rel_tol, seed, int(kernel_opt), 0,
+                             workers, max_epochs, rel_tol, seed, int(kernel_opt), int(cp),
                              int(nonnegative), init_scale, eval_threads)
         L.ref_state_new.argtypes = [C.c_void_p, C.POINTER(RefConfig)]
         self.s = L.ref_state_new(self.b, C.byref(self.cfg))
@@ -358,6 +359,8 @@ class RefRun:
         self.L.ref_state_get_model.argtypes = [C.c_void_p, f64p, C.POINTER(f64p),
                                                C.POINTER(f64p)]
         self.L.ref_state_get_model(self.s, _p(m.core, C.c_double), fp, vp)
+        if self.cp:  # CoreTensor::stored() of a CP core: the superdiagonal
+            m.core = np.ascontiguousarray(m.core.reshape(-1)[: int(self.ranks[0])])
         return m
 
     def set_model(self, m):

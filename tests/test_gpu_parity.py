@@ -706,3 +706,126 @@ def test_hog3tm_kernel_probe_config2_tile_shapes():
     st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
     api.run_epoch(st)
     _hog3tm_probe_check(st, b, ranks, 0.01, n_oracle=200)
+
+
+# ---------------------------------------------------------------- CP core --
+# CoreStructure::HyperDiagonalCp (src/gradients.cpp:108-115,145-152,192-205,
+# src/tucker.cpp:104-112, src/trainer.cpp:69-72,370-371): on the device the
+# core is stored densely with zero off-diagonal elements and only its
+# superdiagonal takes steps.
+
+@pytest.mark.parametrize("order,J", [(3, 3), (3, 10), (4, 4)])
+@pytest.mark.parametrize("opt", [False, True])
+def test_cp_compute_gradient_matches_oracle(order, J, opt):
+    rng = np.random.default_rng(100 + order * 10 + J)
+    n = 64
+    core = rng.uniform(-1, 1, J)
+    rows = rng.uniform(-1, 1, (n, order * J))
+    for e in range(0, n, 5):  # planted zeros (the opt kernel's fallback paths)
+        rows[e, e % (order * J)] = 0.0
+    x = rng.uniform(-2, 2, n)
+    counts = rng.integers(1, 9, (n, order)).astype(np.uint32)
+    fn = api.compute_gradient_opt if opt else api.compute_gradient
+    grow, gcore, res = fn(x, core, rows, 0.1, counts, 50, ranks=[J] * order, cp=True)
+    assert gcore.shape == (n, J)
+    f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)
+    for e in range(n):
+        rr = [f32(rows[e, k * J:(k + 1) * J]) for k in range(order)]
+        g_ref, c_ref, r_ref = O.compute_gradient(int(opt), float(np.float32(x[e])), f32(core), rr,
+                                                 0.1, counts[e], 50, cp=1, ranks=[J] * order)
+        sc = max(1.0, abs(r_ref)) * (np.abs(core).max() * np.prod(
+            [np.abs(q).max() + 1e-3 for q in rr]) + 0.1)
+        assert abs(res[e] - r_ref) <= 1e-5 * sc
+        assert np.abs(grow[e] - g_ref).max() <= 1e-5 * sc, e
+        assert np.abs(gcore[e] - c_ref).max() <= 1e-5 * sc, e
+
+
+def _cp_bundle(seed=3):
+    spec = synth.config1(literal=False)
+    spec.nnz, spec.dims, spec.seed = 20_000, [300, 250, 200], seed
+    spec.ranks = [4, 4, 4]
+    spec.matrices[0].cols, spec.matrices[0].nnz = 120, 3_000
+    b, test, _ = synth.generate(spec)
+    return b, test
+
+
+def test_cp_initial_model_and_serial_epoch_match_reference():
+    """initialize with a CP core draws only its superdiagonal
+    (src/trainer.cpp:30-58); one serial-order epoch (the reference's exact
+    schedule, P = 1) matches the reference's run_epoch(workers=1) within 1e-4."""
+    b, _ = _cp_bundle()
+    cfg = TrainConfig(ranks=[4, 4, 4], seed=5, eta0=0.01, lambda_reg=0.01, core_structure="cp",
+                      exec_mode="serial")
+    st = api.make_state(cfg, b)
+    ref = O.RefRun(b, [4, 4, 4], seed=5, eta0=0.01, mu=0.1, lambda_reg=0.01, workers=1,
+                   cp=True)
+    m0, r0 = st.model, ref.model()
+    assert m0.core.shape == (4,)
+    assert np.array_equal(m0.core.astype(np.float32), r0.core.astype(np.float32))
+    for a, c in zip(m0.factors, r0.factors):
+        assert np.array_equal(a.astype(np.float32), c.astype(np.float32))
+    ref.set_model(m0)  # start both from the same f32-rounded model
+    for _ in range(2):
+        api.run_epoch(st)
+        ref.run_epoch()
+    m, r = st.model, ref.model()
+    for a, c in zip([m.core] + m.factors + m.couplings, [r.core] + r.factors + r.couplings):
+        assert np.all(np.abs(a - c) <= 1e-4 * np.maximum(np.abs(c), 1e-2 * np.abs(c).max()))
+    ref.close()
+
+
+def test_cp_hogwild_rmse_within_1pct_of_reference():
+    """10 Hogwild epochs with a CP core vs the reference's own threaded run."""
+    b, test = _cp_bundle()
+    cfg = TrainConfig(ranks=[4, 4, 4], seed=0, eta0=0.01, lambda_reg=0.01, core_structure="cp")
+    st = api.make_state(cfg, b)
+    ref = O.RefRun(b, [4, 4, 4], seed=0, eta0=0.01, mu=0.1, lambda_reg=0.01, workers=8, cp=True)
+    for _ in range(10):
+        api.run_epoch(st)
+        ref.run_epoch()
+    tr, tr_ref = api.epoch_stats(st, 0.01).train_rmse, ref.epoch_stats(0.01)[0]
+    te, te_ref = api.test_rmse(st, test), ref.test_rmse(test)
+    ref.close()
+    assert abs(tr - tr_ref) <= 0.01 * tr_ref, (tr, tr_ref)
+    assert abs(te - te_ref) <= 0.01 * te_ref, (te, te_ref)
+    m = st.model
+    assert m.core.shape == (4,)
+
+
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_cp_train_finalisation_matches_reference(nonneg):
+    """train()'s tail for a CP model: finalize_orthogonalize gives a dense
+    core (core_mode_product, src/tucker.cpp:167-206); the nonnegative
+    projection keeps the superdiagonal (src/trainer.cpp:370-371)."""
+    b, _ = _cp_bundle(seed=4)
+    cfg = TrainConfig(ranks=[4, 4, 4], seed=1, eta0=0.01, lambda_reg=0.01, core_structure="cp",
+                      nonnegative=nonneg, max_epochs=2, exec_mode="serial")
+    st = api.make_state(cfg, b)
+    api.run_epoch(st)
+    m = st.model
+    ref = O.RefRun(b, [4, 4, 4], seed=1, eta0=0.01, mu=0.1, lambda_reg=0.01, workers=1, cp=True,
+                   nonnegative=nonneg)
+    ref.set_model(m)
+    ref.finalize(nonneg=nonneg)
+    r = ref.model() if nonneg else None
+    fin = st.finalized_model()
+    if nonneg:
+        assert fin.core.shape == (4,)
+        np.testing.assert_allclose(fin.core, r.core, rtol=1e-9, atol=1e-12)
+        for a, c in zip(fin.factors, r.factors):
+            np.testing.assert_allclose(a, c, rtol=1e-9, atol=1e-12)
+    else:
+        assert fin.core.shape == (4, 4, 4)
+        # predictions preserved by the finalisation
+        idx = b.tensor.indices[:200]
+        def pred(core, F):
+            return np.einsum("abc,na,nb,nc->n", core, F[0][idx[:, 0]], F[1][idx[:, 1]],
+                             F[2][idx[:, 2]])
+        dense = np.zeros((4, 4, 4))
+        for k in range(4):
+            dense[k, k, k] = m.core[k]
+        np.testing.assert_allclose(pred(fin.core, fin.factors), pred(dense, m.factors),
+                                   rtol=1e-9, atol=1e-9)
+        for f in fin.factors:
+            np.testing.assert_allclose(f.T @ f, np.eye(4), atol=1e-9)
+    ref.close()
