@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "cmtf_b200.h")
 
 def header_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(cmtf_gpu_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(cmtf_(?:gpu|coo|model|split)\w*)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():
@@ -46,7 +46,7 @@ def test_library_is_sm100a():
 
 def test_abi_version_and_defaults():
     L = _abi.lib()
-    assert L.cmtf_gpu_abi_version() == 1
+    assert L.cmtf_gpu_abi_version() == 2
     c = _abi.cmtf_gpu_config()
     L.cmtf_gpu_config_default(C.byref(c))
     # TrainConfig member initialisers (include/cmtf/trainer.hpp:18-36)
