@@ -86,8 +86,10 @@ def test_config_validation_matches_reference_messages(cfg, needle):
 def test_unsupported_shapes_are_refused_loudly():
     rc, msg = _create(TrainConfig(ranks=[100, 2, 2]))
     assert rc == _abi.EUNSUPPORTED and "rank" in msg
-    rc, msg = _create(TrainConfig(ranks=[2, 2, 2], core_structure="cp"))
-    assert rc == _abi.EUNSUPPORTED and "CP" in msg
+    # CP cores run on the device; validate_config's equal-rank rule
+    # (src/trainer.cpp:69-72) is checked before touching a device
+    rc, msg = _create(TrainConfig(ranks=[2, 3, 2], core_structure="cp"))
+    assert rc == _abi.EVALIDATION and msg == "CP mode requires equal ranks on every mode"
 
 
 def test_no_cpu_fallback_without_device():
