@@ -96,6 +96,10 @@ typedef struct cmtf_gpu_config {
   float kappa_core;      /* damping of the batched core step; the curvature
                             estimate is the trace E|phi|^2, an upper
                             bound of the top eigenvalue; 0 = default 2.0 */
+  int32_t debug_count_visits; /* TrainConfig::debug_count_visits
+                            (include/cmtf/trainer.hpp:31-32): count every
+                            record visit of the current epoch on the
+                            device (cmtf_gpu_visit_counts)              */
 } cmtf_gpu_config;
 
 typedef struct cmtf_gpu_ctx cmtf_gpu_ctx;
@@ -255,6 +259,15 @@ int cmtf_gpu_sync(cmtf_gpu_ctx *ctx, uint32_t mode_mask, uint32_t mat_mask,
  * emulation of the ranks, used by tests). */
 int cmtf_gpu_sync_local(cmtf_gpu_ctx *const *ctxs, int32_t n, uint32_t mode_mask,
                         uint32_t mat_mask, int32_t core);
+
+/* The exactly-once visit check (TrainState::visit_counts,
+ * include/cmtf/trainer.hpp:55; the reference's test_trainer.cpp:207-219):
+ * visits of the last epoch per training entry (caller order, nnz values) and
+ * per coupled-matrix record of the merged shuffled stream (sum of matrix nnz
+ * values).  Needs debug_count_visits; CMTF_EUNSUPPORTED after a serial-mode
+ * epoch (one thread block replays the schedule; nothing to count). */
+int cmtf_gpu_visit_counts(cmtf_gpu_ctx *ctx, uint32_t *tensor_counts,
+                          uint32_t *matrix_counts);
 
 /* Device-side timing marks on the context's launching stream: record event
  * `slot` (0..7); elapsed milliseconds between two recorded marks. */

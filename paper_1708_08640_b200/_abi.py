@@ -48,6 +48,7 @@ class cmtf_gpu_config(C.Structure):
         ("kernel_version", C.c_int32),
         ("core_flush_every", C.c_int32),
         ("kappa_core", C.c_float),
+        ("debug_count_visits", C.c_int32),
     ]
 
 
@@ -102,6 +103,7 @@ SIGNATURES = [
     ("cmtf_gpu_elapsed_ms", C.c_int, [P, C.c_int32, C.c_int32, f64p]),
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
+    ("cmtf_gpu_visit_counts", C.c_int, [P, u32p, u32p]),
     # text formats and host-side data preparation (io.cpp)
     ("cmtf_coo_parse", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(P)]),
     ("cmtf_coo_order", C.c_int32, [P]),

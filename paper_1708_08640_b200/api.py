@@ -152,6 +152,7 @@ class TrainConfig:
     kernel_version: int = 0  # 0 = auto (v2), 1 = v1
     core_flush_every: int = 0  # 0 = default 1
     kappa_core: float = 0.0  # 0 = default 2.0
+    debug_count_visits: bool = False  # TrainConfig::debug_count_visits (trainer.hpp:31-32)
 
     def to_c(self):
         c = _abi.cmtf_gpu_config()
@@ -175,6 +176,7 @@ class TrainConfig:
         c.hot_tau, c.kappa = self.hot_tau, self.kappa
         c.flush_every, c.kernel_version = self.flush_every, self.kernel_version
         c.core_flush_every = self.core_flush_every
+        c.debug_count_visits = int(self.debug_count_visits)
         c.kappa_core = self.kappa_core
         return c, ranks
 
@@ -316,6 +318,15 @@ class TrainState:
                                                         C.byref(n)))
         return {"tensor_ms": ms[0], "matrix_ms": ms[1], "scan_ms": ms[2],
                 "total_ms": ms[3], "launches": n.value}
+
+    def visit_counts(self):
+        """TrainState::visit_counts of the last epoch: (per training entry in
+        the caller's order, per record of the merged matrix stream)."""
+        t = np.zeros(self.bundle.tensor.nnz, dtype=np.uint32)
+        m = np.zeros(max(1, sum(x.nnz for x in self.bundle.matrices)), dtype=np.uint32)
+        self._check(self._L.cmtf_gpu_visit_counts(self._h, _ptr(t, C.c_uint32),
+                                                  _ptr(m, C.c_uint32)))
+        return t, m[: sum(x.nnz for x in self.bundle.matrices)]
 
     def kernel_info(self):
         w, t, s = C.c_int32(), C.c_int32(), C.c_int32()

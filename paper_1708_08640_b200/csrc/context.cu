@@ -203,6 +203,13 @@ struct cmtf_gpu_ctx {
   int v2_e = 2;
   size_t v2_smem = 0;
   uint32_t tm_stage_off = 0;  // hog3tm bulk row-step staging (floats; 0 = REDs)
+  // debug_count_visits: per tensor record / merged matrix record visit counts
+  // of the current epoch (indexed by record position)
+  uint32_t* visits = nullptr;
+  uint32_t* mvisits = nullptr;
+  uint64_t visits_cap = 0, mvisits_cap = 0;
+  int64_t visits_epoch = -1;
+  bool visits_ok = true;  // every sweep of this epoch ran a counting kernel
 
   // DSGD: replicated parameters, global sizes, communicator
   uint64_t nnz_global = 0;  // 0 = local nnz
@@ -233,6 +240,7 @@ struct cmtf_gpu_ctx {
     bool hot_host = false; // CMTF_HOT_HOST: host hot-row selection
     bool hot_check = false;// CMTF_HOT_CHECK: compare device vs host selection
     bool tm_red = false;   // CMTF_TM_RED=1: hog3tm cold-row steps as REDs (no bulk staging)
+    int tm_strided = 0;    // CMTF_TM_STRIDED=1: hog3tm lanes take strided records
   } env;
   int hog_threads_used = 0;
 
@@ -848,7 +856,8 @@ int scan_nonfinite(cmtf_gpu_ctx* ctx, std::string* offender) {
   return CMTF_OK;
 }
 
-int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M0, float eta, uint64_t lo, uint64_t hi) {
+int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M0, float eta, uint64_t lo, uint64_t hi,
+                 uint32_t* visits = nullptr) {
   DevMatrix M = M0;
   if (hi > M0.nnz) hi = M0.nnz;
   if (hi <= lo) return CMTF_OK;
@@ -865,7 +874,8 @@ int matrix_sweep(cmtf_gpu_ctx* ctx, const DevMatrix& M0, float eta, uint64_t lo,
 #define MS_CASE(JPV)                                                           \
   case JPV:                                                                   \
     matrix_sweep_kernel<JPV><<<blocks, bt, 0, ctx->stream>>>(                   \
-        M.rec, M.nnz, U, M.V, M.vreg, w, eta, ctx->cfg.nonnegative);          \
+        M.rec, M.nnz, U, M.V, M.vreg, w, eta, ctx->cfg.nonnegative,           \
+        visits ? visits + lo : nullptr);                                      \
     break;
   switch (JP) {
     MS_CASE(4) MS_CASE(8) MS_CASE(12) MS_CASE(16) MS_CASE(20) MS_CASE(24)
@@ -1441,6 +1451,8 @@ bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint6
   a.nonneg = ctx->cfg.nonnegative;
   a.probe = ctx->probe;
   a.probe_core = ctx->probe_core;
+  a.visits = ctx->cfg.debug_count_visits ? ctx->visits + t_lo : nullptr;
+  a.mvisits = ctx->cfg.debug_count_visits ? ctx->mvisits : nullptr;
   ctx->hog_threads_used = (int)W;
   return true;
 }
@@ -1471,6 +1483,7 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   if (v3_tm(ctx)) {
     a.rrec = ctx->rrec + t_lo;
     a.stage_off = ctx->tm_stage_off;
+    a.strided = ctx->env.tm_strided;
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
@@ -1539,6 +1552,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t
     a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
     a.nonneg = ctx->cfg.nonnegative;
     ctx->kernel_which = 1;
+    ctx->visits_ok = false;  // the v1 kernel does not count visits
     return launch_hog3(ctx, J, a, opt, ctx->cfg.order_policy == 1 ? 0 : ctx->sort_mode,
                        ctx->cfg.hog_threads);
   }
@@ -1552,6 +1566,7 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t
   a.eta = eta;
   a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
   a.nonneg = ctx->cfg.nonnegative;
+  a.visits = ctx->cfg.debug_count_visits ? ctx->visits + t_lo : nullptr;
   const int bt = 256;
   const size_t smem =
       sizeof(float) * (2 * a.cs.size + (bt / 32) * 2 * a.cs.off[a.cs.order]);
@@ -1735,6 +1750,8 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
     {
       const char* v = std::getenv("CMTF_TM_RED");
       ctx->env.tm_red = v && v[0] == '1';
+      const char* w = std::getenv("CMTF_TM_STRIDED");
+      ctx->env.tm_strided = w && w[0] == '1';
     }
   }
   auto cleanup = [&](int rc) {
@@ -1780,6 +1797,8 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->mrec_alt);
   dfree(ctx->rrec);
   dfree(ctx->rrec_alt);
+  dfree(ctx->visits);
+  dfree(ctx->mvisits);
   dfree(ctx->s_idx);
   dfree(ctx->s_vals);
   dfree(ctx->s_rec);
@@ -2074,6 +2093,7 @@ int cmtf_gpu_check_entries(int32_t device, int32_t order, const uint32_t* dims,
   auto run = [&]() -> int {
     uint32_t* d_idx = nullptr;
     double* d_vals = nullptr;
+    if (on_device(ctx, idx) || on_device(ctx, vals)) CU(cudaDeviceSynchronize());
     TRY(dalloc(ctx, &d_idx, nnz * (uint64_t)order));
     TRY(dalloc(ctx, &d_vals, nnz));
     auto cleanup = [&](int rc) {
@@ -2146,6 +2166,9 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   ctx->sort_mode = sm;
 
   const bool in_place = on_device(ctx, idx) && on_device(ctx, vals);
+  // device-resident inputs may still be written by work on the caller's
+  // streams (the context's streams are non-blocking): wait for the device
+  if (in_place) CU(cudaDeviceSynchronize());
   const bool sorted_order = ctx->cfg.order_policy == 0;  // sorted order needs keys + a gather
   if (!in_place) {
     TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * N));
@@ -2314,6 +2337,7 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
   CU(cudaMemsetAsync(M.count, 0, cols * sizeof(uint32_t), ctx->stream));
   if (nnz > 0) {
     const bool in_place = on_device(ctx, idx) && on_device(ctx, vals);
+    if (in_place) CU(cudaDeviceSynchronize());  // see cmtf_gpu_set_tensor
     if (!in_place) {
       TRY(ensure(ctx, &ctx->s_idx, &ctx->s_idx_cap, nnz * 2));
       TRY(ensure(ctx, &ctx->s_vals, &ctx->s_vals_cap, nnz));
@@ -2710,6 +2734,17 @@ int normalize_pos(cmtf_gpu_ctx* ctx) {
 int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
           const uint64_t* m_hi) {
   const float eta = (float)ctx->eta;
+  if (ctx->cfg.debug_count_visits && ctx->visits_epoch != ctx->epoch) {
+    // a new epoch: fresh counts (the reference fills visit_counts per epoch)
+    uint64_t mtot = 0;
+    for (auto& M : ctx->mats) mtot += M.nnz;
+    TRY(ensure(ctx, &ctx->visits, &ctx->visits_cap, std::max<uint64_t>(1, ctx->nnz)));
+    TRY(ensure(ctx, &ctx->mvisits, &ctx->mvisits_cap, std::max<uint64_t>(1, mtot)));
+    CU(cudaMemsetAsync(ctx->visits, 0, ctx->nnz * sizeof(uint32_t), ctx->stream));
+    CU(cudaMemsetAsync(ctx->mvisits, 0, mtot * sizeof(uint32_t), ctx->stream));
+    ctx->visits_epoch = ctx->epoch;
+    ctx->visits_ok = ctx->cfg.exec_mode != CMTF_EXEC_SERIAL;
+  }
   if (ctx->cfg.exec_mode == CMTF_EXEC_SERIAL) {
     TRY(serial_epoch(ctx, eta));
     ctx->last_launches += 1;
@@ -2738,10 +2773,13 @@ int sweep(cmtf_gpu_ctx* ctx, uint64_t t_lo, uint64_t t_hi, const uint64_t* m_lo,
   TRY(hogwild_tensor_sweep(ctx, eta, t_lo, t_hi));
   ctx->last_launches += 1;
   CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  uint64_t vbase = 0;  // visit counts: the matrices' records concatenated
   for (size_t m = 0; m < ctx->mats.size(); ++m) {
     const auto& M = ctx->mats[m];
     const uint64_t lo = m_lo ? m_lo[m] : 0, hi = m_hi ? m_hi[m] : M.nnz;
-    TRY(matrix_sweep(ctx, M, eta, lo, hi));
+    TRY(matrix_sweep(ctx, M, eta, lo, hi,
+                     ctx->cfg.debug_count_visits ? ctx->mvisits + vbase : nullptr));
+    vbase += M.nnz;
     ctx->last_launches += hi > lo ? 1 : 0;
   }
   CU(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -3059,6 +3097,7 @@ int cmtf_gpu_test_rmse(cmtf_gpu_ctx* ctx, const uint32_t* idx, const double* val
   uint32_t* d_idx = nullptr;
   double* d_vals = nullptr;
   uint32_t *d_rec = nullptr, *d_keys = nullptr, *d_ids = nullptr;
+  if (on_device(ctx, idx) || on_device(ctx, vals)) CU(cudaDeviceSynchronize());
   TRY(dalloc(ctx, &d_idx, nnz * N));
   TRY(dalloc(ctx, &d_vals, nnz));
   TRY(dalloc(ctx, &d_rec, nnz * (N + 1)));
@@ -3730,6 +3769,32 @@ int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double* y,
   }
   for (uint64_t q = 0; q < n; ++q)
     if (residual) residual[q] = hr[q];
+  return CMTF_OK;
+}
+
+int cmtf_gpu_visit_counts(cmtf_gpu_ctx* ctx, uint32_t* tensor_counts, uint32_t* matrix_counts) {
+  TRY(require_bundle(ctx));
+  if (!ctx->cfg.debug_count_visits)
+    return set_err(ctx, CMTF_EVALIDATION, "debug_count_visits is off");
+  if (ctx->visits_epoch < 0) return set_err(ctx, CMTF_EVALIDATION, "no epoch has run");
+  if (!ctx->visits_ok)
+    return set_err(ctx, CMTF_EUNSUPPORTED,
+                   "the epoch ran a kernel without visit counting (serial replay or v1)");
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (tensor_counts && ctx->nnz) {
+    // record position -> the caller's entry id (pos[], through the per-epoch
+    // group map)
+    TRY(normalize_pos(ctx));
+    std::vector<uint32_t> byp(ctx->nnz), pos(ctx->nnz);
+    CU(cudaMemcpy(byp.data(), ctx->visits, ctx->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(pos.data(), ctx->pos, ctx->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (uint64_t id = 0; id < ctx->nnz; ++id) tensor_counts[id] = byp[pos[id]];
+  }
+  uint64_t mtot = 0;
+  for (auto& M : ctx->mats) mtot += M.nnz;
+  if (matrix_counts && mtot)
+    CU(cudaMemcpy(matrix_counts, ctx->mvisits, mtot * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return CMTF_OK;
 }
 

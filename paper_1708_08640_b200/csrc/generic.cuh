@@ -357,6 +357,7 @@ struct HogArgs {
   float eta;
   float core_reg;
   int nonneg;
+  uint32_t* visits;  // debug_count_visits (null: off)
 };
 
 template <bool OPT>
@@ -385,6 +386,7 @@ __global__ void hogwild_generic_kernel(HogArgs a) {
     uint32_t idx[kMaxOrder];
     float r = 0.f;
     if (active) {
+      if (a.visits && l == 0) atomicAdd(a.visits + e, 1u);
       const uint32_t* rp = a.rec + e * (cs.order + 1);
       for (int n = 0; n < cs.order; ++n) idx[n] = rp[n];
       const float x = __uint_as_float(rp[cs.order]);
@@ -440,7 +442,7 @@ template <int JP>
 __global__ void __launch_bounds__(256)
 matrix_sweep_kernel(const uint32_t* rec, uint64_t nnz, float* U,
                     float* V, const float* vreg, float weight, float eta,
-                    int nonneg) {
+                    int nonneg, uint32_t* visits) {
   const uint64_t W = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t lo = nnz * t / W, hi = nnz * (t + 1) / W;
@@ -448,6 +450,7 @@ matrix_sweep_kernel(const uint32_t* rec, uint64_t nnz, float* U,
   uint32_t cur = 0xffffffffu;
   float u[JP];
   for (uint64_t e = lo; e < hi; ++e) {
+    if (visits) atomicAdd(visits + e, 1u);
     const uint3 rr = *reinterpret_cast<const uint3*>(rec + 3 * e);
     if (rr.x != cur) {
       if (cur != 0xffffffffu) {

@@ -342,7 +342,13 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
   const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
   const uint64_t gl = ((uint64_t)blockIdx.x * NW + w) * 32 + lane;
-  const uint64_t lo = a.nnz * gl / Wt, hi = a.nnz * (gl + 1) / Wt;
+  // a lane's entries: a contiguous chunk (st = 1), or -- strided -- every
+  // Wt-th record from its lane id, so that the whole grid sweeps the record
+  // array front to back (an L2-blocked record order then keeps the active
+  // row blocks L2-resident)
+  const uint64_t st = a.strided ? Wt : 1;
+  const uint64_t lo = a.strided ? gl : a.nnz * gl / Wt;
+  const uint64_t hi = a.strided ? a.nnz : a.nnz * (gl + 1) / Wt;
   const uint64_t iters = (a.nnz + Wt - 1) / Wt;
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     *reinterpret_cast<uint4*>(tl + L::U_LBO) = l1;
   };
   uint4 rc = lo < hi ? __ldg(a.rec + lo) : make_uint4(0, 0, 0, 0);
-  uint4 rc1 = lo + 1 < hi ? __ldg(a.rec + lo + 1) : make_uint4(0, 0, 0, 0);
+  uint4 rc1 = lo + st < hi ? __ldg(a.rec + lo + st) : make_uint4(0, 0, 0, 0);
   int sl[3];
   float rg[3];
   {
@@ -520,20 +526,20 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   };
 
   for (uint64_t it = 0; it < iters; ++it) {
-    const uint64_t e0 = lo + it;
+    const uint64_t e0 = lo + it * st;
     const bool active = e0 < hi;
     const uint32_t par = (uint32_t)(it & 1);
-    const uint4 rc2 = e0 + 2 < hi ? __ldg(a.rec + e0 + 2) : make_uint4(0, 0, 0, 0);
+    const uint4 rc2 = e0 + 2 * st < hi ? __ldg(a.rec + e0 + 2 * st) : make_uint4(0, 0, 0, 0);
     int nsl[3];
     float nrg[3];
     {
-      const bool nxt = e0 + 1 < hi;
+      const bool nxt = e0 + st < hi;
       const uint32_t nx[3] = {rc1.x, rc1.y, rc1.z};
 #pragma unroll
       for (int n = 0; n < 3; ++n)
         nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
       // the regulariser coefficients stream beside the records (rrec)
-      const float4 rr = nxt ? __ldg(a.rrec + e0 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 rr = nxt ? __ldg(a.rrec + e0 + st) : make_float4(0.f, 0.f, 0.f, 0.f);
       nrg[0] = rr.x;
       nrg[1] = rr.y;
       nrg[2] = rr.z;
@@ -654,6 +660,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       if (active) {
         lamG += n1 * n2 * n3;
         kw += 1.f;
+        if (a.visits) atomicAdd(a.visits + e0, 1u);
       }
       float gr[J];
 #pragma unroll
@@ -766,7 +773,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     TMP(5);
     // ---- next entry's rows into the tiles (the sweep MMAs are done) ----
-    issue_rows(rc1, nsl, e0 + 1 < hi);
+    issue_rows(rc1, nsl, e0 + st < hi);
 
     TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----

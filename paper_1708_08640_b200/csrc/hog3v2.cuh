@@ -93,6 +93,11 @@ struct Hog3v2Args {
   float* probe;
   float* probe_core;
   uint32_t stage_off;  // hog3tm: shared-memory staging of the bulk row steps (floats; 0 = REDs)
+  // debug_count_visits (include/cmtf/trainer.hpp:31-32): +1 per visit of a
+  // tensor record (indexed like rec) / matrix record (indexed like mrec)
+  uint32_t* visits;
+  uint32_t* mvisits;
+  int strided;  // hog3tm: lanes take every W-th record (grid-wide front-to-back sweep)
 };
 
 // ---------------------------------------------------------------------
@@ -644,6 +649,7 @@ __device__ __forceinline__ void matrix_entries_until_pf(const Args& a, float* sm
       vv[4 * k] = qv.x; vv[4 * k + 1] = qv.y; vv[4 * k + 2] = qv.z; vv[4 * k + 3] = qv.w;
     }
     if (has) {  // advance: the record after next, and the next entry's rows
+      if (a.mvisits) atomicAdd(a.mvisits + mphys(a, mpos), 1u);
       ++mpos;
       p.mr = p.mr2;
       if (mpos + 1 < mhi) p.mr2 = __ldg(a.mrec + mphys(a, mpos + 1));
@@ -679,6 +685,7 @@ __device__ __forceinline__ void matrix_entries_until(const Args& a, float* sm, u
     const bool has = mpos < due;
     const uint4 mr = mrn;  // record prefetched one entry ahead
     if (has) {
+      if (a.mvisits) atomicAdd(a.mvisits + mphys(a, mpos), 1u);
       ++mpos;
       if (mpos < mhi) mrn = __ldg(a.mrec + mphys(a, mpos));
     }
@@ -979,6 +986,7 @@ hog3v2_kernel(Hog3v2Args a) {
       if (active[j]) {
         lamG += n1 * n2 * n3;
         kw += 1.f;
+        if (a.visits) atomicAdd(a.visits + e0 + j, 1u);
       }
       // row steps: every lane of the warp takes part (hot-row aggregation)
       float gr[J];

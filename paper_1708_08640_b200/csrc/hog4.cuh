@@ -50,6 +50,8 @@ struct Hog4Args {
   int nonneg;
   float* probe;       // unused (hog3tm only)
   float* probe_core;
+  uint32_t* visits;   // debug_count_visits: +1 per tensor / matrix record visit
+  uint32_t* mvisits;
 };
 
 template <int J, int NW, bool TC = false>
@@ -163,6 +165,7 @@ hog4_kernel(Hog4Args a) {
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e = lo + it;
     const bool active = e < hi;
+    if (active && a.visits) atomicAdd(a.visits + e, 1u);
     float* stg = stg0 + (it & 1) * L::STAGE_FLOATS;
     float* myst = stg + (w * 32 + lane) * SW;
     const float x = __uint_as_float(xv);

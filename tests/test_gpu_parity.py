@@ -829,3 +829,34 @@ def test_cp_train_finalisation_matches_reference(nonneg):
         for f in fin.factors:
             np.testing.assert_allclose(f.T @ f, np.eye(4), atol=1e-9)
     ref.close()
+
+
+def _visit_cases():
+    c2 = synth.config2(0.02)
+    c4 = synth.config4_small(40_000)
+    c1 = synth.config1(literal=False)
+    return [
+        ("order3tm, hot rows", c2, [10, 10, 10], {}),
+        ("order3tm, bulk row steps", synth.config5_small(200_000), [10, 10, 10], {}),
+        ("order3v2 naive", c2, [10, 10, 10], {"kernel": "naive"}),
+        ("order4", c4, [8, 8, 8, 8], {}),
+        ("generic (CP core)", c1, [5, 5, 5], {"core_structure": "cp"}),
+    ]
+
+
+@pytest.mark.parametrize("case", _visit_cases(), ids=lambda c: c[0])
+def test_every_training_index_is_visited_exactly_once_per_epoch(case):
+    """The reference's debug_count_visits check (test_trainer.cpp:207-219,
+    trainer.cpp:158-161,191) on the device epoch kernels: after each of two
+    epochs (the second with a freshly reshuffled record order) every training
+    entry and every coupled-matrix record was visited exactly once."""
+    name, spec, ranks, extra = case
+    b, _, _ = synth.generate(spec)
+    st = api.make_state(TrainConfig(ranks=ranks, eta0=1e-3, lambda_reg=0.01,
+                                    debug_count_visits=True, **extra), b)
+    for _ in range(2):
+        api.run_epoch(st)
+        t, m = st.visit_counts()
+        assert t.shape[0] == b.tensor.nnz and np.all(t == 1), (name, np.unique(t))
+        assert m.shape[0] == sum(x.nnz for x in b.matrices) and np.all(m == 1), \
+            (name, np.unique(m))
