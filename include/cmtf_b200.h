@@ -205,25 +205,45 @@ int cmtf_gpu_kernel_probe(cmtf_gpu_ctx *ctx, double *xhat, double *residual,
 
 /* Stateless batched form of compute_gradient / compute_gradient_opt
  * (include/cmtf/gradients.hpp:59-74): n independent entries, each with its
- * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core.
- * core_structure 0: dense core (prod J values); 1: CP / hyper-diagonal
- * (src/gradients.cpp:108-115,145-152,192-205): core and each entry's core
- * gradient hold the ranks[0] superdiagonal values, all ranks equal. */
+ * own x, N rows (rows[e*sumJ ...]) and N counts, sharing one core, computed
+ * in f64 on the device (the reference's algorithms term for term, incl.
+ * the opt kernel's 1e-12 divisor fallbacks).  core_structure 0: dense core
+ * (prod J values); 1: CP / hyper-diagonal (src/gradients.cpp:108-115,
+ * 145-152,192-205): core, each entry's core gradient and intermediate tensor
+ * hold the ranks[0] superdiagonal values, all ranks equal.  intermediate
+ * (opt only, may be NULL): KernelWorkspace::s, the intermediate tensor
+ * S[d] = g_d prod_n u_n[j_n] of each entry. */
 int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order,
                               const uint32_t *ranks, int32_t core_structure,
                               const double *core, uint64_t n, const double *x,
                               const double *rows, const uint32_t *counts,
                               double lambda_reg, uint64_t nnz_total,
                               int32_t with_core, double *grow, double *gcore,
-                              double *residual, int32_t device);
+                              double *residual, double *intermediate,
+                              int32_t device);
 
-/* Batched matrix_entry_gradients (include/cmtf/gradients.hpp:83-86). */
+/* Batched matrix_entry_gradients (include/cmtf/gradients.hpp:83-86), f64
+ * on the device like cmtf_gpu_compute_gradient. */
 int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double *y,
                                     const double *u, const double *v,
                                     double lambda_m, double lambda_reg,
                                     const uint32_t *col_count, double *du,
                                     double *dv, double *residual,
                                     int32_t device);
+
+/* collapse (include/cmtf/gradients.hpp:32-34, src/gradients.cpp:35-60) of
+ * an intermediate tensor (prod J values; CP: ranks[0]) along `mode`, f64 on
+ * the device; out has ranks[mode] values. */
+int cmtf_gpu_collapse(int32_t order, const uint32_t *ranks, int32_t core_structure,
+                      const double *values, int32_t mode, double *out,
+                      int32_t device);
+
+/* The next serial-mode epoch replays exactly this schedule (tensor ids
+ * [0, nnz) then matrix entries in bundle order, as build_schedule,
+ * src/trainer.cpp:114-120) instead of shuffling its own persisted copy: a
+ * caller holding TrainState::schedule (shuffle_schedule on the host, as the
+ * reference's run_epoch does) passes it here before cmtf_gpu_run_epoch. */
+int cmtf_gpu_set_schedule(cmtf_gpu_ctx *ctx, const uint64_t *schedule, uint64_t n);
 
 /* ---- DSGD (multi-GPU) support: SURVEY.md 8(e) ----------------------
  * A rank uploads its local bundle grouped by stratum (order_policy 2 keeps

@@ -86,7 +86,7 @@ SIGNATURES = [
     ("cmtf_gpu_kernel_probe", C.c_int, [P, f64p, f64p, f64p, f64p]),
     ("cmtf_gpu_compute_gradient", C.c_int,
      [C.c_int32, C.c_int32, u32p, C.c_int32, f64p, C.c_uint64, f64p, f64p, u32p, C.c_double,
-      C.c_uint64, C.c_int32, f64p, f64p, f64p, C.c_int32]),
+      C.c_uint64, C.c_int32, f64p, f64p, f64p, f64p, C.c_int32]),
     ("cmtf_gpu_matrix_entry_gradients", C.c_int,
      [C.c_uint64, C.c_uint32, f64p, f64p, f64p, C.c_double, C.c_double, u32p, f64p,
       f64p, f64p, C.c_int32]),
@@ -104,6 +104,9 @@ SIGNATURES = [
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
     ("cmtf_gpu_visit_counts", C.c_int, [P, u32p, u32p]),
+    ("cmtf_gpu_collapse", C.c_int, [C.c_int32, u32p, C.c_int32, f64p, C.c_int32, f64p,
+                                    C.c_int32]),
+    ("cmtf_gpu_set_schedule", C.c_int, [P, u64p, C.c_uint64]),
     # text formats and host-side data preparation (io.cpp)
     ("cmtf_coo_parse", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(P)]),
     ("cmtf_coo_order", C.c_int32, [P]),

@@ -466,7 +466,7 @@ def _compute_gradient(kernel: int, x, core, rows, lambda_reg, counts, nnz_total,
         kernel, len(ranks), _ptr(ranks, C.c_uint32), int(cp), _ptr(core, C.c_double), n,
         _ptr(x, C.c_double), _ptr(rows, C.c_double), _ptr(counts, C.c_uint32),
         lambda_reg, nnz_total, int(with_core), _ptr(grow, C.c_double),
-        _ptr(gcore, C.c_double), _ptr(res, C.c_double), device)
+        _ptr(gcore, C.c_double), _ptr(res, C.c_double), None, device)
     _raise(rc, L.cmtf_gpu_last_error().decode())
     return grow, gcore, res
 

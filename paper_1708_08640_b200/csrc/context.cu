@@ -26,6 +26,7 @@
 #include "hog3v2.cuh"
 #include "hog4.cuh"
 #include "hog3tm.cuh"
+#include "stateless64.cuh"
 
 #include "host_rng.hpp"
 
@@ -203,6 +204,7 @@ struct cmtf_gpu_ctx {
   int v2_e = 2;
   size_t v2_smem = 0;
   uint32_t tm_stage_off = 0;  // hog3tm bulk row-step staging (floats; 0 = REDs)
+  bool schedule_given = false;  // cmtf_gpu_set_schedule: replay it next serial epoch
   // debug_count_visits: per tensor record / merged matrix record visit counts
   // of the current epoch (indexed by record position)
   uint32_t* visits = nullptr;
@@ -1551,8 +1553,8 @@ int hogwild_tensor_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t
     a.eta_core = eta;
     a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all_of(ctx));
     a.nonneg = ctx->cfg.nonnegative;
+    a.visits = ctx->cfg.debug_count_visits ? ctx->visits + t_lo : nullptr;
     ctx->kernel_which = 1;
-    ctx->visits_ok = false;  // the v1 kernel does not count visits
     return launch_hog3(ctx, J, a, opt, ctx->cfg.order_policy == 1 ? 0 : ctx->sort_mode,
                        ctx->cfg.hog_threads);
   }
@@ -1598,9 +1600,13 @@ int serial_epoch(cmtf_gpu_ctx* ctx, float eta) {
     ctx->schedule.resize(total);
     for (uint64_t i = 0; i < total; ++i) ctx->schedule[i] = i;
   }
-  auto rng = make_rng(ctx->cfg.seed, 0x02, (uint64_t)ctx->epoch);
-  for (uint64_t i = total; i > 1; --i)
-    std::swap(ctx->schedule[i - 1], ctx->schedule[bounded(rng, i)]);
+  if (ctx->schedule_given) {
+    ctx->schedule_given = false;  // the caller's order for this epoch, as given
+  } else {
+    auto rng = make_rng(ctx->cfg.seed, 0x02, (uint64_t)ctx->epoch);
+    for (uint64_t i = total; i > 1; --i)
+      std::swap(ctx->schedule[i - 1], ctx->schedule[bounded(rng, i)]);
+  }
   if (ctx->d_sched_cap < total) {
     TRY(dalloc(ctx, &ctx->d_sched, total));
     ctx->d_sched_cap = total;
@@ -3622,12 +3628,10 @@ int cmtf_gpu_kernel_probe(cmtf_gpu_ctx* ctx, double* xhat, double* residual, dou
 
 int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ranks,
                               int32_t core_structure, const double* core, uint64_t n,
-                              const double* x,
-                              const double* rows, const uint32_t* counts,
+                              const double* x, const double* rows, const uint32_t* counts,
                               double lambda_reg, uint64_t nnz_total, int32_t with_core,
                               double* grow, double* gcore, double* residual,
-                              int32_t device) {
-  cmtf_gpu_ctx* ctx = nullptr;
+                              double* intermediate, int32_t device) {
   if (order < 1 || order > kMaxOrder)
     return set_err(nullptr, CMTF_EVALIDATION, "kernel argument order mismatch");
   CoreShape cs{};
@@ -3658,71 +3662,82 @@ int cmtf_gpu_compute_gradient(int32_t kernel, int32_t order, const uint32_t* ran
     st *= (int)ranks[q];
   }
   // a CP core is passed as its stored superdiagonal (ranks[0] values) and
-  // returns its gradient the same way (src/gradients.cpp:108-115)
+  // returns its gradient and intermediate tensor the same way
+  // (src/gradients.cpp:108-115,145-152)
   const uint64_t stored = cp ? ranks[0] : size;
   for (uint64_t e = 0; e < n * order; ++e)
     if (counts[e] == 0)
       return set_err(nullptr, CMTF_EVALIDATION, "mode counts must be >= 1");
   if (n == 0) return CMTF_OK;
+  cmtf_gpu_ctx* ctx = nullptr;
   CU(cudaSetDevice(device));
-  std::vector<float> hcore(size, 0.f), hrows(n * off), hx(n);
-  for (uint64_t q = 0; q < stored; ++q) hcore[cp ? q * cs.dstep : q] = (float)core[q];
-  for (uint64_t q = 0; q < n * off; ++q) hrows[q] = (float)rows[q];
-  for (uint64_t q = 0; q < n; ++q) hx[q] = (float)x[q];
-  float *d_core = nullptr, *d_rows = nullptr, *d_x = nullptr, *d_r = nullptr,
-        *d_grow = nullptr, *d_gcore = nullptr;
+  std::vector<double> hcore(size, 0.0);
+  for (uint64_t q = 0; q < stored; ++q) hcore[cp ? q * cs.dstep : q] = core[q];
+  double *d_core = nullptr, *d_rows = nullptr, *d_x = nullptr, *d_r = nullptr,
+         *d_grow = nullptr, *d_gcore = nullptr, *d_inter = nullptr;
   uint32_t* d_counts = nullptr;
-  TRY(dalloc(ctx, &d_core, size));
-  TRY(dalloc(ctx, &d_rows, n * off));
-  TRY(dalloc(ctx, &d_x, n));
-  TRY(dalloc(ctx, &d_r, n));
-  TRY(dalloc(ctx, &d_grow, n * off));
-  TRY(dalloc(ctx, &d_counts, n * order));
-  if (with_core) TRY(dalloc(ctx, &d_gcore, n * size));
-  CU(cudaMemcpy(d_core, hcore.data(), size * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_rows, hrows.data(), n * off * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_x, hx.data(), n * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_counts, counts, n * order * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  ProbeArgs a{};
-  a.cs = cs;
-  a.G = d_core;
-  a.rows = d_rows;
-  a.x = d_x;
-  a.counts = d_counts;
-  a.lambda = (float)lambda_reg;
-  a.n = n;
-  a.core_reg = (float)(lambda_reg / (double)nnz_total);
-  a.with_core = with_core;
-  a.resid = d_r;
-  a.grow = d_grow;
-  a.gcore = d_gcore;
-  const int bt = 128;
-  const size_t smem = sizeof(float) * (bt / 32) * 2 * off;
-  if (kernel == CMTF_KERNEL_OPT)
-    probe_kernel<true><<<grid_for(n, bt / 32), bt, smem>>>(a);
-  else
-    probe_kernel<false><<<grid_for(n, bt / 32), bt, smem>>>(a);
-  CU(cudaGetLastError());
-  std::vector<float> hr(n), hg(n * off), hc(with_core ? n * size : 0);
-  CU(cudaMemcpy(hr.data(), d_r, n * sizeof(float), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(hg.data(), d_grow, n * off * sizeof(float), cudaMemcpyDeviceToHost));
-  if (with_core)
-    CU(cudaMemcpy(hc.data(), d_gcore, hc.size() * sizeof(float), cudaMemcpyDeviceToHost));
-  cudaFree(d_core);
-  cudaFree(d_rows);
-  cudaFree(d_x);
-  cudaFree(d_r);
-  cudaFree(d_grow);
-  cudaFree(d_counts);
-  if (d_gcore) cudaFree(d_gcore);
-  for (uint64_t q = 0; q < n; ++q)
-    if (residual) residual[q] = hr[q];
-  for (uint64_t q = 0; q < n * off; ++q) grow[q] = hg[q];
-  if (with_core && gcore)
+  auto cleanup = [&]() {
+    cudaFree(d_core);
+    cudaFree(d_rows);
+    cudaFree(d_x);
+    cudaFree(d_r);
+    cudaFree(d_grow);
+    cudaFree(d_counts);
+    if (d_gcore) cudaFree(d_gcore);
+    if (d_inter) cudaFree(d_inter);
+  };
+  auto run = [&]() -> int {
+    TRY(dalloc(ctx, &d_core, size));
+    TRY(dalloc(ctx, &d_rows, n * off));
+    TRY(dalloc(ctx, &d_x, n));
+    TRY(dalloc(ctx, &d_r, n));
+    TRY(dalloc(ctx, &d_grow, n * off));
+    TRY(dalloc(ctx, &d_counts, n * order));
+    if (with_core) TRY(dalloc(ctx, &d_gcore, n * size));
+    if (intermediate && kernel == CMTF_KERNEL_OPT) TRY(dalloc(ctx, &d_inter, n * size));
+    CU(cudaMemcpy(d_core, hcore.data(), size * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_rows, rows, n * off * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_x, x, n * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_counts, counts, n * order * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    Probe64Args a{};
+    a.cs = cs;
+    a.G = d_core;
+    a.rows = d_rows;
+    a.x = d_x;
+    a.counts = d_counts;
+    a.lambda = lambda_reg;
+    a.n = n;
+    a.core_reg = lambda_reg / (double)nnz_total;
+    a.with_core = with_core;
+    a.resid = d_r;
+    a.grow = d_grow;
+    a.gcore = d_gcore;
+    a.inter = d_inter;
+    const int bt = 128;
+    const size_t smem = sizeof(double) * (bt / 32) * 3 * off;
+    if (kernel == CMTF_KERNEL_OPT)
+      probe64_kernel<true><<<grid_for(n, bt / 32), bt, smem>>>(a);
+    else
+      probe64_kernel<false><<<grid_for(n, bt / 32), bt, smem>>>(a);
+    CU(cudaGetLastError());
+    std::vector<double> hc(d_gcore ? n * size : 0), hs(d_inter ? n * size : 0);
+    if (residual) CU(cudaMemcpy(residual, d_r, n * sizeof(double), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(grow, d_grow, n * off * sizeof(double), cudaMemcpyDeviceToHost));
+    if (d_gcore)
+      CU(cudaMemcpy(hc.data(), d_gcore, hc.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (d_inter)
+      CU(cudaMemcpy(hs.data(), d_inter, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
     for (uint64_t e = 0; e < n; ++e)
-      for (uint64_t q = 0; q < stored; ++q)
-        gcore[e * stored + q] = hc[e * size + (cp ? q * cs.dstep : q)];
-  return CMTF_OK;
+      for (uint64_t q = 0; q < stored; ++q) {
+        const uint64_t d = e * size + (cp ? q * cs.dstep : q);
+        if (with_core && gcore) gcore[e * stored + q] = hc[d];
+        if (intermediate && d_inter) intermediate[e * stored + q] = hs[d];
+      }
+    return CMTF_OK;
+  };
+  const int rc = run();
+  cleanup();
+  return rc;
 }
 
 int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double* y,
@@ -3734,42 +3749,69 @@ int cmtf_gpu_matrix_entry_gradients(uint64_t n, uint32_t j, const double* y,
   if (n == 0) return CMTF_OK;
   if (j == 0) return set_err(nullptr, CMTF_EVALIDATION, "coupled rows must have equal length");
   CU(cudaSetDevice(device));
-  std::vector<float> hy(n), hu(n * j), hv(n * j);
-  for (uint64_t q = 0; q < n; ++q) hy[q] = (float)y[q];
-  for (uint64_t q = 0; q < n * j; ++q) {
-    hu[q] = (float)u[q];
-    hv[q] = (float)v[q];
-  }
-  float *d_y = nullptr, *d_u = nullptr, *d_v = nullptr, *d_du = nullptr, *d_dv = nullptr,
-        *d_r = nullptr;
+  double *d_y = nullptr, *d_u = nullptr, *d_v = nullptr, *d_du = nullptr, *d_dv = nullptr,
+         *d_r = nullptr;
   uint32_t* d_c = nullptr;
-  TRY(dalloc(ctx, &d_y, n));
-  TRY(dalloc(ctx, &d_u, n * j));
-  TRY(dalloc(ctx, &d_v, n * j));
-  TRY(dalloc(ctx, &d_du, n * j));
-  TRY(dalloc(ctx, &d_dv, n * j));
-  TRY(dalloc(ctx, &d_r, n));
-  TRY(dalloc(ctx, &d_c, n));
-  CU(cudaMemcpy(d_y, hy.data(), n * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_u, hu.data(), n * j * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_v, hv.data(), n * j * sizeof(float), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_c, col_count, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  matrix_probe_kernel<<<grid_for(n), 256>>>(n, j, d_y, d_u, d_v, (float)lambda_m,
-                                            (float)lambda_reg, d_c, d_du, d_dv, d_r);
-  CU(cudaGetLastError());
-  std::vector<float> hdu(n * j), hdv(n * j), hr(n);
-  CU(cudaMemcpy(hdu.data(), d_du, n * j * sizeof(float), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(hdv.data(), d_dv, n * j * sizeof(float), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(hr.data(), d_r, n * sizeof(float), cudaMemcpyDeviceToHost));
+  auto run = [&]() -> int {
+    TRY(dalloc(ctx, &d_y, n));
+    TRY(dalloc(ctx, &d_u, n * j));
+    TRY(dalloc(ctx, &d_v, n * j));
+    TRY(dalloc(ctx, &d_du, n * j));
+    TRY(dalloc(ctx, &d_dv, n * j));
+    TRY(dalloc(ctx, &d_r, n));
+    TRY(dalloc(ctx, &d_c, n));
+    CU(cudaMemcpy(d_y, y, n * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_u, u, n * j * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_v, v, n * j * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_c, col_count, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    matrix_probe64_kernel<<<grid_for(n), 256>>>(n, j, d_y, d_u, d_v, lambda_m, lambda_reg, d_c,
+                                                d_du, d_dv, d_r);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(du, d_du, n * j * sizeof(double), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(dv, d_dv, n * j * sizeof(double), cudaMemcpyDeviceToHost));
+    if (residual) CU(cudaMemcpy(residual, d_r, n * sizeof(double), cudaMemcpyDeviceToHost));
+    return CMTF_OK;
+  };
+  const int rc = run();
   for (auto p : {d_y, d_u, d_v, d_du, d_dv, d_r}) cudaFree(p);
   cudaFree(d_c);
-  for (uint64_t q = 0; q < n * j; ++q) {
-    du[q] = hdu[q];
-    dv[q] = hdv[q];
+  return rc;
+}
+
+int cmtf_gpu_collapse(int32_t order, const uint32_t* ranks, int32_t core_structure,
+                      const double* values, int32_t mode, double* out, int32_t device) {
+  cmtf_gpu_ctx* ctx = nullptr;
+  if (order < 1 || order > kMaxOrder || !ranks)
+    return set_err(nullptr, CMTF_EVALIDATION, "invalid core shape");
+  if (mode < 0 || mode >= order) return set_err(nullptr, CMTF_EVALIDATION, "collapse mode out of range");
+  CoreShape cs{};
+  cs.order = order;
+  uint64_t size = 1;
+  for (int q = 0; q < order; ++q) {
+    cs.J[q] = ranks[q];
+    size *= ranks[q];
   }
-  for (uint64_t q = 0; q < n; ++q)
-    if (residual) residual[q] = hr[q];
-  return CMTF_OK;
+  if (core_structure == 1) {  // CP: element (k,...,k) is the only one with mode index k
+    for (uint32_t k = 0; k < ranks[mode]; ++k) out[k] = values[k];
+    return CMTF_OK;
+  }
+  if (size > (uint64_t)kMaxCore) return set_err(nullptr, CMTF_EUNSUPPORTED, "core too large");
+  cs.size = (uint32_t)size;
+  CU(cudaSetDevice(device));
+  double *d_s = nullptr, *d_o = nullptr;
+  auto run = [&]() -> int {
+    TRY(dalloc(ctx, &d_s, size));
+    TRY(dalloc(ctx, &d_o, ranks[mode]));
+    CU(cudaMemcpy(d_s, values, size * sizeof(double), cudaMemcpyHostToDevice));
+    collapse64_kernel<<<1, 64>>>(cs, d_s, mode, d_o);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(out, d_o, ranks[mode] * sizeof(double), cudaMemcpyDeviceToHost));
+    return CMTF_OK;
+  };
+  const int rc = run();
+  cudaFree(d_s);
+  cudaFree(d_o);
+  return rc;
 }
 
 int cmtf_gpu_visit_counts(cmtf_gpu_ctx* ctx, uint32_t* tensor_counts, uint32_t* matrix_counts) {
@@ -3795,6 +3837,18 @@ int cmtf_gpu_visit_counts(cmtf_gpu_ctx* ctx, uint32_t* tensor_counts, uint32_t* 
   for (auto& M : ctx->mats) mtot += M.nnz;
   if (matrix_counts && mtot)
     CU(cudaMemcpy(matrix_counts, ctx->mvisits, mtot * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_set_schedule(cmtf_gpu_ctx* ctx, const uint64_t* schedule, uint64_t n) {
+  TRY(require_bundle(ctx));
+  uint64_t total = ctx->nnz;
+  for (auto& m : ctx->mats) total += m.nnz;
+  if (n != total) return set_err(ctx, CMTF_EVALIDATION, "schedule length mismatch");
+  for (uint64_t i = 0; i < n; ++i)
+    if (schedule[i] >= total) return set_err(ctx, CMTF_EVALIDATION, "schedule id out of range");
+  ctx->schedule.assign(schedule, schedule + n);
+  ctx->schedule_given = true;
   return CMTF_OK;
 }
 

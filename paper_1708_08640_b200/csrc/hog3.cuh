@@ -36,6 +36,7 @@ struct Hog3Args {
   float eta_core;
   float core_reg;    // lambda / nnz_total
   int nonneg;
+  uint32_t* visits;  // debug_count_visits (null: off)
 };
 
 template <int J1, int J2, int J3>
@@ -117,6 +118,7 @@ hog3_kernel(Hog3Args a) {
   for (uint64_t it = 0; it < iters; ++it) {
     const uint64_t e = lo + it;
     const bool active = e < hi;
+    if (active && a.visits) atomicAdd(a.visits + e, 1u);
     const uint4 rc = nrec;
     if (e + 1 < hi) nrec = __ldg(a.rec + e + 1);
     float r = 0.f;
