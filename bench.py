@@ -453,6 +453,14 @@ def run_ours(args):
                                            pinned(m.values), m.weight)
                              for m in bundle.matrices])
             bundle = pb
+        # the device-generated copies are no longer needed (the context holds
+        # its own records): free them before re-uploading from the host
+        st.bundle = bundle
+        del t, pb
+        test = None
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
         ts, parts = [], []
         for k in range(max(2, args.steps)):
             torch.cuda.synchronize()

@@ -275,6 +275,22 @@ int cmtf_gpu_comm_init(cmtf_gpu_ctx *ctx, int32_t nranks, int32_t rank,
  * base + sum of all ranks' deltas.  core != 0 includes the core. */
 int cmtf_gpu_sync(cmtf_gpu_ctx *ctx, uint32_t mode_mask, uint32_t mat_mask,
                   int32_t core);
+/* Row-block rotation of a stratified factor (U2 / U3
+ * blocks move along the ring instead of being all-reduced): send rows
+ * [send_lo, send_hi) of factor `which` (mode n, or 100 + m for coupled
+ * factor m) to rank send_peer and receive rows [recv_lo, recv_hi) from rank
+ * recv_peer, as one NCCL group on the context's stream (no host wait). */
+int cmtf_gpu_exchange_rows(cmtf_gpu_ctx *ctx, int32_t which, uint32_t send_lo,
+                           uint32_t send_hi, int32_t send_peer, uint32_t recv_lo,
+                           uint32_t recv_hi, int32_t recv_peer);
+/* Consolidation of a block-distributed factor: rank b broadcasts rows
+ * [lo[b], hi[b]) to every rank (n_blocks = number of ranks). */
+int cmtf_gpu_broadcast_rows(cmtf_gpu_ctx *ctx, int32_t which, int32_t n_blocks,
+                            const uint32_t *lo, const uint32_t *hi);
+/* Single-device emulation of one rotation step: copy rows [lo, hi) of
+ * factor `which` from context src to context dst. */
+int cmtf_gpu_exchange_rows_local(cmtf_gpu_ctx *src, cmtf_gpu_ctx *dst,
+                                 int32_t which, uint32_t lo, uint32_t hi);
 /* The same reduction for n contexts living on ONE device (single-GPU
  * emulation of the ranks, used by tests). */
 int cmtf_gpu_sync_local(cmtf_gpu_ctx *const *ctxs, int32_t n, uint32_t mode_mask,

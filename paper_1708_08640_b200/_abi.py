@@ -97,6 +97,10 @@ SIGNATURES = [
     ("cmtf_gpu_comm_unique_id", C.c_int, [C.c_void_p]),
     ("cmtf_gpu_comm_init", C.c_int, [P, C.c_int32, C.c_int32, C.c_void_p]),
     ("cmtf_gpu_sync", C.c_int, [P, C.c_uint32, C.c_uint32, C.c_int32]),
+    ("cmtf_gpu_exchange_rows", C.c_int, [P, C.c_int32, C.c_uint32, C.c_uint32, C.c_int32,
+                                         C.c_uint32, C.c_uint32, C.c_int32]),
+    ("cmtf_gpu_broadcast_rows", C.c_int, [P, C.c_int32, C.c_int32, u32p, u32p]),
+    ("cmtf_gpu_exchange_rows_local", C.c_int, [P, P, C.c_int32, C.c_uint32, C.c_uint32]),
     ("cmtf_gpu_sync_local", C.c_int, [C.POINTER(P), C.c_int32, C.c_uint32, C.c_uint32,
                                       C.c_int32]),
     ("cmtf_gpu_mark", C.c_int, [P, C.c_int32]),

@@ -48,6 +48,13 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  // point-to-point and broadcast (DSGD row-block rotation, consolidation)
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 
 NcclApi& nccl_api() {
@@ -70,8 +77,14 @@ NcclApi& nccl_api() {
   api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
   api.getErrorString =
       reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+  api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+  api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
+  api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));
+  api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+  api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
   if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.allReduce ||
-      !api.getErrorString) {
+      !api.getErrorString || !api.send || !api.recv || !api.broadcast || !api.groupStart ||
+      !api.groupEnd) {
     api.error = "libnccl.so.2 lacks a required symbol";
     api.getUniqueId = nullptr;
   }
@@ -3021,7 +3034,89 @@ int cmtf_gpu_sync(cmtf_gpu_ctx* ctx, uint32_t mode_mask, uint32_t mat_mask, int3
     off += s.n;
   }
   CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(ctx->stream));
+  // no host wait: the next sweep is ordered after the reduction on the
+  // context's stream
+  return CMTF_OK;
+}
+
+namespace {
+// rows [lo, hi) of factor `which` (mode n, or 100 + m for coupled factor m)
+int rows_of(cmtf_gpu_ctx* ctx, int32_t which, uint32_t lo, uint32_t hi, float** p, uint64_t* n) {
+  uint32_t rows = 0, JP = 0;
+  float* base = nullptr;
+  if (which >= 0 && which < ctx->order) {
+    rows = ctx->dims[which];
+    JP = ctx->JP(which);
+    base = ctx->U[which];
+  } else if (which >= 100 && which - 100 < (int)ctx->mats.size()) {
+    const auto& M = ctx->mats[which - 100];
+    rows = M.cols;
+    JP = ctx->JP(M.mode);
+    base = M.V;
+  } else {
+    return set_err(ctx, CMTF_EVALIDATION, "no such factor %d", which);
+  }
+  if (lo > hi || hi > rows) return set_err(ctx, CMTF_EVALIDATION, "row range out of bounds");
+  *p = base + (uint64_t)lo * JP;
+  *n = (uint64_t)(hi - lo) * JP;
+  return CMTF_OK;
+}
+}  // namespace
+
+int cmtf_gpu_exchange_rows(cmtf_gpu_ctx* ctx, int32_t which, uint32_t send_lo, uint32_t send_hi,
+                           int32_t send_peer, uint32_t recv_lo, uint32_t recv_hi,
+                           int32_t recv_peer) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (!ctx->comm) return set_err(ctx, CMTF_EVALIDATION, "no communicator (cmtf_gpu_comm_init)");
+  float *sp = nullptr, *rp = nullptr;
+  uint64_t sn = 0, rn = 0;
+  TRY(rows_of(ctx, which, send_lo, send_hi, &sp, &sn));
+  TRY(rows_of(ctx, which, recv_lo, recv_hi, &rp, &rn));
+  NcclApi& N = nccl_api();
+  ncclResult_t r = N.groupStart();
+  if (r == ncclSuccess && sn) r = N.send(sp, sn, ncclFloat, send_peer, ctx->comm, ctx->stream);
+  if (r == ncclSuccess && rn) r = N.recv(rp, rn, ncclFloat, recv_peer, ctx->comm, ctx->stream);
+  const ncclResult_t r2 = N.groupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return set_err(ctx, CMTF_ENCCL, "ncclSend/ncclRecv: %s", N.getErrorString(r));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_exchange_rows_local(cmtf_gpu_ctx* src, cmtf_gpu_ctx* dst, int32_t which, uint32_t lo,
+                                 uint32_t hi) {
+  TRY(require_bundle(src));
+  TRY(require_bundle(dst));
+  cmtf_gpu_ctx* ctx = dst;
+  if (src->device != dst->device) return set_err(dst, CMTF_EVALIDATION, "exchange_rows_local needs one device");
+  CU(cudaSetDevice(dst->device));
+  float *sp = nullptr, *dp = nullptr;
+  uint64_t sn = 0, dn = 0;
+  TRY(rows_of(src, which, lo, hi, &sp, &sn));
+  TRY(rows_of(dst, which, lo, hi, &dp, &dn));
+  if (sn != dn) return set_err(dst, CMTF_EVALIDATION, "row layouts differ");
+  CU(cudaStreamSynchronize(src->stream));
+  CU(cudaMemcpyAsync(dp, sp, sn * sizeof(float), cudaMemcpyDeviceToDevice, dst->stream));
+  CU(cudaStreamSynchronize(dst->stream));
+  return CMTF_OK;
+}
+
+int cmtf_gpu_broadcast_rows(cmtf_gpu_ctx* ctx, int32_t which, int32_t n_blocks,
+                            const uint32_t* lo, const uint32_t* hi) {
+  TRY(require_bundle(ctx));
+  CU(cudaSetDevice(ctx->device));
+  if (!ctx->comm) return set_err(ctx, CMTF_EVALIDATION, "no communicator (cmtf_gpu_comm_init)");
+  NcclApi& N = nccl_api();
+  ncclResult_t r = N.groupStart();
+  for (int b = 0; b < n_blocks && r == ncclSuccess; ++b) {
+    float* p = nullptr;
+    uint64_t n = 0;
+    TRY(rows_of(ctx, which, lo[b], hi[b], &p, &n));
+    if (n) r = N.broadcast(p, p, n, ncclFloat, b, ctx->comm, ctx->stream);
+  }
+  const ncclResult_t r2 = N.groupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return set_err(ctx, CMTF_ENCCL, "ncclBroadcast: %s", N.getErrorString(r));
   return CMTF_OK;
 }
 

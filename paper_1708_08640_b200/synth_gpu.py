@@ -214,6 +214,7 @@ def generate(spec: GpuSpec, device="cuda"):
         mats.append(DeviceMatrix(ms.mode, rows, ms.cols, ij.to(torch.int32).contiguous(),
                                  y.contiguous(), ms.weight))
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # generation temporaries: give the memory back
     return DeviceBundle(train, mats), test
 
 
