@@ -516,44 +516,57 @@ def run_ours(args):
 
 
 def run_dsgd(args):
-    """N > 1: DSGD strata over the ranks (one process per GPU), deltas of the
-    replicated parameters all-reduced with NCCL inside the library after every
-    sub-epoch.  Default: weak scaling -- the workload grows with N (config 2 at
-    N x its size, generated on the device), so each GPU keeps a config-2-sized
-    share with all SMs busy under the same staleness bound (the worker rule
-    caps in-flight entries at ~1/112 of a rank's share; a config-2-sized
-    problem split 8 ways would leave 7/8 of every GPU idle).  --strong keeps
-    the total fixed."""
+    """N > 1: DSGD over the ranks (one process per GPU).
+    Every rank generates the workload on its own device (same seed), keeps
+    only its own entries (device partition, dsgd.partition_rank), and runs
+    the stratified epoch: stratum sweeps, ring rotation of the stratified
+    row blocks (ncclSend / ncclRecv) and delta all-reduces of the replicated
+    parameters, all on the context's stream.  Config 5 stratifies all three
+    1e7-row modes (G^2 steps); the others modes 1 and 2.  BASELINE's
+    multi-GPU configs (3 - 5) keep the total workload fixed (strong scaling);
+    config 2 grows with N (weak scaling: config 2 at N x its nonzeros, every
+    GPU a config-2-sized share) unless --strong."""
     import ctypes as C
 
     import torch
     import torch.distributed as dist
 
     from paper_1708_08640_b200 import api, dsgd
+    from paper_1708_08640_b200.synth_gpu import DeviceBundle, DeviceMatrix, DeviceTensor
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29511")
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"), rank=rank,
                             world_size=world)
-    weak = not args.strong
+    n_strat = 3 if args.config == "config5" else 2
+    weak = not args.strong and args.config in ("config1", "config2")
     spec, bundle, test, ranks, lr, lam = make_workload(
-        args, mult=world if weak else 1.0, device_gen=weak and world > 1)
-    bundle = host_bundle(bundle)  # partitioning runs on the host
-    if hasattr(test, "to_host"):
-        test = test.to_host()
+        args, mult=world if weak else 1.0, device_gen=True)
+    dev = f"cuda:{local}"
+    if not hasattr(bundle.tensor, "to_host"):  # host-generated (config 1): to the device
+        t = bundle.tensor
+        bundle = DeviceBundle(
+            DeviceTensor(t.dims, torch.from_numpy(t.indices.view(np.int32)).to(dev),
+                         torch.from_numpy(t.values).to(dev)),
+            [DeviceMatrix(m.coupled_mode, m.rows, m.cols,
+                          torch.from_numpy(m.indices.view(np.int32)).to(dev),
+                          torch.from_numpy(m.values).to(dev), m.weight) for m in bundle.matrices])
+    nt, Bt, Ft, mats = algorithmic(bundle, ranks)
+    n_upd = nt + sum(n for n, _ in mats)
+    plan, counts, col_counts, nnz = dsgd.partition_rank(bundle, world, rank, n_strat=n_strat)
+    del bundle
+    import gc
+    gc.collect()
     torch.cuda.empty_cache()
     cfg = api.TrainConfig(ranks=ranks, seed=0, eta0=lr, lambda_reg=lam, kernel=args.kernel,
                           device=local)
-    part = dsgd.partition(bundle, world)
-    rs = dsgd.RankState(part, rank, cfg)
+    rs = dsgd.RankState(plan, rank, cfg, counts, col_counts, nnz)
     obj = [dsgd.new_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     dsgd.comm_init(rs, world, rank, obj[0])
     L, h = rs.state._L, rs.state._h
-    nt, Bt, Ft, mats = algorithmic(bundle, ranks)
-    n_upd = nt + sum(n for n, _ in mats)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         dsgd.run_epoch_nccl(rs)
     torch.cuda.synchronize()
@@ -572,66 +585,82 @@ def run_dsgd(args):
         rs.state._check(L.cmtf_gpu_elapsed_ms(h, 0, 1, C.byref(ms)))
         per.append(ms.value)
     clk = clocks.stop()
-    t = torch.tensor([sum(per) / len(per)], device=f"cuda:{local}")
+    t = torch.tensor([sum(per) / len(per)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item())
     value = n_upd / (ms_step * 1e-3)
     props = torch.cuda.get_device_properties(local)
     peak = fp32_peak_tflops(props.multi_processor_count, 1965.0) * world
     achieved = nt * Ft / (ms_step * 1e-3) / 1e12
-    n_sync = bin(rs.plan.sync_modes).count("1") + len(bundle.matrices) + 1
-    launches = args.steps * (world * (1 + 2 * n_sync) + 2 * bin(rs.plan.end_modes).count("1")
-                             + 1 + len(ranks) + len(bundle.matrices))
-    line = None
+    sch = plan.schedule
+    n_rot = sum(len(sch.rotations_after(s)) for s in range(sch.steps))
+    n_sync = bin(plan.shared_modes).count("1") + bin(plan.mat_mask).count("1") + 1
+    launches = args.steps * (sch.steps * (1 + 2 * n_sync) + 2 + len(ranks) + len(mats))
+    # quality: consolidate the blocks, test RMSE on the held-out split;
+    # train RMSE from every rank's local SSE
+    dsgd.consolidate_nccl(rs)
+    torch.cuda.synchronize()
+    st_local = api.epoch_stats(rs.state, lam)
+    sse = torch.tensor([st_local.train_rmse ** 2 * plan.bundle.tensor.nnz], device=dev,
+                       dtype=torch.float64)
+    dist.all_reduce(sse)
+    train_rmse = float((sse / nnz).sqrt().item())
+    test_rmse = api.test_rmse(rs.state, test) if rank == 0 else None
+    # e2e: re-upload the rank's local bundle from pinned host memory, run the
+    # epoch, read the stats back (wall clock, max over ranks)
+    lb = plan.bundle
+    pb = DeviceBundle(DeviceTensor(lb.tensor.dims, lb.tensor.indices.cpu().pin_memory(),
+                                   lb.tensor.values.cpu().pin_memory()),
+                      [DeviceMatrix(m.coupled_mode, m.rows, m.cols, m.indices.cpu().pin_memory(),
+                                    m.values.cpu().pin_memory(), m.weight) for m in lb.matrices])
+    h2d = pb.tensor.indices.nbytes + pb.tensor.values.nbytes + sum(
+        m.indices.nbytes + m.values.nbytes for m in pb.matrices)
+    rs.plan.bundle = pb
+    rs.state.bundle = pb
+    del lb, test
+    gc.collect()
+    torch.cuda.empty_cache()
+    ts = []
+    for _ in range(max(2, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        rs.reupload()
+        dsgd.run_epoch_nccl(rs)
+        api.epoch_stats(rs.state, lam)
+        ts.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.median(ts)], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    hb = torch.tensor([float(h2d)], device=dev, dtype=torch.float64)
+    dist.all_reduce(hb)
     if rank == 0:
-        full = api.TrainState(api.TrainConfig(ranks=ranks, seed=0, eta0=lr, lambda_reg=lam,
-                                              device=local), bundle)
-        full.model = rs.state.model
         line = {
             "metric": "tensor+matrix nonzero SGD updates/sec per epoch", "value": value,
             "unit": "updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if weak else "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} ({CONFIG_INDEX.get(args.config, '?')}), "
-                               f"scale {args.scale}" + (f", nnz {args.nnz:g}, rank {args.rank}"
-                                                         if args.config == "config5" else "")
-                               + (f", x{world} (weak scaling: one config-sized share per GPU, "
-                                  "device-generated)" if weak and world > 1 else ""),
+            "vs_baseline": None, "dtype": "f32 (tcgen05 MMAs on split-fp16 x3 operands, "
+                                          "fp32 accumulate)", "data": "synthetic",
+            "config": {"workload": workload_name(args)
+                       + (f", x{world} (weak scaling: one config-sized share per GPU, "
+                          "device-generated)" if weak else ", fixed total (strong scaling)"),
                        "tensor_entries": nt, "matrix_entries": [n for n, _ in mats],
                        "ranks": ranks, "kernel": args.kernel, "lr": lr, "lambda": lam,
-                       "parallelism": f"dsgd{world} (mode-1 x mode-2 strata, NCCL all-reduce "
-                                      "of replicated deltas per sub-epoch)",
+                       "parallelism": f"dsgd{world}: {n_strat}-mode strata, {sch.steps} steps "
+                                      "per epoch, row blocks rotated with ncclSend/ncclRecv, "
+                                      "replicated deltas all-reduced per step",
                        "l2": "flushed between epochs"},
-            "quality": {"train_rmse": api.epoch_stats(full, lam).train_rmse,
-                        "test_rmse": api.test_rmse(full, test), "epochs_done": rs.state.epoch},
+            "quality": {"train_rmse": train_rmse, "test_rmse": test_rmse,
+                        "epochs_done": rs.state.epoch},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "peak_source": f"nominal FP32 x {world} GPUs",
-                         "kernel": "whole DSGD epoch (sweeps + NCCL syncs)"},
-            "clocks": clk, "gpu_launches": launches,
-            "e2e": None,
+                         "kernel": "whole DSGD epoch (sweeps + NCCL rotations / reductions)"},
+            "clocks": clk, "gpu_launches": launches, "rotations_per_epoch": n_rot,
+            "e2e": {"value": n_upd / float(te.item()), "unit": "updates/s",
+                    "h2d_bytes_per_step": int(hb.item()), "d2h_bytes_per_step": 16 * world,
+                    "ms_per_step": 1e3 * float(te.item())},
         }
-    # e2e: re-upload the rank's local bundle from host memory, run the epoch,
-    # read the stats back (wall clock, max over ranks)
-    ts = []
-    for _ in range(max(2, args.steps // 2)):
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        rs.reupload(part)
-        dsgd.run_epoch_nccl(rs)
-        api.epoch_stats(rs.state, lam)
-        ts.append(time.perf_counter() - t0)
-    te = torch.tensor([statistics.median(ts)], device=f"cuda:{local}")
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    if rank == 0:
-        lb = rs.plan.bundle
-        h2d = lb.tensor.indices.nbytes + lb.tensor.values.nbytes + sum(
-            m.indices.nbytes + m.values.nbytes for m in lb.matrices)
-        line["e2e"] = {"value": n_upd / float(te.item()), "unit": "updates/s",
-                       "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": 16 * world,
-                       "ms_per_step": 1e3 * float(te.item())}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 

@@ -22,6 +22,7 @@ for G in Gs:
     t0 = time.time()
     for ep in range(10):
         dsgd.run_epoch_emulated(ranks)
+    dsgd.consolidate_emulated(ranks)
     el = time.time() - t0
     full = api.TrainState(cfg, b)
     full.model = ranks[0].state.model

@@ -25,6 +25,7 @@ for G in (2, 4):
     ranks = [dsgd.RankState(part, p, cfg()) for p in range(G)]
     for _ in range(10):
         dsgd.run_epoch_emulated(ranks)
+    dsgd.consolidate_emulated(ranks)
     full = api.TrainState(cfg(), b)
     full.model = ranks[0].state.model
     tr, te = api.epoch_stats(full, 0.01).train_rmse, api.test_rmse(full, test)

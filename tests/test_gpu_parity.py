@@ -413,12 +413,13 @@ def test_config3_full_scale_within_1pct_of_reference():
     assert abs(te - ref["test"][-1]) <= 0.01 * ref["test"][-1], (te, ref["test"][-1])
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_dsgd_emulated_ranks_within_1pct(G):
+@pytest.mark.parametrize("G,n_strat", [(2, 2), (4, 2), (2, 3)])
+def test_dsgd_emulated_ranks_within_1pct(G, n_strat):
     """DSGD with G ranks emulated on one GPU -- the multi-GPU
-    algorithm minus the NCCL transport: strata sweeps + delta reductions of the
-    replicated parameters.  10 epochs on config 2 at 10% scale vs the
-    reference's own run."""
+    algorithm minus the NCCL transport: strata sweeps, delta reductions of
+    the replicated parameters, ring rotation of the stratified row blocks
+    (device copies between the rank contexts) and the final consolidation.
+    10 epochs on config 2 at 10% scale vs the reference's own run."""
     import json
     import os
     from conftest import GOLDEN
@@ -426,13 +427,16 @@ def test_dsgd_emulated_ranks_within_1pct(G):
     ref = json.load(open(os.path.join(GOLDEN, "config2_s01_reference.json")))
     b, test, _ = synth.generate(synth.config2(0.1))
     cfg = TrainConfig(ranks=[10, 10, 10], seed=0, eta0=1e-3, mu=0.1, lambda_reg=0.01)
-    part = dsgd.partition(b, G)
+    part = dsgd.partition(b, G, n_strat=n_strat)
     ranks = [dsgd.RankState(part, p, cfg) for p in range(G)]
     for _ in range(10):
         dsgd.run_epoch_emulated(ranks)
+    dsgd.consolidate_emulated(ranks)
     models = [r.state.model for r in ranks]
-    for m in models[1:]:  # replicas agree after the end-of-epoch sync
+    for m in models[1:]:  # replicas agree after the consolidation
         np.testing.assert_allclose(m.core, models[0].core, rtol=0, atol=1e-6)
+        for a, c in zip(m.factors, models[0].factors):
+            np.testing.assert_allclose(a, c, rtol=0, atol=1e-6)
     full = api.TrainState(cfg, b)
     full.model = models[0]
     tr = api.epoch_stats(full, 0.01).train_rmse
