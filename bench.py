@@ -348,12 +348,34 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(local)
     sms = props.multi_processor_count
     peak_nominal = fp32_peak_tflops(sms, 1965.0)
-    achieved = nt * Ft / (ten_ms * 1e-3) / 1e12
+    # the binding bound is the slower of the gather bytes at
+    # HBM bandwidth and the flops at FP32 peak (J = 10: FP32; J = 5: HBM)
+    hbm_peak = 6548.5e9
+    hbm_src = "fallback 6548.5 GB/s"
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        pass
     bytes_t = nt * Bt
-    roof = {"bound": "fp32", "achieved": achieved, "peak": peak_nominal, "unit": "TFLOP/s",
-            "frac": achieved / peak_nominal, "traffic": None,
-            "peak_source": f"nominal FP32: {sms} SMs x 128 FMA x 2 x 1965 MHz (no FP32 "
-                           "entry in MEASURED_PEAKS.json)",
+    hbm_bound = Bt / hbm_peak > Ft / (peak_nominal * 1e12)
+    if hbm_bound:
+        achieved = bytes_t / (ten_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak / 1e9, "unit": "GB/s",
+                "frac": achieved / (hbm_peak / 1e9), "traffic": None, "peak_source": hbm_src}
+    else:
+        achieved = nt * Ft / (ten_ms * 1e-3) / 1e12
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak_nominal, "unit": "TFLOP/s",
+                "frac": achieved / peak_nominal, "traffic": None,
+                "peak_source": f"nominal FP32: {sms} SMs x 128 FMA x 2 x 1965 MHz (no FP32 "
+                               "entry in MEASURED_PEAKS.json)"}
+    # the factor rows of the large configs are random 48-byte rows in tables
+    # far beyond L2: the memory system's measured ceiling for that access
+    # pattern (scripts/micro/red_bench.cu on this B200: ~1.8e10 random row
+    # gathers/s, ~1.3-1.9e10 random row updates/s) bounds the sweep before
+    # either term above does
+    rows_per_s = (len(ranks) * nt + 2 * sum(n for n, _ in mats)) / (ten_ms * 1e-3)
+    roof.update({
             "kernel": {"order3v2": "hog3v2_kernel (fused tensor+matrix epoch sweep)",
                        "order3tm": "hog3tm_kernel (fused epoch sweep, tcgen05 contractions + "
                                    "core gradient, TMEM accumulators)",
@@ -363,8 +385,12 @@ def run_ours(args):
             "kernel_ms": ten_ms,
             "flops_per_update": Ft, "bytes_per_update": Bt,
             "gather_gbs": bytes_t / (ten_ms * 1e-3) / 1e9,
-            "frac_at_measured_clock": (achieved / fp32_peak_tflops(sms, clk["sm_mhz"])
-                                       if clk.get("sm_mhz") else None)}
+            "fp32_tflops": nt * Ft / (ten_ms * 1e-3) / 1e12,
+            "row_updates_per_s": rows_per_s,
+            "random_row_ceiling_per_s": 1.8e10,
+            "frac_at_measured_clock": ((nt * Ft / (ten_ms * 1e-3) / 1e12)
+                                       / fp32_peak_tflops(sms, clk["sm_mhz"])
+                                       if clk.get("sm_mhz") and not hbm_bound else None)})
     # DRAM traffic per launch of the dominant kernel, from the committed ncu
     # --set full capture of the same command (profiles/ncu_r1_metrics.json)
     try:
@@ -395,11 +421,7 @@ def run_ours(args):
     except Exception:
         pass
     # epoch roofline time: both terms, slower of HBM and FP32
-    hbm = 6548.5e9
-    try:
-        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
-    except Exception:
-        pass
+    hbm = hbm_peak
     t_roof = nt * max(Bt / hbm, Ft / (peak_nominal * 1e12)) + sum(
         n * max((16 + 16 * j) / hbm, 10 * j / (peak_nominal * 1e12)) for n, j in mats)
     roof["epoch_roofline_frac"] = t_roof / (ms_step * 1e-3)

@@ -54,6 +54,25 @@ struct Hog4Args {
   uint32_t* mvisits;
 };
 
+// D += A B on the tensor cores at fp32-level accuracy: every operand is
+// split x = hi + lo (split_tf32) and the product formed as
+// hi*hi + hi*lo + lo*hi (3xTF32, ~21 mantissa bits; the lo*lo term is below
+// fp32 rounding) -- the per-entry contractions keep the north_star's 1e-5
+// per-entry tolerance instead of TF32's ~1e-3
+__device__ __forceinline__ void mma_3xtf32(float* d, const uint32_t* ah, const uint32_t* al,
+                                           const uint32_t* b) {
+  uint32_t bh[2], bl[2];
+  split_tf32(__uint_as_float(b[0]), bh[0], bl[0]);
+  split_tf32(__uint_as_float(b[1]), bh[1], bl[1]);
+  mma_tf32(d, ah, bl);
+  mma_tf32(d, al, bh);
+  mma_tf32(d, ah, bh);
+}
+__device__ __forceinline__ void split4(const uint32_t* a, uint32_t* ah, uint32_t* al) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) split_tf32(__uint_as_float(a[k]), ah[k], al[k]);
+}
+
 template <int J, int NW, bool TC = false>
 struct V4Layout {
   static_assert(J == 8 && NW == 8, "hog4 is specialised for J = 8 (one core slab per warp)");
@@ -447,6 +466,8 @@ hog4_kernel(Hog4Args a) {
         av1[1] = __float_as_uint(s1[3 * JP + t4]);
         av1[2] = __float_as_uint(s0[3 * JP + t4 + 4]);
         av1[3] = __float_as_uint(s1[3 * JP + t4 + 4]);
+        uint32_t av1h[4], av1l[4];
+        split4(av1, av1h, av1l);
         const float2 c0 = *reinterpret_cast<const float2*>(s0 + 2 * JP + 2 * t4);
         const float2 c1 = *reinterpret_cast<const float2*>(s1 + 2 * JP + 2 * t4);
         const float u3c[4] = {c0.x, c0.y, c1.x, c1.y};
@@ -479,7 +500,7 @@ hog4_kernel(Hog4Args a) {
             bb[0] = __float_as_uint(g1a[(ib * J + g8) * L::S1 + t4]);
             bb[1] = __float_as_uint(g1a[(ib * J + g8) * L::S1 + t4 + 4]);
             float d[4] = {0.f, 0.f, 0.f, 0.f};
-            mma_tf32(d, av1, bb);  // T[R0][2t4], T[R0][2t4+1], T[R1][2t4], T[R1][2t4+1]
+            mma_3xtf32(d, av1h, av1l, bb);  // T[R0][2t4], T[R0][2t4+1], T[R1][2t4], T[R1][2t4+1]
             const float pab0 = ua0 * u2r0[ib], pab1 = ua1 * u2r1[ib];
             const float sp0 = fmaf(d[1], u3c[1], d[0] * u3c[0]);
             const float sp1 = fmaf(d[3], u3c[3], d[2] * u3c[2]);
@@ -498,7 +519,9 @@ hog4_kernel(Hog4Args a) {
             ap[3] = __float_as_uint(pab1 * u3k[3]);
             b2[0] = __float_as_uint(g2a[(ib * J + t4) * JP + g8]);
             b2[1] = __float_as_uint(g2a[(ib * J + t4 + 4) * JP + g8]);
-            mma_tf32(d4x[ib & 3], ap, b2);  // g4[R0][2t4], [R0][2t4+1], [R1][2t4], [R1][2t4+1]
+            uint32_t aph[4], apl[4];
+            split4(ap, aph, apl);
+            mma_3xtf32(d4x[ib & 3], aph, apl, b2);  // g4[R0][2t4], [R0][2t4+1], [R1][2t4], [R1][2t4+1]
           }
           w1p0 += __shfl_xor_sync(0xffffffffu, w1p0, 1);
           w1p1 += __shfl_xor_sync(0xffffffffu, w1p1, 1);
@@ -623,6 +646,8 @@ hog4_kernel(Hog4Args a) {
       av[1] = 0u;
       av[2] = __float_as_uint(s1[3 * JP + g8]);
       av[3] = 0u;
+      uint32_t avh[4], avl[4];
+      split4(av, avh, avl);
       const float4 b00 = *reinterpret_cast<const float4*>(s0 + JP);
       const float4 b01 = *reinterpret_cast<const float4*>(s0 + JP + 4);
       const float4 b10 = *reinterpret_cast<const float4*>(s1 + JP);
@@ -635,7 +660,7 @@ hog4_kernel(Hog4Args a) {
         bv[0] = __float_as_uint(p0 * v0[ib]);  // B[e0][c=g8] = Q_e0[(ib, g8)]
         bv[1] = __float_as_uint(p1 * v1[ib]);
         float d[4] = {acc[ib][0], acc[ib][1], 0.f, 0.f};
-        mma_tf32(d, av, bv);
+        mma_3xtf32(d, avh, avl, bv);
         acc[ib][0] = d[0];  // D[d=g8][c=2t4], D[g8][2t4+1]
         acc[ib][1] = d[1];
       }
