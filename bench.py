@@ -41,7 +41,7 @@ FP32_FMA_PER_SM_CLK = 128  # Blackwell SM: 4 x 32 FP32 lanes
 # operands, hi*hi + hi*lo + lo*hi, ~22 mantissa bits -- fp32-level accuracy)
 DTYPE = {"order3tm": "f32 (tcgen05 MMAs on split-fp16 x3 operands, fp32 accumulate)",
          "order3v2": "f32 (core gradient: tf32 mma.sync)",
-         "order4": "f32 (tf32 mma.sync contractions)",
+         "order4": "f32 (mma.sync on split 3xTF32 operands, fp32 accumulate)",
          "order3": "f32", "generic": "f32"}
 CONFIG_INDEX = {"config1": "BASELINE configs[0]", "config2": "BASELINE configs[1]",
                 "config3": "BASELINE configs[2]", "config4": "BASELINE configs[3]",

@@ -1941,6 +1941,43 @@ __global__ void dup_hash_kernel(const uint32_t* idx, uint64_t nnz, DupKey k,
   }
 }
 
+// The duplicate check of an upload, chunk by chunk as the chunks land (it
+// overlaps the rest of the host-to-device copy).  Exact mixed-radix keys
+// when the index space fits 64 bits (a repeated key is a duplicate; the
+// smallest wins an atomicMin, = the lexicographically smallest tuple);
+// otherwise 64-bit hashes of the tuples: equal tuples always collide, so no
+// collision proves there is no duplicate, and a collision (a duplicate or a
+// hash collision) sends the upload to the exact LSD-sort check.
+__global__ void dup_insert_kernel(const uint32_t* idx, uint64_t e_lo, uint64_t e_hi, DupKey k,
+                                  unsigned long long* table, uint64_t cap_mask,
+                                  unsigned long long* first_key) {
+  for (uint64_t e = e_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < e_hi;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0;
+    if (k.exact) {
+      for (int n = 0; n < k.order; ++n) key = key * k.dims[n] + idx[e * k.order + n];
+    } else {
+      key = 0x243f6a8885a308d3ull;
+      for (int n = 0; n < k.order; ++n) {
+        key ^= idx[e * k.order + n] + 0x9e3779b97f4a7c15ull + (key << 6) + (key >> 2);
+        key *= 0xbf58476d1ce4e5b9ull;
+        key ^= key >> 31;
+      }
+      if (key == ~0ull) key = 0;  // the empty-slot marker
+    }
+    unsigned long long h = key * 0x9e3779b97f4a7c15ull;
+    h ^= h >> 29;
+    for (uint64_t s = h & cap_mask;; s = (s + 1) & cap_mask) {
+      const unsigned long long prev = atomicCAS(table + s, ~0ull, key);
+      if (prev == ~0ull) break;
+      if (prev == key) {
+        atomicMin(first_key, k.exact ? key : 0ull);
+        break;
+      }
+    }
+  }
+}
+
 // check_entries' first failure (src/sparse_data.cpp:29-41) from the device
 // validation's first bad entries: bad[0] = first index out of range, bad[1] =
 // first non-finite value.  The reference scans entries in order and checks an
@@ -1971,6 +2008,26 @@ bool on_device(const cmtf_gpu_ctx* ctx, const void* p) {
   }
   return at.type == cudaMemoryTypeDevice && at.device == ctx->device;
 }
+
+// CMTF_PREP_TIMING: phase times of an upload (synchronising at each tick)
+struct PhaseTimer {
+  const char* what;
+  cmtf_gpu_ctx* ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  PhaseTimer(const char* w, cmtf_gpu_ctx* c)
+      : what(w), ctx(c), on(std::getenv("CMTF_PREP_TIMING") != nullptr),
+        t0(std::chrono::steady_clock::now()) {}
+  void tick(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamSynchronize(ctx->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "%s %-14s %.3f ms\n", what, phase,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 // The upload staging (up to ~45 bytes per entry: 45 GB at 1e9 entries) is
 // released after every upload instead of living with the context.
@@ -2184,6 +2241,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   }
   ctx->sort_mode = sm;
 
+  PhaseTimer pt("set_tensor", ctx);
   const bool in_place = on_device(ctx, idx) && on_device(ctx, vals);
   // device-resident inputs may still be written by work on the caller's
   // streams (the context's streams are non-blocking): wait for the device
@@ -2237,6 +2295,22 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
     TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
     TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
   }
+  // duplicate-check table (load factor <= 1/2), filled chunk by chunk
+  DupKey dk{};
+  dk.order = N;
+  {
+    double bits = 0;
+    for (int n = 0; n < N; ++n) {
+      dk.dims[n] = dims[n];
+      bits += std::log2((double)std::max<uint32_t>(dims[n], 1));
+    }
+    dk.exact = bits < 63.5;
+  }
+  uint64_t dcap = 1;
+  while (dcap < 2 * nnz) dcap <<= 1;
+  TRY(ensure(ctx, &ctx->dup_keys, &ctx->dup_keys_cap, dcap));
+  CU(cudaMemsetAsync(ctx->dup_keys, 0xff, dcap * sizeof(unsigned long long), ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_first + 2, 0xff, sizeof(unsigned long long), ctx->stream));
   for (int k = 0; k < kChunks; ++k) {
     const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
     if (c0 >= c1) break;
@@ -2245,11 +2319,16 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
         d_idx, d_vals, c0, c1, N, mt, shuffled ? -1 : sm, (uint32_t)ctx->cfg.seed + 0x5bd1e995u,
         direct ? ctx->rec : d_rec, need_keys ? d_keys : nullptr, d_ids, ctx->d_first,
         direct ? nnz : 0, pa, pb, ctx->pos);
+    dup_insert_kernel<<<grid_for(c1 - c0), 256, 0, ctx->stream>>>(
+        d_idx, c0, c1, dk, ctx->dup_keys, dcap - 1, ctx->d_first + 2);
   }
   CU(cudaGetLastError());
-  unsigned long long bad[2];
+  unsigned long long bad[3];
   CU(cudaMemcpyAsync(bad, ctx->d_first, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  dfree(ctx->dup_keys);
+  ctx->dup_keys_cap = 0;
+  pt.tick("h2d+pack+dup");
   if (bad[0] != ~0ull || bad[1] != ~0ull) {
     dfree(ctx->rec);
     ctx->rec_cap = 0;
@@ -2257,10 +2336,21 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
     release_staging(ctx);
     return rc;
   }
-  {
+  if (bad[2] != ~0ull) {  // a repeated key (exact) or hash (wide tuples)
     std::vector<uint32_t> tup;
     bool dup = false;
-    const int rc = find_duplicate(ctx, d_idx, nnz, N, dims, &tup, &dup);
+    int rc = CMTF_OK;
+    if (dk.exact) {  // decode the smallest duplicated mixed-radix key
+      unsigned long long f = bad[2];
+      tup.assign(N, 0u);
+      for (int n = N - 1; n >= 0; --n) {
+        tup[n] = (uint32_t)(f % dims[n]);
+        f /= dims[n];
+      }
+      dup = true;
+    } else {  // exact check: the smallest duplicated tuple, or a hash collision
+      rc = find_duplicate(ctx, d_idx, nnz, N, dims, &tup, &dup);
+    }
     if (rc || dup) {
       dfree(ctx->rec);
       ctx->rec_cap = 0;
@@ -2269,6 +2359,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
       return set_err(ctx, CMTF_EVALIDATION, "%s", dup_message("tensor", tup).c_str());
     }
   }
+  pt.tick("duplicates");
   TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
   TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
   ctx->posA = 1;
@@ -2287,6 +2378,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   CU(cudaStreamSynchronize(ctx->stream));
   if (sorted_ids) cudaFree(sorted_ids);
   release_staging(ctx);
+  pt.tick("finish");
   // model buffers (allocated with the bundle's shapes; kept on re-upload of a
   // same-shaped bundle, as run_epoch(state, bundle) keeps the state's model)
   if (!same_shape || !ctx->G) {

@@ -295,6 +295,17 @@ def test_duplicate_indices_rejected_like_the_reference():
     t = api.SparseTensor([1 << 20] * 4, big, np.ones(3))
     with pytest.raises(api.ValidationError, match=r"duplicate tensor index \(6 7 8 9\)"):
         api.make_state(TrainConfig(ranks=[2, 2, 2, 2]), api.DataBundle(t, []))
+    # two duplicated wide tuples among many distinct ones: the smaller is reported
+    wide = rng.integers(0, 1 << 20, size=(20000, 4)).astype(np.uint32)
+    wide = np.unique(wide, axis=0)
+    wide = np.concatenate([wide, [[9, 9, 9, 9], [5, 6, 7, 8], [9, 9, 9, 9], [5, 6, 7, 8]]])
+    rng.shuffle(wide)
+    t = api.SparseTensor([1 << 20] * 4, wide.astype(np.uint32), np.ones(len(wide)))
+    with pytest.raises(api.ValidationError, match=r"duplicate tensor index \(6 7 8 9\)"):
+        api.make_state(TrainConfig(ranks=[2, 2, 2, 2]), api.DataBundle(t, []))
+    # and none: the hashed pass alone accepts the upload
+    t = api.SparseTensor([1 << 20] * 4, np.unique(wide, axis=0), np.ones(len(np.unique(wide, axis=0))))
+    api.make_state(TrainConfig(ranks=[2, 2, 2, 2]), api.DataBundle(t, []))
 
 
 def test_order4_and_ragged_ranks_use_generic_path():
