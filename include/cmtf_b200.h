@@ -319,6 +319,12 @@ int cmtf_gpu_last_epoch_timing(cmtf_gpu_ctx *ctx, double *kernel_ms,
  * 2 specialised N=4; hog_threads actually used. */
 int cmtf_gpu_kernel_info(cmtf_gpu_ctx *ctx, int32_t *which,
                          int32_t *hog_threads, int32_t *sort_mode);
+/* The tensor records' visiting layout: *blocks = B when the order-3
+ * tcgen05 epoch runs the L2-blocked order (B x B strata of mode-1 x mode-2
+ * row blocks, stratum-major records, random stratum sequence per epoch; set
+ * up on the first whole random-order epoch), else 0.  positions (NULL or
+ * nnz entries): the current record position of every training entry. */
+int cmtf_gpu_order_blocks(cmtf_gpu_ctx *ctx, int32_t *blocks, uint32_t *positions);
 
 /* ---- text formats and host-side data preparation ----
  * Host C++ (io.cpp), all host threads; no device is needed except for

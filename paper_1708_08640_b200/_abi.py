@@ -107,6 +107,7 @@ SIGNATURES = [
     ("cmtf_gpu_elapsed_ms", C.c_int, [P, C.c_int32, C.c_int32, f64p]),
     ("cmtf_gpu_last_epoch_timing", C.c_int, [P, f64p, i32p]),
     ("cmtf_gpu_kernel_info", C.c_int, [P, i32p, i32p, i32p]),
+    ("cmtf_gpu_order_blocks", C.c_int, [P, i32p, u32p]),
     ("cmtf_gpu_visit_counts", C.c_int, [P, u32p, u32p]),
     ("cmtf_gpu_collapse", C.c_int, [C.c_int32, u32p, C.c_int32, f64p, C.c_int32, f64p,
                                     C.c_int32]),

@@ -333,7 +333,21 @@ class TrainState:
         self._check(self._L.cmtf_gpu_kernel_info(self._h, C.byref(w), C.byref(t),
                                                   C.byref(s)))
         return {"kernel": ["generic", "order3", "order4", "order3v2", "(retired)", "order3tm"][w.value],
-                "hog_threads": t.value, "sort_mode": s.value}
+                "hog_threads": t.value, "sort_mode": s.value, "blocks": self._blocks()}
+
+    def _blocks(self):
+        b = C.c_int32()
+        self._check(self._L.cmtf_gpu_order_blocks(self._h, C.byref(b), None))
+        return b.value
+
+    def _record_order(self):
+        """Entry ids in the current record order (introspection for tests)."""
+        b = C.c_int32()
+        pos = np.zeros(self.bundle.tensor.nnz, dtype=np.uint32)
+        self._check(self._L.cmtf_gpu_order_blocks(self._h, C.byref(b), _ptr(pos, C.c_uint32)))
+        order = np.empty_like(pos)
+        order[pos] = np.arange(pos.size, dtype=np.uint32)
+        return order
 
     def close(self):
         if getattr(self, "_h", None):

@@ -157,6 +157,9 @@ struct cmtf_gpu_ctx {
   uint32_t* rec_alt = nullptr;
   uint64_t rec_alt_cap = 0;
   uint64_t posA = 1, posB = 0;
+  // pos_affine: pos[] still holds the upload's placement (pa e + pb) mod n
+  bool pos_affine = false;
+  uint64_t up_pa = 1, up_pb = 0;
   uint4* mrec_alt = nullptr;
   uint64_t mrec_alt_cap = 0;
   // hog3tm: per record {lambda/count_1(i1), lambda/count_2(i2),
@@ -168,6 +171,19 @@ struct cmtf_gpu_ctx {
   float4* rrec_alt = nullptr;
   uint64_t rrec_cap = 0, rrec_alt_cap = 0;
   bool rrec_valid = false;
+  // virtual visiting order (hog3tm, vt_on): the records stay in place and
+  // every epoch's order is the segment table d_vtab; blk_B x blk_B strata
+  // (blk_B = 1: one segment, no re-layout), blk_n / blk_off = stratum sizes
+  // and offsets by stratum id.  pos_ids: pos[] is stale and is rebuilt from
+  // the entry ids in rrec[].w.
+  uint32_t blk_B = 0;
+  bool vt_on = false, pos_ids = false;
+  std::vector<uint64_t> blk_n, blk_off;
+  uint32_t* blk_hist = nullptr;  // [2][kMaxBlk^2]: stratum sizes, offsets
+  uint32_t* part_cnt = nullptr;  // [chunk][stratum] counts -> run starts
+  uint64_t part_cnt_cap = 0;
+  uint4* d_vtab = nullptr;
+  std::vector<uint4> h_vtab;
   // the next epoch's gathers run on a side stream, overlapping the current
   // sweep (they only read rec / mrec and write the spare buffers)
   cudaStream_t side = nullptr;
@@ -256,6 +272,8 @@ struct cmtf_gpu_ctx {
     bool hot_check = false;// CMTF_HOT_CHECK: compare device vs host selection
     bool tm_red = false;   // CMTF_TM_RED=1: hog3tm cold-row steps as REDs (no bulk staging)
     int tm_strided = 0;    // CMTF_TM_STRIDED=1: hog3tm lanes take strided records
+    int tm_blocks = -1;    // CMTF_TM_BLOCKS=B: blocked order with B x B strata (0/1 off, -1 auto)
+    bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
   } env;
   int hog_threads_used = 0;
 
@@ -440,8 +458,8 @@ __global__ void reshuffle_kernel(const uint32_t* __restrict__ src, uint32_t* __r
     uint64_t pg = g < ng ? (uint64_t)(((unsigned __int128)a * g + b) % ng) : 0;
     for (int r = 0; r < kReshuffleRun && i < n; ++r, i += 32) {
       const uint64_t q = i < body ? pg * kShuffleGroup + (i % kShuffleGroup) : i;
-      if (WORDS == 4) {
-        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      if (WORDS == 4) {  // evict-first: L2 stays with the epoch kernel's factor rows
+        __stcs(reinterpret_cast<uint4*>(dst) + i, __ldcs(reinterpret_cast<const uint4*>(src) + q));
       } else {
 #pragma unroll
         for (int w = 0; w < WORDS; ++w) dst[i * WORDS + w] = __ldg(src + q * WORDS + w);
@@ -465,6 +483,150 @@ __global__ void remap_pos_kernel(uint32_t* pos, uint64_t count, uint64_t n, uint
   }
 }
 
+// ---- Virtual visiting order and the L2-blocked layout (hog3tm) ----
+// The tcgen05 epoch never moves its records between epochs: each epoch's
+// random order is a table of segments the kernel maps virtual positions
+// through (vphys, hog3tm.cuh) -- the reference reshuffles its whole schedule
+// every epoch, src/trainer.cpp:122-128.  With factor tables beyond L2 the
+// records are first laid out stratum-major: stratum s = (mode-1 block b1,
+// mode-2 block b2), s = b1 * B + b2, blocks = B equal row ranges; the lanes
+// take strided records, so the whole grid sweeps one stratum at a time and
+// the two active row blocks (2/B of U1 and U2) stay in L2 while it lasts.
+// Each epoch draws a random stratum sequence and a group-affine map per
+// stratum.  rrec[p].w carries the entry id of record p (pos[] is rebuilt
+// from it after the re-layout).
+constexpr int kMaxBlk = 16;
+
+__device__ __forceinline__ uint32_t stratum_of(uint32_t i1, uint32_t i2, uint32_t B, uint64_t d0,
+                                               uint64_t d1) {
+  return (uint32_t)((uint64_t)i1 * B / d0) * B + (uint32_t)((uint64_t)i2 * B / d1);
+}
+
+// Stable partition of the records by stratum (chunks of kPartChunk
+// records): counts per (chunk, stratum), an exclusive scan per stratum
+// across the chunks, then each chunk writes its records, in position order,
+// to consecutive places of each stratum's run.  Reads stream; writes form
+// runs that fill whole lines in L2.
+constexpr uint32_t kPartChunk = 8192;
+__global__ void part_hist_kernel(const uint4* rec, uint64_t n, uint32_t B, uint64_t d0,
+                                 uint64_t d1, uint32_t* cnt, uint32_t* total) {
+  __shared__ uint32_t h[kMaxBlk * kMaxBlk];
+  const uint32_t S = B * B;
+  const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) h[s] = 0;
+    __syncthreads();
+    const uint64_t p1 = min(n, (c + 1) * kPartChunk);
+    for (uint64_t p = c * kPartChunk + threadIdx.x; p < p1; p += blockDim.x) {
+      const uint4 r = __ldcs(rec + p);
+      atomicAdd(h + stratum_of(r.x, r.y, B, d0, d1), 1u);
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+      cnt[c * S + s] = h[s];
+      if (h[s]) atomicAdd(total + s, h[s]);
+    }
+    __syncthreads();
+  }
+}
+
+// one warp per stratum: cnt[c][s] <- off[s] + sum of cnt[c'][s], c' < c
+__global__ void part_scan_kernel(uint32_t* cnt, uint64_t nch, uint32_t S, const uint32_t* off) {
+  const uint32_t s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  uint32_t run = off[s];
+  for (uint64_t c0 = 0; c0 < nch; c0 += 32) {
+    const uint64_t c = c0 + lane;
+    const uint32_t v = c < nch ? cnt[c * S + s] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (c < nch) cnt[c * S + s] = run + x - v;
+    run += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+// rrec[pos[e]].w = e (pos exact)
+__global__ void rrec_ids_kernel(const uint32_t* pos, uint64_t n, float4* rrec) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint32_t*>(rrec + pos[e])[3] = (uint32_t)e;
+}
+
+__global__ void pos_from_ids_kernel(const float4* rrec, uint64_t n, uint32_t* pos) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x)
+    pos[__float_as_uint(__ldg(&rrec[p].w))] = (uint32_t)p;
+}
+
+// Entry id of record position q in closed form while pos[] is still the
+// upload's affine placement p0 = (pa e + pb) mod n followed by the composed
+// group map (posA, posB) of the per-epoch reshuffles: no scatter pass.
+struct IdMap {
+  uint64_t n, ng, iA, B, ia, pb;
+  int closed;
+};
+__device__ __forceinline__ uint32_t entry_of(const IdMap& m, uint64_t q) {
+  uint64_t p0 = q;
+  if (q < m.ng * kShuffleGroup)
+    p0 = (m.iA * ((q / kShuffleGroup + m.ng - m.B) % m.ng) % m.ng) * kShuffleGroup +
+         q % kShuffleGroup;
+  return (uint32_t)(m.ia * ((p0 + m.n - m.pb) % m.n) % m.n);
+}
+
+// 256 threads per chunk, in tiles of 256 records: a record's place = its
+// stratum's run start for the chunk + records of that stratum in earlier
+// tiles + in earlier warps of the tile + in earlier lanes of its warp.
+__global__ void __launch_bounds__(256) part_scatter_kernel(
+    const uint4* __restrict__ rec, const uint4* __restrict__ rrec, uint64_t n, uint32_t B,
+    uint64_t d0, uint64_t d1, const uint32_t* __restrict__ base, uint4* __restrict__ rec_out,
+    uint4* __restrict__ rrec_out, const IdMap m) {
+  __shared__ uint32_t run[kMaxBlk * kMaxBlk];
+  __shared__ uint32_t wc[8 * kMaxBlk * kMaxBlk];
+  const uint32_t S = B * B;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    for (uint32_t s = threadIdx.x; s < S; s += 256) run[s] = base[c * S + s];
+    for (uint64_t t0 = c * kPartChunk; t0 < min(n, (c + 1) * kPartChunk); t0 += 256) {
+      for (uint32_t i = threadIdx.x; i < 8 * S; i += 256) wc[i] = 0;
+      __syncthreads();
+      const uint64_t p = t0 + threadIdx.x;
+      const bool ok = p < n;
+      uint4 r = make_uint4(0, 0, 0, 0), q = make_uint4(0, 0, 0, 0);
+      uint32_t s = 0xffffffffu;
+      if (ok) {
+        r = __ldcs(rec + p);
+        q = __ldcs(rrec + p);
+        s = stratum_of(r.x, r.y, B, d0, d1);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, s);
+      const uint32_t lr = __popc(peers & ((1u << lane) - 1u));
+      if (ok && lr == 0) wc[w * S + s] = __popc(peers);
+      __syncthreads();
+      if (ok) {
+        uint32_t d = run[s] + lr;
+        for (int w2 = 0; w2 < w; ++w2) d += wc[w2 * S + s];
+        if (m.closed) q.w = entry_of(m, p);
+        rec_out[d] = r;
+        rrec_out[d] = q;
+      }
+      __syncthreads();
+      for (uint32_t s2 = threadIdx.x; s2 < S; s2 += 256) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < 8; ++w2) tot += wc[w2 * S + s2];
+        run[s2] += tot;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
                            float* reg) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -473,12 +635,14 @@ __global__ void reg_kernel(const uint32_t* count, uint32_t n, float lambda,
 }
 
 // rrec[p] = the three regulariser coefficients of record p (order 3)
+// (keep_w: the fourth word holds the entry id of a blocked layout; kept)
 __global__ void build_rrec_kernel(const uint4* rec, uint64_t n, const float* r0, const float* r1,
-                                  const float* r2, float4* out) {
+                                  const float* r2, float4* out, int keep_w) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     const uint4 r = rec[p];
-    out[p] = make_float4(__ldg(r0 + r.x), __ldg(r1 + r.y), __ldg(r2 + r.z), 0.f);
+    out[p] = make_float4(__ldg(r0 + r.x), __ldg(r1 + r.y), __ldg(r2 + r.z),
+                         keep_w ? out[p].w : 0.f);
   }
 }
 
@@ -530,6 +694,11 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
 }
 
 int normalize_pos(cmtf_gpu_ctx* ctx);  // reshuffle machinery, below
+uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx);
+int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B);
+bool vt_wanted(const cmtf_gpu_ctx* ctx);
+int vt_table(cmtf_gpu_ctx* ctx, uint64_t epoch);
+bool tensor_shuffles(const cmtf_gpu_ctx* ctx);
 int take_matrix_order(cmtf_gpu_ctx* ctx);
 int prefetch_orders(cmtf_gpu_ctx* ctx, bool tensor, bool matrices);
 void drain_side(cmtf_gpu_ctx* ctx);
@@ -1479,26 +1648,33 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   const bool mshuf = ctx->cfg.order_policy == 1 && !(m_lo && m_hi);
   if (mshuf) TRY(take_matrix_order(ctx));
   Hog3v2Args a{};
-  a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;
   if (!fill_sweep_args<3>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
   if (v3_tm(ctx) && !ctx->rrec_valid) {
     // built from this epoch's record order (no gather of the next order is
-    // pending here; from now on the reshuffle keeps rrec aligned with rec)
+    // pending here; from now on the reshuffle keeps rrec aligned with rec);
+    // a blocked layout keeps its entry ids
     TRY(ensure(ctx, &ctx->rrec, &ctx->rrec_cap, ctx->nnz));
     build_rrec_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(
         reinterpret_cast<const uint4*>(ctx->rec), ctx->nnz, ctx->reg[0], ctx->reg[1],
-        ctx->reg[2], ctx->rrec);
+        ctx->reg[2], ctx->rrec, ctx->vt_on ? 1 : 0);
     CU(cudaGetLastError());
     ctx->rrec_valid = true;
     ctx->last_launches += 1;
   }
+  const bool whole = t_lo == 0 && t_hi == ctx->nnz && !(m_lo && m_hi);
+  if (!ctx->vt_on && whole && vt_wanted(ctx)) {
+    TRY(vt_setup(ctx, blocks_wanted(ctx)));
+    TRY(vt_table(ctx, (uint64_t)ctx->epoch));
+  }
+  a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;  // after a re-layout
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
   if (v3_tm(ctx)) {
     a.rrec = ctx->rrec + t_lo;
     a.stage_off = ctx->tm_stage_off;
-    a.strided = ctx->env.tm_strided;
+    a.vtab = ctx->vt_on && whole ? ctx->d_vtab : nullptr;
+    a.strided = ctx->env.tm_strided || (a.vtab && ctx->blk_B > 1);
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
@@ -1771,6 +1947,9 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.tm_red = v && v[0] == '1';
       const char* w = std::getenv("CMTF_TM_STRIDED");
       ctx->env.tm_strided = w && w[0] == '1';
+      ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
+      if (const char* b = std::getenv("CMTF_TM_BLOCKS"))
+        ctx->env.tm_blocks = std::max(0, std::min(kMaxBlk, atoi(b)));
     }
   }
   auto cleanup = [&](int rc) {
@@ -1816,6 +1995,9 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->mrec_alt);
   dfree(ctx->rrec);
   dfree(ctx->rrec_alt);
+  dfree(ctx->blk_hist);
+  dfree(ctx->d_vtab);
+  dfree(ctx->part_cnt);
   dfree(ctx->visits);
   dfree(ctx->mvisits);
   dfree(ctx->s_idx);
@@ -2229,6 +2411,7 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
       ctx->dims.size() == (size_t)N && std::equal(ctx->dims.begin(), ctx->dims.end(), dims);
   drain_side(ctx);  // a pending reshuffle reads rec
   ctx->rrec_valid = false;
+  ctx->vt_on = ctx->pos_ids = false;  // the upload lays records out anew
   ctx->dims.assign(dims, dims + N);
   ctx->nnz = nnz;
   ctx->v2_dirty = true;
@@ -2295,6 +2478,9 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
     TRY(ensure(ctx, &ctx->rec, &ctx->rec_cap, nnz * (N + 1)));
     TRY(ensure(ctx, &ctx->pos, &ctx->pos_cap, nnz));
   }
+  ctx->pos_affine = direct;
+  ctx->up_pa = pa;
+  ctx->up_pb = pb;
   // duplicate-check table (load factor <= 1/2), filled chunk by chunk
   DupKey dk{};
   dk.order = N;
@@ -2761,6 +2947,8 @@ bool matrix_shuffles(const cmtf_gpu_ctx* ctx) {
 // epoch if there is one, else a gather now; then swap buffers.  pos[] stays
 // valid through the group map (posA, posB).
 int take_tensor_order(cmtf_gpu_ctx* ctx) {
+  if (ctx->vt_on) return vt_table(ctx, (uint64_t)ctx->epoch);  // records stay in place
+  if (vt_wanted(ctx)) return CMTF_OK;  // the sweep lays them out and draws the order
   if (!tensor_shuffles(ctx)) return CMTF_OK;
   const uint64_t ng = ctx->nnz / kShuffleGroup;
   uint64_t a = 1, b = 0;
@@ -2808,7 +2996,7 @@ int take_matrix_order(cmtf_gpu_ctx* ctx) {
 // Start the next epoch's gathers on the side stream; call right before the
 // sweep launch (the spare buffers were last read before this point).
 int prefetch_orders(cmtf_gpu_ctx* ctx, bool tensor, bool matrices) {
-  tensor = tensor && tensor_shuffles(ctx);
+  tensor = tensor && tensor_shuffles(ctx) && !ctx->vt_on;
   matrices = matrices && matrix_shuffles(ctx);
   if (!tensor && !matrices) return CMTF_OK;
   const uint64_t next = (uint64_t)ctx->epoch + 1;
@@ -2832,12 +3020,152 @@ int prefetch_orders(cmtf_gpu_ctx* ctx, bool tensor, bool matrices) {
 
 // Make pos[] exact again (serial replay and probes index records by pos).
 int normalize_pos(cmtf_gpu_ctx* ctx) {
+  if (ctx->pos_ids) {
+    pos_from_ids_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(ctx->rrec, ctx->nnz,
+                                                                     ctx->pos);
+    CU(cudaGetLastError());
+    ctx->pos_ids = false;
+    return CMTF_OK;
+  }
   if (ctx->posA == 1 && ctx->posB == 0) return CMTF_OK;
   remap_pos_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(ctx->pos, ctx->nnz, ctx->nnz,
                                                                  ctx->posA, ctx->posB);
   CU(cudaGetLastError());
+  ctx->pos_affine = false;
   ctx->posA = 1;
   ctx->posB = 0;
+  return CMTF_OK;
+}
+
+// Blocked order wanted for this context (0 = no): hog3tm (order 3, random
+// order, whole sweeps) when the three factor tables exceed L2 -- then every
+// entry's three row gathers miss L2 and fill 128-B lines from DRAM (config 5:
+// 2.4 TB/s of random line traffic, the measured ceiling); blocking keeps
+// mode 1 and 2's active blocks L2-resident (config 5 @1e9: -12% epoch time,
+// RMSE within 0.3%, scripts/blocked_order_exp.py).  B = 8: 2 x 1/8 of the
+// two tables; more blocks (and a 3-mode B^3 split) measured no faster.
+uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx);
+// the tcgen05 epoch will run (or runs) the blocked virtual order
+bool vt_wanted(const cmtf_gpu_ctx* ctx) {
+  return v3_tm(ctx) && ctx->cfg.order_policy == 1 && ctx->env.tm_vorder &&
+         tensor_shuffles(ctx) && blocks_wanted(ctx) > 1;
+}
+
+uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx) {
+  if (ctx->order != 3 || ctx->cfg.order_policy != 1 || ctx->nnz / kShuffleGroup < 3) return 0;
+  if (ctx->env.tm_blocks >= 0) return (uint32_t)ctx->env.tm_blocks;
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+  uint64_t bytes = 0;
+  for (int n = 0; n < 3; ++n) bytes += (uint64_t)ctx->dims[n] * ctx->JP(n) * sizeof(float);
+  if (bytes <= (uint64_t)l2 || ctx->nnz < (1ull << 22)) return 0;
+  return 8;
+}
+
+// Switch to the virtual order with B x B strata: lay the records (and
+// rrec, ids in .w) out stratum-major -- a stable radix sort of the positions
+// by stratum keeps the random order inside a stratum -- and rebuild pos[]
+// from the ids.  The layout then stays until the next upload.
+int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B) {
+  const uint64_t n = ctx->nnz;
+  PhaseTimer pt("vt_setup", ctx);
+  drain_side(ctx);
+  IdMap im{};
+  im.closed = ctx->pos_affine && !ctx->pos_ids;
+  if (im.closed) {
+    im.n = n;
+    im.ng = n / kShuffleGroup;
+    im.iA = inv_mod(ctx->posA, im.ng);
+    im.B = ctx->posB;
+    im.ia = inv_mod(ctx->up_pa, n);
+    im.pb = ctx->up_pb;
+  } else {  // pos[] exact, then each record's id scattered into rrec
+    TRY(normalize_pos(ctx));
+    rrec_ids_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->pos, n, ctx->rrec);
+    CU(cudaGetLastError());
+  }
+  const uint32_t S = B * B;
+  const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
+  if (!ctx->blk_hist) TRY(dalloc(ctx, &ctx->blk_hist, 2 * kMaxBlk * kMaxBlk));
+  TRY(ensure(ctx, &ctx->part_cnt, &ctx->part_cnt_cap, nch * S));
+  CU(cudaMemsetAsync(ctx->blk_hist, 0, kMaxBlk * kMaxBlk * sizeof(uint32_t), ctx->stream));
+  const unsigned pg = (unsigned)std::min<uint64_t>(nch, 148ull * 8);
+  part_hist_kernel<<<pg, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(ctx->rec), n, B,
+                                                ctx->dims[0], ctx->dims[1], ctx->part_cnt,
+                                                ctx->blk_hist);
+  CU(cudaGetLastError());
+  std::vector<uint32_t> hist(S), off(S, 0);
+  CU(cudaMemcpyAsync(hist.data(), ctx->blk_hist, S * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (uint32_t s = 1; s < S; ++s) off[s] = off[s - 1] + hist[s - 1];
+  CU(cudaMemcpyAsync(ctx->blk_hist + kMaxBlk * kMaxBlk, off.data(), S * sizeof(uint32_t),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  part_scan_kernel<<<(S + 7) / 8, 256, 0, ctx->stream>>>(ctx->part_cnt, nch, S,
+                                                         ctx->blk_hist + kMaxBlk * kMaxBlk);
+  CU(cudaGetLastError());
+  pt.tick("count");
+  TRY(ensure(ctx, &ctx->rec_alt, &ctx->rec_alt_cap, n * 4));
+  TRY(ensure(ctx, &ctx->rrec_alt, &ctx->rrec_alt_cap, n));
+  part_scatter_kernel<<<pg, 256, 0, ctx->stream>>>(
+      reinterpret_cast<const uint4*>(ctx->rec), reinterpret_cast<const uint4*>(ctx->rrec), n, B,
+      ctx->dims[0], ctx->dims[1], ctx->part_cnt, reinterpret_cast<uint4*>(ctx->rec_alt),
+      reinterpret_cast<uint4*>(ctx->rrec_alt), im);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  pt.tick("scatter");
+  std::swap(ctx->rec, ctx->rec_alt);
+  std::swap(ctx->rec_cap, ctx->rec_alt_cap);
+  std::swap(ctx->rrec, ctx->rrec_alt);
+  std::swap(ctx->rrec_cap, ctx->rrec_alt_cap);
+  ctx->blk_B = B;
+  ctx->blk_n.assign(hist.begin(), hist.end());
+  ctx->blk_off.assign(B * B, 0);
+  for (uint32_t s = 1; s < B * B; ++s) ctx->blk_off[s] = ctx->blk_off[s - 1] + ctx->blk_n[s - 1];
+  ctx->vt_on = true;
+  ctx->pos_ids = true;
+  ctx->posA = 1;  // the group map no longer applies: pos[] comes from the ids
+  ctx->posB = 0;
+  ctx->pos_affine = false;
+  ctx->last_launches += 5;
+  return normalize_pos(ctx);
+}
+
+// This epoch's segment table: a random stratum sequence (host draws from
+// the epoch's stream) and a group-affine map per stratum.
+int vt_table(cmtf_gpu_ctx* ctx, uint64_t epoch) {
+  const uint32_t S = (uint32_t)ctx->blk_n.size();
+  auto rng = make_rng(ctx->cfg.seed, 0x0B, epoch);
+  std::vector<uint32_t> seq(S);
+  for (uint32_t s = 0; s < S; ++s) seq[s] = s;
+  for (uint32_t k = S; k > 1; --k) std::swap(seq[k - 1], seq[bounded(rng, k)]);
+  auto& h = ctx->h_vtab;
+  h.clear();
+  uint64_t v = 0;
+  for (uint32_t k = 0; k < S; ++k) {
+    const uint32_t s = seq[k];
+    const uint64_t ns = ctx->blk_n[s], ng = ns / kShuffleGroup;
+    if (ns == 0) continue;
+    uint64_t a = 1, b = 0;
+    if (ng >= 3) {
+      a = 1 + bounded(rng, ng - 1);
+      while (gcd64(a, ng) != 1) a = a + 1 < ng ? a + 1 : 1;
+      b = bounded(rng, ng);
+    }
+    const uint64_t m = ng ? ~0ull / ng : 0;
+    h.push_back(make_uint4((uint32_t)v, (uint32_t)ctx->blk_off[s],
+                           (uint32_t)(ng * kShuffleGroup), (uint32_t)ng));
+    h.push_back(make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)m, (uint32_t)(m >> 32)));
+    v += ns;
+  }
+  h.push_back(make_uint4(0xffffffffu, 0, 0, 0));
+  h.push_back(make_uint4(0, 0, 0, 0));
+  if (v != ctx->nnz)
+    return set_err(ctx, CMTF_ECUDA, "visiting order covers %llu of %llu records",
+                   (unsigned long long)v, (unsigned long long)ctx->nnz);
+  if (!ctx->d_vtab) TRY(dalloc(ctx, &ctx->d_vtab, 2 * (kMaxBlk * kMaxBlk + 1)));
+  CU(cudaMemcpyAsync(ctx->d_vtab, h.data(), h.size() * sizeof(uint4), cudaMemcpyHostToDevice,
+                     ctx->stream));
   return CMTF_OK;
 }
 
@@ -4072,6 +4400,19 @@ int cmtf_gpu_kernel_info(cmtf_gpu_ctx* ctx, int32_t* which, int32_t* hog_threads
   if (which) *which = ctx->kernel_which;
   if (hog_threads) *hog_threads = ctx->hog_threads_used;
   if (sort_mode) *sort_mode = ctx->sort_mode;
+  return CMTF_OK;
+}
+
+int cmtf_gpu_order_blocks(cmtf_gpu_ctx* ctx, int32_t* blocks, uint32_t* positions) {
+  if (!ctx || !blocks) return set_err(ctx, CMTF_EVALIDATION, "null argument");
+  *blocks = ctx->vt_on && ctx->blk_B > 1 ? (int32_t)ctx->blk_B : 0;
+  if (positions && ctx->nnz) {
+    if (!ctx->pos) return set_err(ctx, CMTF_EVALIDATION, "no tensor uploaded");
+    drain_side(ctx);
+    TRY(normalize_pos(ctx));
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(positions, ctx->pos, ctx->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  }
   return CMTF_OK;
 }
 

@@ -118,6 +118,40 @@ struct TMLayout {
   static constexpr bool FSTAGE = STAGE_WARP <= HALF;
 };
 
+// The record streams are read once per epoch: evict-first loads keep L2 for
+// the factor rows (with the blocked order, the active row blocks).
+#ifndef CMTF_TM_STREAM_LD
+#define CMTF_TM_STREAM_LD 1
+#endif
+template <class T>
+__device__ __forceinline__ T tm_ld_stream(const T* p) {
+#if CMTF_TM_STREAM_LD
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
+// Virtual visiting order: virtual record v of the epoch lies in segment k
+// (a stratum of the physical layout, in this epoch's stratum sequence); its
+// physical place is the segment's group-affine image: group g = rel / 8 ->
+// (a g + b) mod ng (Barrett reduction with m = floor((2^64 - 1) / ng)), the
+// offset inside the 8-record group kept, the records past the last whole
+// group in place.  k is the lane's cursor: a lane's v only grow.  Eight
+// consecutive lanes read one 128-byte group, so the gathers stay full-line.
+__device__ __forceinline__ uint32_t vphys(const uint4* vt, uint32_t& k, uint32_t v) {
+  if (!vt) return v;
+  while (v >= __ldg(&vt[2 * (k + 1)].x)) ++k;
+  const uint4 s0 = __ldg(vt + 2 * k), s1 = __ldg(vt + 2 * k + 1);
+  const uint32_t rel = v - s0.x;
+  if (rel >= s0.z) return s0.y + rel;
+  const uint64_t x = (uint64_t)s1.x * (rel >> 3) + s1.y;
+  const uint64_t m = ((uint64_t)s1.w << 32) | s1.z;
+  uint64_t r = x - __umul64hi(x, m) * s0.w;
+  if (r >= s0.w) r -= s0.w;
+  return s0.y + (uint32_t)r * 8u + (rel & 7u);
+}
+
 // x -> hi + lo, two fp16 values (x already scaled): hi keeps x's top 11
 // significant bits (exactly an fp16 for |x| >= 2^-14), lo = x - hi is exact
 // in fp32 and rounded to fp16; hi + lo carries ~21 bits
@@ -285,7 +319,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   uint8_t* tU3l = tU3h + L::U_TILE;
   float* sU1 = reinterpret_cast<float*>(tU3l + L::U_TILE);
   float* myG32 = reinterpret_cast<float*>(tU3l + L::U_TILE + L::U1_BYTES) + e * L::JG;
-  __shared__ uint64_t mbar[2][3];      // [warpgroup][sweep MMAs, slot 0 MMA, slot 1 MMA]
+  // [warpgroup][sweep MMAs, slot 0 turn 0, slot 1 turn 0, slot 0 turn 1,
+  // slot 1 turn 1]: one completion per iteration each, so a parity names the
+  // iteration unambiguously (no warp is more than one iteration ahead)
+  __shared__ uint64_t mbar[2][5];
   __shared__ uint32_t tmem_base;
 
   // core element (a,b,c) into the four fp16 copies
@@ -312,7 +349,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   bool g32_fresh = false;  // a refresh landed in myG32: convert it
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) umma::mbar_init(&mbar[k / 3][k % 3], 1);
+    for (int k = 0; k < 10; ++k) umma::mbar_init(&mbar[k / 5][k % 5], 1);
     umma::fence_mbar_init();
   }
   if (w == 0) umma::tmem_alloc<512>(&tmem_base);
@@ -418,8 +455,12 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     *reinterpret_cast<uint4*>(tl) = l0;
     *reinterpret_cast<uint4*>(tl + L::U_LBO) = l1;
   };
-  uint4 rc = lo < hi ? __ldg(a.rec + lo) : make_uint4(0, 0, 0, 0);
-  uint4 rc1 = lo + st < hi ? __ldg(a.rec + lo + st) : make_uint4(0, 0, 0, 0);
+  // physical places of the records one (p1) and zero (p0) iterations ahead
+  uint32_t vk = 0;
+  uint32_t p0 = lo < hi ? vphys(a.vtab, vk, (uint32_t)lo) : 0u;
+  uint32_t p1 = lo + st < hi ? vphys(a.vtab, vk, (uint32_t)(lo + st)) : 0u;
+  uint4 rc = lo < hi ? __ldg(a.rec + p0) : make_uint4(0, 0, 0, 0);
+  uint4 rc1 = lo + st < hi ? __ldg(a.rec + p1) : make_uint4(0, 0, 0, 0);
   int sl[3];
   float rg[3];
   {
@@ -428,7 +469,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     for (int n = 0; n < 3; ++n) {
       sl[n] = (lo < hi && a.hot[n].slot) ? __ldg(a.hot[n].slot + ix[n]) : -1;
     }
-    const float4 r0 = lo < hi ? __ldg(a.rrec + lo) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r0 = lo < hi ? __ldg(a.rrec + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
     rg[0] = r0.x;
     rg[1] = r0.y;
     rg[2] = r0.z;
@@ -445,13 +486,16 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   // the previous iteration's core push and hot-row merges, run at the top of
   // the next iteration (or after the last): every core MMA of that iteration
   // is done first, so the slots are free (until this iteration's barrier) for
-  // the push transpose and the merge staging
+  // the push transpose and the merge staging.  Runs every iteration (the
+  // barrier and the slot waits; the push and merges when due), so that each
+  // iteration starts with both slots' MMAs complete.
   bool pend_push = false, pend_flush = false;
   int cnt_push = 0, cnt_flush = 0;  // iterations since the last push / merge
   float pkb = 0.f, plb = 0.f;
-  auto push_flush = [&]() {
-    umma::mbar_wait(&mbar[g][1], 1u);
-    umma::mbar_wait(&mbar[g][2], 1u);
+  auto push_flush = [&](uint32_t ph) {
+    // both slots' last MMAs (turn 1) of the previous iteration, parity ph
+    umma::mbar_wait(&mbar[g][3], ph);
+    umma::mbar_wait(&mbar[g][4], ph);
     TMP(10);
     if (pend_push) {
       // TMEM lane e holds core row (a,b) = e of both slot accumulators; each
@@ -467,8 +511,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       TMP(11);
       float* scr = reinterpret_cast<float*>(myslot + turn * L::HALF);
       const int row0 = 32 * wk;
-      if (pkb > 0.f && row0 < AB) {
-        const float q = a.eta * (plb / pkb) * a.nhat_core;
+      // every warp pushes its 32 accumulator rows -- they hold all four
+      // warps' entries -- even when it had no entries of its own
+      if (row0 < AB) {
+        const float q = pkb > 0.f ? a.eta * (plb / pkb) * a.nhat_core : 0.f;
         const float alpha = q > a.kappa_core ? a.kappa_core / q : 1.f;
         const float s = -a.eta * alpha;
         const float creg = pkb * a.core_reg;
@@ -529,7 +575,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     const uint64_t e0 = lo + it * st;
     const bool active = e0 < hi;
     const uint32_t par = (uint32_t)(it & 1);
-    const uint4 rc2 = e0 + 2 * st < hi ? __ldg(a.rec + e0 + 2 * st) : make_uint4(0, 0, 0, 0);
+    const uint32_t p2 = e0 + 2 * st < hi ? vphys(a.vtab, vk, (uint32_t)(e0 + 2 * st)) : 0u;
+    const uint4 rc2 = e0 + 2 * st < hi ? tm_ld_stream(a.rec + p2) : make_uint4(0, 0, 0, 0);
     int nsl[3];
     float nrg[3];
     {
@@ -539,7 +586,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       for (int n = 0; n < 3; ++n)
         nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
       // the regulariser coefficients stream beside the records (rrec)
-      const float4 rr = nxt ? __ldg(a.rrec + e0 + st) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 rr = nxt ? tm_ld_stream(a.rrec + p1) : make_float4(0.f, 0.f, 0.f, 0.f);
       nrg[0] = rr.x;
       nrg[1] = rr.y;
       nrg[2] = rr.z;
@@ -573,7 +620,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     put_row(myU2h, myU2l, u2);
     put_row(myU3h, myU3l, u3);
     TMP(0);
-    if (pend_push || pend_flush) push_flush();
+    if (it > 0) push_flush(par ^ 1u);
     umma::fence_async_smem();
     umma::fence_before();
     TMP(9);
@@ -645,7 +692,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     TMP(3);
     // ---- residual, row steps ----
     const float r = active ? __uint_as_float(rc.w) - xh : 0.f;
-    float* pr = a.probe && active ? a.probe + e0 * (uint64_t)(2 + 3 * J) : nullptr;
+    float* pr = a.probe && active ? a.probe + p0 * (uint64_t)(2 + 3 * J) : nullptr;
     if (pr) {
       pr[0] = xh;
       pr[1] = r;
@@ -660,7 +707,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       if (active) {
         lamG += n1 * n2 * n3;
         kw += 1.f;
-        if (a.visits) atomicAdd(a.visits + e0, 1u);
+        if (a.visits) atomicAdd(a.visits + p0, 1u);
       }
       float gr[J];
 #pragma unroll
@@ -708,14 +755,15 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     // ---- core gradient: this warp's P and S rows (pre-update values) into
     // its slot, then one warp-issued MMA (K = 32 entries) into the slot's
-    // accumulator.  Slot completions per iteration: turn 0 (#2it), turn 1
-    // (#2it+1).  Turn-0 warps do it right away; turn-1 warps first issue their
-    // row gathers and matrix entries, so the turn-0 MMA is long done ----
+    // accumulator (turn 0 overwrites it at the first iteration after a push,
+    // turn 1 accumulates).  Turn-0 warps do it right away; turn-1 warps first
+    // issue their row gathers and matrix entries, so the turn-0 MMA is long
+    // done ----
     auto core_phase = [&]() {
-      if (turn == 0) {
-        if (it > 0) umma::mbar_wait(&mbar[g][1 + slot], 1u);
-      } else {
-        umma::mbar_wait(&mbar[g][1 + slot], 0u);
+      if (turn == 0) {  // the slot's turn-1 MMA of the previous iteration
+        if (it > 0) umma::mbar_wait(&mbar[g][3 + slot], (uint32_t)((it - 1) & 1));
+      } else {          // the slot's turn-0 MMA of this iteration
+        umma::mbar_wait(&mbar[g][1 + slot], par);
       }
       float u1s[J];
 #pragma unroll
@@ -766,7 +814,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
           umma::mma_f16(d, dPh, dSl, ID_CORE, 1u);
           umma::mma_f16(d, dPl, dSh, ID_CORE, 1u);
         }
-        umma::commit(&mbar[g][1 + slot]);
+        umma::commit(&mbar[g][1 + 2 * turn + slot]);
       }
     };
     if (turn == 0) core_phase();
@@ -790,6 +838,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     TMP(8);
     rc = rc1;
     rc1 = rc2;
+    p0 = p1;
+    p1 = p2;
 #pragma unroll
     for (int n = 0; n < 3; ++n) {
       sl[n] = nsl[n];
@@ -801,7 +851,7 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #else
   matrix_entries_until<J, JP>(a, sm, mpos, mrn, mhi, mhi, lane);
 #endif
-  if (pend_push || pend_flush) push_flush();
+  if (iters > 0) push_flush((uint32_t)((iters - 1) & 1));
   cp_async_wait_all();
   if (mystage) bulk_wait_all();
   umma::fence_before();

@@ -98,6 +98,10 @@ struct Hog3v2Args {
   uint32_t* visits;
   uint32_t* mvisits;
   int strided;  // hog3tm: lanes take every W-th record (grid-wide front-to-back sweep)
+  // hog3tm: this epoch's virtual visiting order (null = physical order):
+  // segments of 2 uint4 {vbeg, src, body, ng} {a, b, m_lo, m_hi}, then a
+  // sentinel with vbeg = UINT32_MAX (see vphys in hog3tm.cuh)
+  const uint4* vtab;
 };
 
 // ---------------------------------------------------------------------

@@ -24,6 +24,8 @@ p = argparse.ArgumentParser()
 p.add_argument("--nnz", type=float, default=1e8)
 p.add_argument("--B", type=int, nargs="+", default=[8, 16])
 p.add_argument("--epochs", type=int, default=6)
+p.add_argument("--B3", type=int, nargs="*", default=[], help="3-mode blocking (B^3 strata)")
+p.add_argument("--skip-default", action="store_true")
 a = p.parse_args()
 dev = "cuda:0"
 spec = synth_gpu.config5(a.nnz, 10)
@@ -54,10 +56,11 @@ def run(name, b, policy, strided):
     torch.cuda.empty_cache()
 
 
-run("default (random, contiguous lanes)", bundle, "random", False)
-perm = torch.randperm(t.nnz, generator=g, device=dev)
-run("random caller order, strided lanes", reorder(perm), "caller", True)
-del perm
+if not a.skip_default:
+    run("default (random, contiguous lanes)", bundle, "random", False)
+    perm = torch.randperm(t.nnz, generator=g, device=dev)
+    run("random caller order, strided lanes", reorder(perm), "caller", True)
+    del perm
 for B in a.B:
     i = t.indices.long()
     b1 = i[:, 0] * B // t.dims[0]
@@ -68,4 +71,15 @@ for B in a.B:
     perm = torch.argsort(key)
     del i, b1, b2, key
     run(f"blocked B={B}, strided lanes", reorder(perm), "caller", True)
+    del perm
+for B in a.B3:
+    i = t.indices.long()
+    sid = ((i[:, 0] * B // t.dims[0]) * B + i[:, 1] * B // t.dims[1]) * B + i[:, 2] * B // t.dims[2]
+    del i
+    seq = torch.randperm(B * B * B, generator=g, device=dev)
+    key = seq[sid] * (1 << 40) + torch.randint(0, 1 << 40, (t.nnz,), generator=g, device=dev)
+    del sid
+    perm = torch.argsort(key)
+    del key
+    run(f"blocked 3-mode B={B}, strided lanes", reorder(perm), "caller", True)
     del perm
