@@ -274,6 +274,8 @@ struct cmtf_gpu_ctx {
     int tm_strided = 0;    // CMTF_TM_STRIDED=1: hog3tm lanes take strided records
     int tm_blocks = -1;    // CMTF_TM_BLOCKS=B: blocked order with B x B strata (0/1 off, -1 auto)
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
+    int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
+    bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
   } env;
   int hog_threads_used = 0;
 
@@ -1520,8 +1522,13 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   }
   // hog3tm: per-thread staging rows for the bulk asynchronous row steps
   // (3 rows x JP floats per thread) when they fit beside the hot replicas
+  // Not with the L2-blocked order: its mode-1/2 rows are L2-resident and
+  // REDs on them are cheap, while each bulk reduction costs the issuing warp
+  // a 32-lane uniform-operand loop (config 5 @1e9: 244 -> 213 ms/epoch with
+  // REDs; config 3 unchanged).  CMTF_TM_BULK overrides.
   ctx->tm_stage_off = 0;
-  if (tm3 && !ctx->cfg.nonnegative && !ctx->env.tm_red) {
+  const bool want_bulk = ctx->env.tm_bulk > 0 || (ctx->env.tm_bulk < 0 && !vt_wanted(ctx));
+  if (tm3 && !ctx->cfg.nonnegative && !ctx->env.tm_red && want_bulk) {
     const uint32_t so = (off + 3) & ~3u;
     const size_t need = (size_t)(so + 256 * 3 * JP) * sizeof(float);
     if (need <= limit) {
@@ -1673,6 +1680,8 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   if (v3_tm(ctx)) {
     a.rrec = ctx->rrec + t_lo;
     a.stage_off = ctx->tm_stage_off;
+    a.bulk_mask = ctx->env.tm_bulk >= 0 ? ctx->env.tm_bulk : 7;
+    a.g_alt = ctx->env.tm_galt ? 1 : 0;
     a.vtab = ctx->vt_on && whole ? ctx->d_vtab : nullptr;
     a.strided = ctx->env.tm_strided || (a.vtab && ctx->blk_B > 1);
     ctx->kernel_which = 5;
@@ -1950,6 +1959,8 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
       if (const char* b = std::getenv("CMTF_TM_BLOCKS"))
         ctx->env.tm_blocks = std::max(0, std::min(kMaxBlk, atoi(b)));
+      if (const char* b = std::getenv("CMTF_TM_BULK")) ctx->env.tm_bulk = atoi(b) & 7;
+      ctx->env.tm_galt = !off("CMTF_TM_GALT");
     }
   }
   auto cleanup = [&](int rc) {

@@ -522,7 +522,12 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         // the shared copies follow the global core every kRefresh pushes
         // (and right away in nonnegative mode); the refresh read is issued
         // before this push's REDs and gets this push's own delta added
-        const bool refresh = ++npush % kRefresh == 0;
+        // (g_alt: the shared fp16 copies are common to both warpgroups, so
+        // they take turns -- each refresh is converted once, and the copies
+        // still follow the global core every push of either warpgroup)
+        ++npush;
+        const bool refresh =
+            a.g_alt ? (npush + (uint32_t)g) % (2 * kRefresh) == 0 : npush % kRefresh == 0;
         if (e < AB) {
 #pragma unroll
           for (int c = 0; c < J; ++c) {
@@ -717,21 +722,21 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
         for (int k = 0; k < J; ++k) pr[2 + k] = gr[k];
       if (mystage) bulk_wait_read();  // the previous entry's reductions read their staging
       tm_step_row<J, JP>(a.U[0], rc.x, sl[0], const_cast<float*>(rep[0]), stat[0], active, u1, gr,
-                         a.eta, a.nonneg, c1, mystage);
+                         a.eta, a.nonneg, c1, (a.bulk_mask & 1) ? mystage : nullptr);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g2[k], rg[1] * u2[k]);
       if (pr)
 #pragma unroll
         for (int k = 0; k < J; ++k) pr[2 + J + k] = gr[k];
       tm_step_row<J, JP>(a.U[1], rc.y, sl[1], const_cast<float*>(rep[1]), stat[1], active, u2, gr,
-                         a.eta, a.nonneg, c2, mystage ? mystage + JP : nullptr);
+                         a.eta, a.nonneg, c2, mystage && (a.bulk_mask & 2) ? mystage + JP : nullptr);
 #pragma unroll
       for (int k = 0; k < J; ++k) gr[k] = fmaf(-r, g3[k], rg[2] * u3[k]);
       if (pr)
 #pragma unroll
         for (int k = 0; k < J; ++k) pr[2 + 2 * J + k] = gr[k];
       tm_step_row<J, JP>(a.U[2], rc.z, sl[2], const_cast<float*>(rep[2]), stat[2], active, u3, gr,
-                         a.eta, a.nonneg, c3, mystage ? mystage + 2 * JP : nullptr);
+                         a.eta, a.nonneg, c3, mystage && (a.bulk_mask & 4) ? mystage + 2 * JP : nullptr);
       if (mystage) bulk_commit();
     }
 

@@ -97,6 +97,8 @@ struct Hog3v2Args {
   // tensor record (indexed like rec) / matrix record (indexed like mrec)
   uint32_t* visits;
   uint32_t* mvisits;
+  int g_alt;      // hog3tm: the two warpgroups take turns converting core refreshes
+  int bulk_mask;  // hog3tm: modes (bit n) whose cold-row steps use the bulk staging
   int strided;  // hog3tm: lanes take every W-th record (grid-wide front-to-back sweep)
   // hog3tm: this epoch's virtual visiting order (null = physical order):
   // segments of 2 uint4 {vbeg, src, body, ng} {a, b, m_lo, m_hi}, then a
