@@ -6,7 +6,7 @@
 
 namespace cmtfb {
 
-constexpr int kMaxOrder = 8;     // device kernels; the reference allows 16
+constexpr int kMaxOrder = 16;    // as the reference (src/gradients.cpp:14, src/tucker.cpp:13)
 constexpr int kMaxRank = 64;     // per-mode rank bound of the device path
 constexpr int kEvalBlock = 1024; // src/eval.cpp:10 (kBlock)
 

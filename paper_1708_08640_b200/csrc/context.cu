@@ -2924,6 +2924,14 @@ int launch_tensor_gather(cmtf_gpu_ctx* ctx, uint64_t epoch, cudaStream_t st, uin
     case 7: launch_reshuffle<7>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
     case 8: launch_reshuffle<8>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
     case 9: launch_reshuffle<9>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 10: launch_reshuffle<10>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 11: launch_reshuffle<11>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 12: launch_reshuffle<12>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 13: launch_reshuffle<13>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 14: launch_reshuffle<14>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 15: launch_reshuffle<15>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 16: launch_reshuffle<16>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
+    case 17: launch_reshuffle<17>(ctx->rec, ctx->rec_alt, n, *a, *b, st); break;
     default: return set_err(ctx, CMTF_EUNSUPPORTED, "order %d", ctx->order);
   }
   if (ctx->rrec_valid) {

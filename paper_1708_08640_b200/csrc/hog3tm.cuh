@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   const uint64_t iters = (a.nnz + Wt - 1) / Wt;
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
+  MatSched msched;  // warp-uniform interleaving of the matrix entries (hog3v2.cuh)
+  msched.init(mlo, mhi, (a.nnz + Wt - 1) / Wt);
 #if CMTF_TM_MPF
   MatPrefetch mpf;
   mat_prefetch_init<JP>(a, mpf, mlo, mhi);
@@ -830,12 +832,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 
     TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----
+    const uint64_t mdue = mlo + msched.step();
 #if CMTF_TM_MPF
-    matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
-                                   lane);
+    matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mdue, mhi, lane);
 #else
-    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
-                                lane);
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mdue, mhi, lane);
 #endif
     TMP(7);
     if (turn == 1) core_phase();

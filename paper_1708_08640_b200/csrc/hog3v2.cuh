@@ -682,6 +682,34 @@ __device__ __forceinline__ void matrix_entries_until_pf(const Args& a, float* sm
   }
 }
 
+// Even interleaving of a lane's matrix entries with its tensor iterations on
+// a WARP-uniform schedule.  The lanes' matrix counts differ by at most one;
+// with per-lane schedules (count * (it + 1) / iters) the due iterations drift
+// apart over the epoch and nearly every iteration runs the matrix path for a
+// few lanes only (config 5: 3.5 of 32, a synchronous row fetch each time).
+// All lanes follow the warp's largest count instead and step together; the
+// quotient is kept incrementally (no 64-bit division per iteration).
+// 32-bit counters: iters <= nnz / 256 < 2^24; a lane's matrix entries beyond
+// 2^31 - 1 -- none in practice -- are swept after the loop.
+struct MatSched {
+  uint32_t cnt_l, cnt_w, iters, acc, rel;
+  __device__ __forceinline__ void init(uint64_t mlo, uint64_t mhi, uint64_t n_iters) {
+    cnt_l = (uint32_t)(mhi - mlo < 0x7fffffffull ? mhi - mlo : 0x7fffffffull);
+    cnt_w = __reduce_max_sync(0xffffffffu, cnt_l);
+    iters = (uint32_t)(n_iters < 0x7fffffffull ? n_iters : 0x7fffffffull);
+    acc = rel = 0;
+  }
+  // entries of this lane due by the end of the next iteration (relative)
+  __device__ __forceinline__ uint32_t step() {
+    acc += cnt_w;
+    while (acc >= iters) {
+      acc -= iters;
+      ++rel;
+    }
+    return rel < cnt_l ? rel : cnt_l;
+  }
+};
+
 // Matrix entries of this lane up to `due`, in lockstep across the warp.
 template <int J, int JP, class Args>
 __device__ __forceinline__ void matrix_entries_until(const Args& a, float* sm, uint64_t& mpos,
@@ -758,6 +786,8 @@ hog3v2_kernel(Hog3v2Args a) {
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
   uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+  MatSched msched;
+  msched.init(mlo, mhi, iters);
   float kw = 0.f;      // entries since the warp's last core flush (lane-local)
   float lamG = 0.f;    // sum |phi|^2 since the last flush (lane-local)
 
@@ -1029,8 +1059,7 @@ hog3v2_kernel(Hog3v2Args a) {
     issue_rows(rc1, nsl, e0 + E);
 
     // ---- matrix entries due by this iteration (interleaved) ----
-    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
-                                lane);
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + msched.step(), mhi, lane);
 
 #pragma unroll
     for (int j = 0; j < E; ++j) {

@@ -128,6 +128,8 @@ hog4_kernel(Hog4Args a) {
   const uint64_t mlo = a.mnnz * gl / Wt, mhi = a.mnnz * (gl + 1) / Wt;
   uint64_t mpos = mlo;
   uint4 mrn = mlo < mhi ? __ldg(a.mrec + mphys(a, mlo)) : make_uint4(0, 0, 0, 0);
+  MatSched msched;
+  msched.init(mlo, mhi, iters);
   float kw = 0.f, lamG = 0.f;
   float acc[J][2];  // dG[a=w][b][c=2t4 (+1)][d=g8] since the last push
 #pragma unroll
@@ -667,8 +669,7 @@ hog4_kernel(Hog4Args a) {
     }
 
     // ---- interleaved matrix entries ----
-    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + (mhi - mlo) * (it + 1) / iters, mhi,
-                                lane);
+    matrix_entries_until<J, JP>(a, sm, mpos, mrn, mlo + msched.step(), mhi, lane);
 
     // ---- damped block-level core push of slab a = w, refresh from global ----
     if (push) {

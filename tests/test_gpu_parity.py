@@ -333,6 +333,43 @@ def test_order4_and_ragged_ranks_use_generic_path():
     assert st2.kernel_info()["kernel"] == "generic"
 
 
+@pytest.mark.parametrize("order,ranks", [(9, [2] * 9), (12, [2, 1, 2, 2, 1, 2, 2, 2, 1, 2, 2, 2]),
+                                         (16, [2, 1] * 8)])
+def test_orders_up_to_16_like_the_reference(order, ranks):
+    """The reference's order bound is 16 (src/gradients.cpp:14, src/tucker.cpp:13):
+    serial epoch vs the oracle, evaluation, and a Hogwild sweep beyond order 8."""
+    rng = np.random.default_rng(order)
+    dims = [3 + (n % 4) for n in range(order)]
+    idx = np.unique(np.stack([rng.integers(0, d, 700) for d in dims], 1), axis=0)
+    vals = rng.uniform(0, 2, idx.shape[0])
+    b = api.DataBundle(api.SparseTensor(dims, idx, vals), [])
+    cfg = TrainConfig(ranks=ranks, seed=3, eta0=0.01, exec_mode="serial")
+    st = api.make_state(cfg, b)
+    tr = O.SerialTrainer(b, ranks, seed=3, eta0=0.01, mu=0.1, lambda_reg=0.1)
+    tr.model.copy_from(st.model)
+    ref_rmse, ref_obj = O.epoch_stats(b, tr.model, 0.1)
+    s_gpu = api.epoch_stats(st, 0.1)
+    assert abs(s_gpu.train_rmse - ref_rmse) <= 1e-5 * ref_rmse
+    assert abs(s_gpu.objective - ref_obj) <= 1e-5 * ref_obj
+    tr.run_epoch()
+    api.run_epoch(st)
+    m = st.model
+    for a, ref in zip([m.core.reshape(-1)] + m.factors, [tr.model.core] + tr.model.factors):
+        scale_close(a, ref, 1e-2 * np.abs(ref).max(), 1e-4)
+    st2 = api.make_state(TrainConfig(ranks=ranks, seed=3, eta0=0.01), b)
+    o0 = api.epoch_stats(st2, 0.1).objective
+    for _ in range(3):
+        api.run_epoch(st2)
+    assert api.epoch_stats(st2, 0.1).objective < o0
+    # one past the bound is refused like the reference (ValidationError)
+    if order == 16:
+        d17 = dims + [2]
+        i17 = np.concatenate([idx, np.zeros((idx.shape[0], 1), idx.dtype)], 1)
+        with pytest.raises(api.ValidationError):
+            api.make_state(TrainConfig(ranks=ranks + [1]),
+                           api.DataBundle(api.SparseTensor(d17, i17, vals), []))
+
+
 def test_nonnegative_clamp_keeps_parameters_nonnegative():
     spec = synth.config1(literal=False)
     spec.nnz, spec.dims = 5000, [50, 50, 50]
