@@ -273,6 +273,8 @@ struct cmtf_gpu_ctx {
     bool tm_red = false;   // CMTF_TM_RED=1: hog3tm cold-row steps as REDs (no bulk staging)
     int tm_strided = 0;    // CMTF_TM_STRIDED=1: hog3tm lanes take strided records
     int tm_blocks = -1;    // CMTF_TM_BLOCKS=B: blocked order with B x B strata (0/1 off, -1 auto)
+    int tm_seq = 1;        // CMTF_TM_SEQ=0: random stratum sequence (1: mode-1-block-major)
+    int tm_pfl2 = -1;      // CMTF_TM_PFL2=0/1: hog3tm L2 prefetch of the next entry's rows (-1 auto)
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
@@ -497,35 +499,47 @@ __global__ void remap_pos_kernel(uint32_t* pos, uint64_t count, uint64_t n, uint
 // Each epoch draws a random stratum sequence and a group-affine map per
 // stratum.  rrec[p].w carries the entry id of record p (pos[] is rebuilt
 // from it after the re-layout).
-constexpr int kMaxBlk = 16;
+constexpr int kMaxBlk = 32;
 
+// block of row i: floor(i * B / d), by a float estimate and an exact
+// correction (a 64-bit division is a ~100-instruction routine)
+__device__ __forceinline__ uint32_t block_of(uint32_t i, uint32_t B, uint64_t d, float scale) {
+  uint32_t q = (uint32_t)((float)i * scale);
+  if (q >= B) q = B - 1;
+  const uint64_t x = (uint64_t)i * B;
+  if ((uint64_t)q * d > x) --q;
+  else if ((uint64_t)(q + 1) * d <= x) ++q;
+  return q;
+}
 __device__ __forceinline__ uint32_t stratum_of(uint32_t i1, uint32_t i2, uint32_t B, uint64_t d0,
                                                uint64_t d1) {
-  return (uint32_t)((uint64_t)i1 * B / d0) * B + (uint32_t)((uint64_t)i2 * B / d1);
+  return block_of(i1, B, d0, (float)B / (float)d0) * B + block_of(i2, B, d1, (float)B / (float)d1);
 }
 
-// Stable partition of the records by stratum (chunks of kPartChunk
+// Partition of the records by stratum (chunks of kPartChunk
 // records): counts per (chunk, stratum), an exclusive scan per stratum
 // across the chunks, then each chunk writes its records, in position order,
 // to consecutive places of each stratum's run.  Reads stream; writes form
 // runs that fill whole lines in L2.
-constexpr uint32_t kPartChunk = 8192;
+// (chunk size grows with the stratum count so the count table stays small)
+inline uint32_t part_chunk(uint32_t S) { return 8192u * std::max(1u, S / 64u); }
 __global__ void part_hist_kernel(const uint4* rec, uint64_t n, uint32_t B, uint64_t d0,
-                                 uint64_t d1, uint32_t* cnt, uint32_t* total) {
+                                 uint64_t d1, uint32_t* cnt, uint32_t* total,
+                                 uint32_t kPartChunk) {
   __shared__ uint32_t h[kMaxBlk * kMaxBlk];
   const uint32_t S = B * B;
   const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
   for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) h[s] = 0;
     __syncthreads();
-    const uint64_t p1 = min(n, (c + 1) * kPartChunk);
-    for (uint64_t p = c * kPartChunk + threadIdx.x; p < p1; p += blockDim.x) {
+    const uint64_t p1 = min(n, (c + 1) * (uint64_t)kPartChunk);
+    for (uint64_t p = c * (uint64_t)kPartChunk + threadIdx.x; p < p1; p += blockDim.x) {
       const uint4 r = __ldcs(rec + p);
       atomicAdd(h + stratum_of(r.x, r.y, B, d0, d1), 1u);
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
-      cnt[c * S + s] = h[s];
+      if (cnt) cnt[c * S + s] = h[s];
       if (h[s]) atomicAdd(total + s, h[s]);
     }
     __syncthreads();
@@ -570,62 +584,158 @@ __global__ void pos_from_ids_kernel(const float4* rrec, uint64_t n, uint32_t* po
 // group map (posA, posB) of the per-epoch reshuffles: no scatter pass.
 struct IdMap {
   uint64_t n, ng, iA, B, ia, pb;
+  uint64_t m_n, m_ng;  // floor((2^64 - 1) / n), / ng: Barrett reduction instead of 64-bit divisions
   int closed;
 };
+// x mod d with m = floor((2^64 - 1) / d): the quotient estimate is at most one short
+__device__ __forceinline__ uint64_t mod_magic(uint64_t x, uint64_t d, uint64_t m) {
+  uint64_t r = x - __umul64hi(x, m) * d;
+  if (r >= d) r -= d;
+  return r;
+}
 __device__ __forceinline__ uint32_t entry_of(const IdMap& m, uint64_t q) {
   uint64_t p0 = q;
-  if (q < m.ng * kShuffleGroup)
-    p0 = (m.iA * ((q / kShuffleGroup + m.ng - m.B) % m.ng) % m.ng) * kShuffleGroup +
-         q % kShuffleGroup;
-  return (uint32_t)(m.ia * ((p0 + m.n - m.pb) % m.n) % m.n);
+  if (q < m.ng * kShuffleGroup) {
+    uint64_t g = q / kShuffleGroup + m.ng - m.B;  // B < ng
+    if (g >= m.ng) g -= m.ng;
+    p0 = mod_magic(m.iA * g, m.ng, m.m_ng) * kShuffleGroup + q % kShuffleGroup;
+  }
+  uint64_t t = p0 + m.n - m.pb;  // pb < n
+  if (t >= m.n) t -= m.n;
+  return (uint32_t)mod_magic(m.ia * t, m.n, m.m_n);
 }
 
-// 256 threads per chunk, in tiles of 256 records: a record's place = its
-// stratum's run start for the chunk + records of that stratum in earlier
-// tiles + in earlier warps of the tile + in earlier lanes of its warp.
+// One block per chunk at a time: a record's place = the next free place of
+// its stratum's run for the chunk (shared-memory counters seeded with the
+// run starts; the order inside a run is the order the atomics land in --
+// the input is a random permutation already and the layout is kept for the
+// whole training, so stability buys nothing).
 __global__ void __launch_bounds__(256) part_scatter_kernel(
     const uint4* __restrict__ rec, const uint4* __restrict__ rrec, uint64_t n, uint32_t B,
     uint64_t d0, uint64_t d1, const uint32_t* __restrict__ base, uint4* __restrict__ rec_out,
-    uint4* __restrict__ rrec_out, const IdMap m) {
+    uint4* __restrict__ rrec_out, const IdMap m, uint32_t kPartChunk) {
   __shared__ uint32_t run[kMaxBlk * kMaxBlk];
-  __shared__ uint32_t wc[8 * kMaxBlk * kMaxBlk];
   const uint32_t S = B * B;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
   for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     for (uint32_t s = threadIdx.x; s < S; s += 256) run[s] = base[c * S + s];
-    for (uint64_t t0 = c * kPartChunk; t0 < min(n, (c + 1) * kPartChunk); t0 += 256) {
-      for (uint32_t i = threadIdx.x; i < 8 * S; i += 256) wc[i] = 0;
-      __syncthreads();
-      const uint64_t p = t0 + threadIdx.x;
-      const bool ok = p < n;
-      uint4 r = make_uint4(0, 0, 0, 0), q = make_uint4(0, 0, 0, 0);
-      uint32_t s = 0xffffffffu;
-      if (ok) {
-        r = __ldcs(rec + p);
-        q = __ldcs(rrec + p);
-        s = stratum_of(r.x, r.y, B, d0, d1);
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, s);
-      const uint32_t lr = __popc(peers & ((1u << lane) - 1u));
-      if (ok && lr == 0) wc[w * S + s] = __popc(peers);
-      __syncthreads();
-      if (ok) {
-        uint32_t d = run[s] + lr;
-        for (int w2 = 0; w2 < w; ++w2) d += wc[w2 * S + s];
-        if (m.closed) q.w = entry_of(m, p);
-        rec_out[d] = r;
-        rrec_out[d] = q;
-      }
-      __syncthreads();
-      for (uint32_t s2 = threadIdx.x; s2 < S; s2 += 256) {
-        uint32_t tot = 0;
-#pragma unroll
-        for (int w2 = 0; w2 < 8; ++w2) tot += wc[w2 * S + s2];
-        run[s2] += tot;
-      }
-      __syncthreads();
+    __syncthreads();
+    const uint64_t p1 = min(n, (c + 1) * (uint64_t)kPartChunk);
+    for (uint64_t p = c * (uint64_t)kPartChunk + threadIdx.x; p < p1; p += 256) {
+      const uint4 r = __ldcs(rec + p);
+      uint4 q = __ldcs(rrec + p);
+      const uint32_t d = atomicAdd(run + stratum_of(r.x, r.y, B, d0, d1), 1u);
+      if (m.closed) q.w = entry_of(m, p);
+      rec_out[d] = r;
+      rrec_out[d] = q;
     }
+    __syncthreads();
+  }
+}
+
+// Partition pass with coalesced writes.  Scattering record by record (the
+// kernel above) issues two 16-byte writes per record to ~S different runs:
+// 2.6e10 scattered writes/s is the memory system's ceiling for them (75 ms
+// per 9e8 records).  Here a block sorts a tile of kTile records by key in
+// shared memory (at most 64 keys), claims a piece of every key's global run
+// with one atomic per key, and writes each piece as consecutive 16-byte
+// stores.  With more than 64 strata the partition takes two passes: by
+// mode-1 block (PASS 1), then -- over that output, tile by tile inside every
+// mode-1 block's run (RunTab) -- by mode-2 block (PASS 2).  PASS 0: one pass
+// over <= 64 strata.  The order inside a stratum is whatever the atomics
+// give (the input is a random permutation; the layout then stays).
+constexpr int kTile = 1024;
+struct RunTab {  // PASS 2: the mode-1 blocks' runs and their tile counts (prefix sums)
+  uint32_t off[kMaxBlk + 1];
+  uint32_t tpre[kMaxBlk + 1];
+};
+template <int PASS>
+__global__ void __launch_bounds__(256) part_tile_kernel(
+    const uint4* __restrict__ rec, const uint4* __restrict__ rrec, uint64_t n, uint32_t B,
+    uint64_t d0, uint64_t d1, uint32_t* __restrict__ cursor, uint4* __restrict__ rec_out,
+    uint4* __restrict__ rrec_out, const IdMap m, const RunTab rt) {
+  __shared__ uint4 srec[kTile];
+  __shared__ uint4 srr[kTile];
+  __shared__ uint8_t skey[kTile];
+  __shared__ uint32_t hist[64], start[64], gbase[64];
+  const float sc0 = (float)B / (float)d0, sc1 = (float)B / (float)d1;
+  const uint64_t ntile = PASS == 2 ? rt.tpre[B] : (n + kTile - 1) / kTile;
+  for (uint64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    uint64_t p0 = tile * kTile;
+    uint32_t cnt = (uint32_t)min((uint64_t)kTile, n - p0);
+    uint32_t run = 0;  // PASS 2: the mode-1 block this tile lies in
+    if (PASS == 2) {
+      while (tile >= rt.tpre[run + 1]) ++run;
+      p0 = rt.off[run] + (tile - rt.tpre[run]) * kTile;
+      cnt = (uint32_t)min((uint64_t)kTile, rt.off[run + 1] - p0);
+    }
+    if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+    __syncthreads();
+    uint4 r[kTile / 256], q[kTile / 256];
+    uint32_t key[kTile / 256], rank[kTile / 256];
+#pragma unroll
+    for (int j = 0; j < kTile / 256; ++j) {
+      const uint32_t t = threadIdx.x + 256 * j;
+      if (t < cnt) {
+        r[j] = __ldcs(rec + p0 + t);
+        q[j] = __ldcs(rrec + p0 + t);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kTile / 256; ++j) {
+      const uint32_t t = threadIdx.x + 256 * j;
+      if (t < cnt) {
+        if (PASS == 1) key[j] = block_of(r[j].x, B, d0, sc0);
+        else {
+          const uint32_t b2 = block_of(r[j].y, B, d1, sc1);
+          key[j] = PASS == 0 ? block_of(r[j].x, B, d0, sc0) * B + b2 : b2;
+        }
+        if (PASS != 2 && m.closed) q[j].w = entry_of(m, p0 + t);
+        rank[j] = atomicAdd(hist + key[j], 1u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 64 counts, one global claim per key
+      const uint32_t h0 = hist[threadIdx.x], h1 = hist[threadIdx.x + 32];
+      uint32_t x0 = h0, x1 = h1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, d);
+        const uint32_t y1 = __shfl_up_sync(0xffffffffu, x1, d);
+        if ((int)threadIdx.x >= d) {
+          x0 += y0;
+          x1 += y1;
+        }
+      }
+      const uint32_t tot0 = __shfl_sync(0xffffffffu, x0, 31);
+      start[threadIdx.x] = x0 - h0;
+      start[threadIdx.x + 32] = tot0 + x1 - h1;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const uint32_t k = threadIdx.x + 32 * half, h = half ? h1 : h0;
+        const uint32_t gi = PASS == 2 ? run * B + k : k;
+        gbase[k] = h ? atomicAdd(cursor + gi, h) : 0u;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTile / 256; ++j) {
+      const uint32_t t = threadIdx.x + 256 * j;
+      if (t < cnt) {
+        const uint32_t slot = start[key[j]] + rank[j];
+        srec[slot] = r[j];
+        srr[slot] = q[j];
+        skey[slot] = (uint8_t)key[j];
+      }
+    }
+    __syncthreads();
+    for (uint32_t slot = threadIdx.x; slot < cnt; slot += 256) {
+      const uint32_t k = skey[slot];
+      const uint32_t d = gbase[k] + (slot - start[k]);
+      rec_out[d] = srec[slot];
+      rrec_out[d] = srr[slot];
+    }
+    __syncthreads();
   }
 }
 
@@ -697,6 +807,7 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
 
 int normalize_pos(cmtf_gpu_ctx* ctx);  // reshuffle machinery, below
 uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx);
+bool tables_beyond_l2(const cmtf_gpu_ctx* ctx);
 int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B);
 bool vt_wanted(const cmtf_gpu_ctx* ctx);
 int vt_table(cmtf_gpu_ctx* ctx, uint64_t epoch);
@@ -1684,6 +1795,7 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     a.g_alt = ctx->env.tm_galt ? 1 : 0;
     a.vtab = ctx->vt_on && whole ? ctx->d_vtab : nullptr;
     a.strided = ctx->env.tm_strided || (a.vtab && ctx->blk_B > 1);
+    a.pf_l2 = ctx->env.tm_pfl2 > 0 ? 1 : 0;  // measured +10% epoch time on config 5: off
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
@@ -1957,6 +2069,8 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       const char* w = std::getenv("CMTF_TM_STRIDED");
       ctx->env.tm_strided = w && w[0] == '1';
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
+      if (const char* h = std::getenv("CMTF_TM_SEQ")) ctx->env.tm_seq = atoi(h);
+      if (const char* h = std::getenv("CMTF_TM_PFL2")) ctx->env.tm_pfl2 = atoi(h) ? 1 : 0;
       if (const char* b = std::getenv("CMTF_TM_BLOCKS"))
         ctx->env.tm_blocks = std::max(0, std::min(kMaxBlk, atoi(b)));
       if (const char* b = std::getenv("CMTF_TM_BULK")) ctx->env.tm_bulk = atoi(b) & 7;
@@ -3061,8 +3175,13 @@ int normalize_pos(cmtf_gpu_ctx* ctx) {
 // entry's three row gathers miss L2 and fill 128-B lines from DRAM (config 5:
 // 2.4 TB/s of random line traffic, the measured ceiling); blocking keeps
 // mode 1 and 2's active blocks L2-resident (config 5 @1e9: -12% epoch time,
-// RMSE within 0.3%, scripts/blocked_order_exp.py).  B = 8: 2 x 1/8 of the
-// two tables; more blocks (and a 3-mode B^3 split) measured no faster.
+// RMSE within 0.3%, scripts/blocked_order_exp.py).  B = 32 with a
+// mode-1-block-major stratum sequence (the mode-1 block stays across B
+// strata): ncu DRAM traffic at config 5 @1e9 769 GB unblocked, 621 GB at
+// B = 8 random sequence, 528 GB at B = 32 block-major (201 -> 193 ms); the
+// rows of a block are reused only while the lines streamed between two
+// touches (~300 B per entry of the unblocked mode and the records) fit L2,
+// which B = 8's 1.25M-row blocks do not.
 uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx);
 // the tcgen05 epoch will run (or runs) the blocked virtual order
 bool vt_wanted(const cmtf_gpu_ctx* ctx) {
@@ -3070,15 +3189,20 @@ bool vt_wanted(const cmtf_gpu_ctx* ctx) {
          tensor_shuffles(ctx) && blocks_wanted(ctx) > 1;
 }
 
-uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx) {
-  if (ctx->order != 3 || ctx->cfg.order_policy != 1 || ctx->nnz / kShuffleGroup < 3) return 0;
-  if (ctx->env.tm_blocks >= 0) return (uint32_t)ctx->env.tm_blocks;
+// the factor tables do not fit L2 together
+bool tables_beyond_l2(const cmtf_gpu_ctx* ctx) {
   int l2 = 0;
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
   uint64_t bytes = 0;
-  for (int n = 0; n < 3; ++n) bytes += (uint64_t)ctx->dims[n] * ctx->JP(n) * sizeof(float);
-  if (bytes <= (uint64_t)l2 || ctx->nnz < (1ull << 22)) return 0;
-  return 8;
+  for (int n = 0; n < ctx->order; ++n) bytes += (uint64_t)ctx->dims[n] * ctx->JP(n) * sizeof(float);
+  return bytes > (uint64_t)l2;
+}
+
+uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx) {
+  if (ctx->order != 3 || ctx->cfg.order_policy != 1 || ctx->nnz / kShuffleGroup < 3) return 0;
+  if (ctx->env.tm_blocks >= 0) return (uint32_t)ctx->env.tm_blocks;
+  if (!tables_beyond_l2(ctx) || ctx->nnz < (1ull << 22)) return 0;
+  return 32;
 }
 
 // Switch to the virtual order with B x B strata: lay the records (and
@@ -3098,45 +3222,69 @@ int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B) {
     im.B = ctx->posB;
     im.ia = inv_mod(ctx->up_pa, n);
     im.pb = ctx->up_pb;
+    im.m_n = ~0ull / n;
+    im.m_ng = ~0ull / im.ng;
   } else {  // pos[] exact, then each record's id scattered into rrec
     TRY(normalize_pos(ctx));
     rrec_ids_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->pos, n, ctx->rrec);
     CU(cudaGetLastError());
   }
   const uint32_t S = B * B;
+  const uint32_t kPartChunk = part_chunk(S);
   const uint64_t nch = (n + kPartChunk - 1) / kPartChunk;
-  if (!ctx->blk_hist) TRY(dalloc(ctx, &ctx->blk_hist, 2 * kMaxBlk * kMaxBlk));
-  TRY(ensure(ctx, &ctx->part_cnt, &ctx->part_cnt_cap, nch * S));
-  CU(cudaMemsetAsync(ctx->blk_hist, 0, kMaxBlk * kMaxBlk * sizeof(uint32_t), ctx->stream));
+  constexpr uint32_t kS = kMaxBlk * kMaxBlk;
+  // blk_hist: [0] stratum sizes, [1] stratum cursors (run starts), [2] mode-1 block cursors
+  if (!ctx->blk_hist) TRY(dalloc(ctx, &ctx->blk_hist, 3 * kS));
+  CU(cudaMemsetAsync(ctx->blk_hist, 0, kS * sizeof(uint32_t), ctx->stream));
   const unsigned pg = (unsigned)std::min<uint64_t>(nch, 148ull * 8);
   part_hist_kernel<<<pg, 256, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(ctx->rec), n, B,
-                                                ctx->dims[0], ctx->dims[1], ctx->part_cnt,
-                                                ctx->blk_hist);
+                                                ctx->dims[0], ctx->dims[1], nullptr,
+                                                ctx->blk_hist, kPartChunk);
   CU(cudaGetLastError());
-  std::vector<uint32_t> hist(S), off(S, 0);
+  std::vector<uint32_t> hist(S), off(S, 0), off1(B, 0);
   CU(cudaMemcpyAsync(hist.data(), ctx->blk_hist, S * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                      ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   for (uint32_t s = 1; s < S; ++s) off[s] = off[s - 1] + hist[s - 1];
-  CU(cudaMemcpyAsync(ctx->blk_hist + kMaxBlk * kMaxBlk, off.data(), S * sizeof(uint32_t),
+  for (uint32_t b = 0; b < B; ++b) off1[b] = off[b * B];
+  CU(cudaMemcpyAsync(ctx->blk_hist + kS, off.data(), S * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(ctx->blk_hist + 2 * kS, off1.data(), B * sizeof(uint32_t),
                      cudaMemcpyHostToDevice, ctx->stream));
-  part_scan_kernel<<<(S + 7) / 8, 256, 0, ctx->stream>>>(ctx->part_cnt, nch, S,
-                                                         ctx->blk_hist + kMaxBlk * kMaxBlk);
-  CU(cudaGetLastError());
   pt.tick("count");
   TRY(ensure(ctx, &ctx->rec_alt, &ctx->rec_alt_cap, n * 4));
   TRY(ensure(ctx, &ctx->rrec_alt, &ctx->rrec_alt_cap, n));
-  part_scatter_kernel<<<pg, 256, 0, ctx->stream>>>(
-      reinterpret_cast<const uint4*>(ctx->rec), reinterpret_cast<const uint4*>(ctx->rrec), n, B,
-      ctx->dims[0], ctx->dims[1], ctx->part_cnt, reinterpret_cast<uint4*>(ctx->rec_alt),
-      reinterpret_cast<uint4*>(ctx->rrec_alt), im);
-  CU(cudaGetLastError());
+  const unsigned tg = (unsigned)std::min<uint64_t>((n + kTile - 1) / kTile, 148ull * 4);
+  const uint4* rec_in = reinterpret_cast<const uint4*>(ctx->rec);
+  const uint4* rrec_in = reinterpret_cast<const uint4*>(ctx->rrec);
+  uint4* rec_o = reinterpret_cast<uint4*>(ctx->rec_alt);
+  uint4* rrec_o = reinterpret_cast<uint4*>(ctx->rrec_alt);
+  if (S <= 64) {  // one pass; the result is in the alternate buffers
+    part_tile_kernel<0><<<tg, 256, 0, ctx->stream>>>(rec_in, rrec_in, n, B, ctx->dims[0],
+                                                     ctx->dims[1], ctx->blk_hist + kS, rec_o,
+                                                     rrec_o, im, RunTab{});
+    CU(cudaGetLastError());
+    std::swap(ctx->rec, ctx->rec_alt);
+    std::swap(ctx->rec_cap, ctx->rec_alt_cap);
+    std::swap(ctx->rrec, ctx->rrec_alt);
+    std::swap(ctx->rrec_cap, ctx->rrec_alt_cap);
+  } else {  // by mode-1 block into the alternate buffers, then by mode-2 block back
+    part_tile_kernel<1><<<tg, 256, 0, ctx->stream>>>(rec_in, rrec_in, n, B, ctx->dims[0],
+                                                     ctx->dims[1], ctx->blk_hist + 2 * kS, rec_o,
+                                                     rrec_o, im, RunTab{});
+    CU(cudaGetLastError());
+    RunTab rt{};
+    for (uint32_t b = 0; b <= B; ++b) {
+      rt.off[b] = b < B ? off1[b] : (uint32_t)n;
+      if (b) rt.tpre[b] = rt.tpre[b - 1] + (rt.off[b] - rt.off[b - 1] + kTile - 1) / kTile;
+    }
+    part_tile_kernel<2><<<tg, 256, 0, ctx->stream>>>(
+        rec_o, rrec_o, n, B, ctx->dims[0], ctx->dims[1], ctx->blk_hist + kS,
+        reinterpret_cast<uint4*>(ctx->rec), reinterpret_cast<uint4*>(ctx->rrec), im, rt);
+    CU(cudaGetLastError());
+  }
   CU(cudaStreamSynchronize(ctx->stream));
   pt.tick("scatter");
-  std::swap(ctx->rec, ctx->rec_alt);
-  std::swap(ctx->rec_cap, ctx->rec_alt_cap);
-  std::swap(ctx->rrec, ctx->rrec_alt);
-  std::swap(ctx->rrec_cap, ctx->rrec_alt_cap);
   ctx->blk_B = B;
   ctx->blk_n.assign(hist.begin(), hist.end());
   ctx->blk_off.assign(B * B, 0);
@@ -3146,8 +3294,8 @@ int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B) {
   ctx->posA = 1;  // the group map no longer applies: pos[] comes from the ids
   ctx->posB = 0;
   ctx->pos_affine = false;
-  ctx->last_launches += 5;
-  return normalize_pos(ctx);
+  ctx->last_launches += 4;
+  return CMTF_OK;  // pos[] is rebuilt from the ids when something asks for it (normalize_pos)
 }
 
 // This epoch's segment table: a random stratum sequence (host draws from
@@ -3157,7 +3305,22 @@ int vt_table(cmtf_gpu_ctx* ctx, uint64_t epoch) {
   auto rng = make_rng(ctx->cfg.seed, 0x0B, epoch);
   std::vector<uint32_t> seq(S);
   for (uint32_t s = 0; s < S; ++s) seq[s] = s;
-  for (uint32_t k = S; k > 1; --k) std::swap(seq[k - 1], seq[bounded(rng, k)]);
+  if (ctx->env.tm_seq == 1) {
+    // mode-1-block-major: a random order of the mode-1 blocks and, inside
+    // each, a random order of the mode-2 blocks -- the mode-1 block stays
+    // L2-resident across B consecutive strata
+    const uint32_t B = ctx->blk_B;
+    std::vector<uint32_t> o1(B), o2(B);
+    for (uint32_t i = 0; i < B; ++i) o1[i] = i;
+    for (uint32_t k = B; k > 1; --k) std::swap(o1[k - 1], o1[bounded(rng, k)]);
+    for (uint32_t i = 0; i < B; ++i) {
+      for (uint32_t j = 0; j < B; ++j) o2[j] = j;
+      for (uint32_t k = B; k > 1; --k) std::swap(o2[k - 1], o2[bounded(rng, k)]);
+      for (uint32_t j = 0; j < B; ++j) seq[i * B + j] = o1[i] * B + o2[j];
+    }
+  } else {
+    for (uint32_t k = S; k > 1; --k) std::swap(seq[k - 1], seq[bounded(rng, k)]);
+  }
   auto& h = ctx->h_vtab;
   h.clear();
   uint64_t v = 0;

@@ -592,6 +592,11 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
 #pragma unroll
       for (int n = 0; n < 3; ++n)
         nsl[n] = a.hot[n].slot ? __ldg(a.hot[n].slot + (nxt ? nx[n] : 0u)) : -1;
+      if (a.pf_l2 && nxt) {
+#pragma unroll
+        for (int n = 0; n < 3; ++n)
+          if (nsl[n] < 0) prefetch_row_l2<JP>(a.U[n] + (uint64_t)nx[n] * JP);
+      }
       // the regulariser coefficients stream beside the records (rrec)
       const float4 rr = nxt ? tm_ld_stream(a.rrec + p1) : make_float4(0.f, 0.f, 0.f, 0.f);
       nrg[0] = rr.x;

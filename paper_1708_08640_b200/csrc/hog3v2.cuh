@@ -104,6 +104,11 @@ struct Hog3v2Args {
   // segments of 2 uint4 {vbeg, src, body, ng} {a, b, m_lo, m_hi}, then a
   // sentinel with vbeg = UINT32_MAX (see vphys in hog3tm.cuh)
   const uint4* vtab;
+  // hog3tm: factor tables beyond L2 -- the next entry's cold rows are
+  // requested into L2 (prefetch.global.L2) at the top of the iteration, most
+  // of an iteration before their cp.async gathers are issued (the gathers
+  // land in the operand tiles, so they must wait for the sweep MMAs)
+  int pf_l2;
 };
 
 // ---------------------------------------------------------------------
@@ -163,6 +168,16 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// the 128-byte line(s) of a factor row of JP floats
+template <int JP>
+__device__ __forceinline__ void prefetch_row_l2(const float* row) {
+  prefetch_l2(row);
+  if (JP * 4 > 16 && (reinterpret_cast<uintptr_t>(row) & 127u) > 128u - JP * 4u)
+    prefetch_l2(row + JP - 1);
 }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
