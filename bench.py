@@ -309,7 +309,8 @@ def run_ours(args):
     spec, bundle, test, ranks, lr, lam = make_workload(args)
     cfg = api.TrainConfig(ranks=ranks, seed=rank, eta0=lr, lambda_reg=lam, kernel=args.kernel,
                           device=local, hog_threads=args.hog_threads,
-                          order_policy=args.order)
+                          order_policy=args.order,
+                          core_flush_every=int(os.environ.get("CMTF_BENCH_CORE_EVERY", "0")))
     st = api.make_state(cfg, bundle)
     nt, Bt, Ft, mats = algorithmic(bundle, ranks)
     n_upd = nt + sum(n for n, _ in mats)

@@ -1746,7 +1746,15 @@ bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint6
   a.core_reg = (float)(ctx->cfg.lambda_reg / (double)nnz_all);
   a.kappa = ctx->cfg.kappa > 0.f ? ctx->cfg.kappa : 0.5f;
   a.kappa_core = ctx->cfg.kappa_core > 0.f ? ctx->cfg.kappa_core : 2.0f;
-  const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every : 1;
+  // core pushes: every iteration, or -- hog3tm with long sweeps (>= 2048
+  // iterations per lane and epoch: configs 3 and 5) -- every second one: the
+  // push (TMEM read-out, coalesced REDs, refresh of the shared core copies)
+  // is 13% of an iteration; config 5 @1e9 195 -> 187 ms/epoch with the same
+  // RMSE after 8 epochs (0.10042), config 5 @1e8 0.32399 vs 0.32407.  Short
+  // sweeps keep every iteration (config 2: RMSE +0.2% otherwise).
+  const bool long_sweep = ctx->order == 3 && v3_tm(ctx) && W > 0 &&
+                          (double)ctx->nnz / W >= 2048.0;
+  const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every : (long_sweep ? 2 : 1);
   a.nhat_core = (float)(W * FG * ctx->v2_e * ctx->world);
   a.flush_every = F;
   a.core_every = FG;
