@@ -57,6 +57,13 @@
 #ifndef CMTF_TM_PROF
 #define CMTF_TM_PROF 0
 #endif
+#ifndef CMTF_TM_EARLY_GATHER
+#define CMTF_TM_EARLY_GATHER 0  // 1: next entry's row gathers issued as soon as the sweep MMAs are
+                                // done (measured same-box: config 5 @1e9 +1.1%, config 3 -0.7%: off)
+#endif
+#ifndef CMTF_TM_PH2
+#define CMTF_TM_PH2 1  // even J: the P rows' hi/lo halves by packed fp16 arithmetic (see core_phase)
+#endif
 #ifndef CMTF_TM_EXACT
 #define CMTF_TM_EXACT 0
 #endif
@@ -71,6 +78,11 @@ __host__ __device__ constexpr int round_up16(int x) { return (x + 15) & ~15; }
 // in fp16, which -- like a diverged model -- surfaces as a non-finite
 // parameter (DivergenceError) rather than as a silently clamped result.
 constexpr float kSU = 64.f, kSG = 64.f, kSP = 64.f, kSS = 64.f;
+// packed-fp16 P rows (CMTF_TM_PH2): u1 is scaled by kSP, u2 by kSP2 before
+// their fp16 splits, so P carries kSP * kSP2 (a product beyond 127 overflows)
+constexpr float kSP2 = 8.f;
+template <int J>
+constexpr bool tm_ph2() { return CMTF_TM_PH2 && J % 2 == 0; }
 
 template <int J>
 struct TMLayout {
@@ -374,7 +386,8 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   const uint32_t sSh = sPl + L::P_BYTES, sSl = sSh + L::S_BYTES;
   constexpr uint32_t ID_SWEEP = umma::idesc_f16(128, NT);
   constexpr uint32_t ID_CORE = umma::idesc_f16(128, 16, true, true);
-  constexpr float kInvT = 1.f / (kSU * kSG), kInvD = 1.f / (kSP * kSS);
+  constexpr float kInvT = 1.f / (kSU * kSG);
+  constexpr float kInvD = 1.f / (kSP * (tm_ph2<J>() ? kSP2 : 1.f) * kSS);
   constexpr uint32_t kRefresh = CMTF_TM_REFRESH;
 
   const uint64_t Wt = (uint64_t)gridDim.x * NW * 32;
@@ -664,6 +677,12 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     umma::mbar_wait(&mbar[g][0], par);
     TMP(2);
     umma::fence_after();
+#if CMTF_TM_EARLY_GATHER
+    // ---- next entry's rows into the tiles: the sweep MMAs (the tiles' only
+    // readers) are done, so the gathers would get the rest of the iteration
+    // to land instead of the matrix phase (turn-0 warps) ----
+    issue_rows(rc1, nsl, e0 + st < hi);
+#endif
 #pragma unroll
     for (int c0 = 0; c0 < NT; c0 += 32) {
       float v[32];
@@ -777,22 +796,70 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
       } else {          // the slot's turn-0 MMA of this iteration
         umma::mbar_wait(&mbar[g][1 + slot], par);
       }
-      float u1s[J];
-#pragma unroll
-      for (int k = 0; k < J; ++k) u1s[k] = u1[k] * kSP;
       uint8_t* Ph = myslot + lane * 16;
+      if constexpr (tm_ph2<J>()) {
+        // P[ab] = u1[a] u2[b] as fp16 hi + lo without forming the fp32
+        // product: with u1 = h1 + l1 and u2 = h2 + l2 split into fp16 halves
+        // (11 significant bits each), hi = rn16(h1 h2), and the rounding
+        // residual h1 h2 - hi has at most 11 significant bits, so one packed
+        // fp16 FMA returns it exactly; lo = residual + l1 h2 + h1 l2 (the
+        // l1 l2 term is below 2^-22).  Four packed instructions per two
+        // elements instead of two multiplies and six split operations.
+        __half2 H1[J], L1[J], h2p[J / 2], l2p[J / 2];
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int ab = 8 * j + q;
-          v[q] = ab < AB ? u1s[ab / J] * u2[ab % J] : 0.f;
+        for (int k = 0; k < J; ++k) {
+          __half h, l;
+          split_h(u1[k] * kSP, h, l);
+          H1[k] = __half2half2(h);
+          L1[k] = __half2half2(l);
         }
-        uint4 h, l;
-        split8(v, h, l);
-        *reinterpret_cast<uint4*>(Ph + j * L::P_SBO) = h;
-        *reinterpret_cast<uint4*>(Ph + L::P_BYTES + j * L::P_SBO) = l;
+#pragma unroll
+        for (int k = 0; k < J / 2; ++k) {
+          const float x0 = u2[2 * k] * kSP2, x1 = u2[2 * k + 1] * kSP2;
+          const float h0 = __uint_as_float(__float_as_uint(x0) & 0xffffe000u);
+          const float h1 = __uint_as_float(__float_as_uint(x1) & 0xffffe000u);
+          h2p[k] = __floats2half2_rn(h0, h1);
+          l2p[k] = __floats2half2_rn(x0 - h0, x1 - h1);
+        }
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int ab = 8 * j + 2 * q;  // even, and J is even: (ab, ab + 1) share a
+            if (ab < AB) {
+              const int ia = ab / J, pb = (ab % J) / 2;
+              const __half2 ph = __hmul2(H1[ia], h2p[pb]);
+              __half2 rl = __hfma2(H1[ia], h2p[pb], __hneg2(ph));
+              rl = __hfma2(L1[ia], h2p[pb], rl);
+              rl = __hfma2(H1[ia], l2p[pb], rl);
+              hw[q] = *reinterpret_cast<const uint32_t*>(&ph);
+              lw[q] = *reinterpret_cast<const uint32_t*>(&rl);
+            } else {
+              hw[q] = lw[q] = 0u;
+            }
+          }
+          *reinterpret_cast<uint4*>(Ph + j * L::P_SBO) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(Ph + L::P_BYTES + j * L::P_SBO) =
+              make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+      } else {
+        float u1s[J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) u1s[k] = u1[k] * kSP;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int ab = 8 * j + q;
+            v[q] = ab < AB ? u1s[ab / J] * u2[ab % J] : 0.f;
+          }
+          uint4 h, l;
+          split8(v, h, l);
+          *reinterpret_cast<uint4*>(Ph + j * L::P_SBO) = h;
+          *reinterpret_cast<uint4*>(Ph + L::P_BYTES + j * L::P_SBO) = l;
+        }
       }
       uint8_t* Sh = myslot + 2 * L::P_BYTES + lane * 16;
       const float rs = -r * kSS;
@@ -832,8 +899,10 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     if (turn == 0) core_phase();
 
     TMP(5);
+#if !CMTF_TM_EARLY_GATHER
     // ---- next entry's rows into the tiles (the sweep MMAs are done) ----
     issue_rows(rc1, nsl, e0 + st < hi);
+#endif
 
     TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----
