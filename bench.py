@@ -42,6 +42,7 @@ FP32_FMA_PER_SM_CLK = 128  # Blackwell SM: 4 x 32 FP32 lanes
 DTYPE = {"order3tm": "f32 (tcgen05 MMAs on split-fp16 x3 operands, fp32 accumulate)",
          "order3v2": "f32 (core gradient: tf32 mma.sync)",
          "order4": "f32 (mma.sync on split 3xTF32 operands, fp32 accumulate)",
+         "order4tm": "f32 (tcgen05 MMAs on split-fp16 x3 operands, fp32 accumulate)",
          "order3": "f32", "generic": "f32"}
 CONFIG_INDEX = {"config1": "BASELINE configs[0]", "config2": "BASELINE configs[1]",
                 "config3": "BASELINE configs[2]", "config4": "BASELINE configs[3]",
@@ -381,6 +382,8 @@ def run_ours(args):
                        "order3tm": "hog3tm_kernel (fused epoch sweep, tcgen05 contractions + "
                                    "core gradient, TMEM accumulators)",
                        "order4": "hog4_kernel (fused epoch sweep, tensor-core contractions)",
+                       "order4tm": "hog4tm_kernel (fused epoch sweep, tcgen05 contractions + core "
+                                   "gradient, TMEM accumulators)",
                        "order3": "hog3_kernel (tensor sweep)",
                        "generic": "hogwild_generic_kernel (tensor sweep)"}.get(info["kernel"]),
             "kernel_ms": ten_ms,
@@ -400,7 +403,8 @@ def run_ours(args):
             fp = os.path.join(ROOT, "profiles", fn)
             if os.path.exists(fp):
                 prof.update(json.load(open(fp)))
-        key = {"order3v2": "hog3v2", "order3tm": "hog3tm", "order4": "hog4"}.get(info["kernel"])
+        key = {"order3v2": "hog3v2", "order3tm": "hog3tm", "order4": "hog4",
+               "order4tm": "hog4tm"}.get(info["kernel"])
         for k, v in prof.items():
             # keys: "<kernel> <config> [scale s | nnz n rank j] (...)"
             if args.config == "config5":

@@ -150,7 +150,7 @@ class TrainConfig:
     kappa: float = 0.0  # 0 = default 0.5
     flush_every: int = 0  # 0 = default: 32 (tcgen05 kernel), 16 (others)
     kernel_version: int = 0  # 0 = auto (v2), 1 = v1
-    core_flush_every: int = 0  # 0 = default 1
+    core_flush_every: int = 0  # 0 = default: 1; 2 for the tcgen05 kernel on long sweeps (>= 2048 iterations per lane)
     kappa_core: float = 0.0  # 0 = default 2.0
     debug_count_visits: bool = False  # TrainConfig::debug_count_visits (trainer.hpp:31-32)
 
@@ -332,7 +332,7 @@ class TrainState:
         w, t, s = C.c_int32(), C.c_int32(), C.c_int32()
         self._check(self._L.cmtf_gpu_kernel_info(self._h, C.byref(w), C.byref(t),
                                                   C.byref(s)))
-        return {"kernel": ["generic", "order3", "order4", "order3v2", "(retired)", "order3tm"][w.value],
+        return {"kernel": ["generic", "order3", "order4", "order3v2", "(retired)", "order3tm", "order4tm"][w.value],
                 "hog_threads": t.value, "sort_mode": s.value, "blocks": self._blocks()}
 
     def _blocks(self):

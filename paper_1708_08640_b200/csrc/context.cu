@@ -25,6 +25,7 @@
 #include "hog3.cuh"
 #include "hog3v2.cuh"
 #include "hog4.cuh"
+#include "hog4tm.cuh"
 #include "hog3tm.cuh"
 #include "stateless64.cuh"
 
@@ -266,6 +267,7 @@ struct cmtf_gpu_ctx {
   // test / experiment switches, read once when the context is created
   struct Env {
     bool v4_tc = true;     // CMTF_V4_TC=0: order-4 CUDA-core sweep
+    bool v4_tm = true;     // CMTF_V4_TM=0: order-4 opt on hog4 (mma.sync) instead of hog4tm (tcgen05)
     bool v3_tm = true;     // CMTF_V3_TM=0: order-3 opt on hog3v2 instead of hog3tm
     int v2_shape = 0;      // CMTF_V2_SHAPE: 1 = "8x1", 2 = "8x2"
     bool hot_host = false; // CMTF_HOT_HOST: host hot-row selection
@@ -1198,6 +1200,10 @@ bool v4_tc(const cmtf_gpu_ctx* ctx) {
   if (ctx->cfg.kernel != CMTF_KERNEL_OPT) return false;
   return ctx->env.v4_tc;
 }
+// order 4, opt kernel on tcgen05 (hog4tm)
+bool v4_tm(const cmtf_gpu_ctx* ctx) {
+  return ctx->cfg.kernel == CMTF_KERNEL_OPT && ctx->env.v4_tc && ctx->env.v4_tm;
+}
 
 bool v2_supported(const cmtf_gpu_ctx* ctx, int* J) {
   if (ctx->cfg.kernel_version == 1) return false;
@@ -1407,8 +1413,10 @@ int prepare_v2(cmtf_gpu_ctx* ctx, int J) {
   // hot rows: expected concurrent updates count * W / nnz >= tau, by count,
   // within the shared-memory budget left after the fixed layout
   float tau = ctx->cfg.hot_tau == 0.f ? 0.5f : ctx->cfg.hot_tau;
-  size_t fixed = four ? sizeof(float) * (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
-                                                           : V4Layout<8, 8>::FIXED_FLOATS)
+  size_t fixed = four ? (v4_tm(ctx) ? (size_t)TM4Layout::FIXED_BYTES
+                                    : sizeof(float) *
+                                          (size_t)(v4_tc(ctx) ? V4Layout<8, 8, true>::FIXED_FLOATS
+                                                              : V4Layout<8, 8>::FIXED_FLOATS))
                       : v2_fixed_bytes_rt(J, sh);
   if (tm3) {
     switch (J) {
@@ -1754,7 +1762,14 @@ bool fill_sweep_args(cmtf_gpu_ctx* ctx, Args& a, float eta, uint64_t t_lo, uint6
   // sweeps keep every iteration (config 2: RMSE +0.2% otherwise).
   const bool long_sweep = ctx->order == 3 && v3_tm(ctx) && W > 0 &&
                           (double)ctx->nnz / W >= 2048.0;
-  const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every : (long_sweep ? 2 : 1);
+  // hog4tm's push is a block-wide step (two block barriers, a 4096-element
+  // refresh of the fp16 core copies): every 8th iteration on long sweeps,
+  // scaled down to every iteration below 1024 iterations per lane
+  int fg4 = 1;
+  if (ctx->order == 4 && v4_tm(ctx) && W > 0)
+    fg4 = (int)std::min(8.0, std::max(1.0, std::floor((double)ctx->nnz / W / 512.0)));
+  const int FG = ctx->cfg.core_flush_every > 0 ? ctx->cfg.core_flush_every
+                                               : (ctx->order == 4 ? fg4 : (long_sweep ? 2 : 1));
   a.nhat_core = (float)(W * FG * ctx->v2_e * ctx->world);
   a.flush_every = F;
   a.core_every = FG;
@@ -1851,6 +1866,14 @@ int v4_sweep(cmtf_gpu_ctx* ctx, float eta, uint64_t t_lo, uint64_t t_hi, const u
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 2;
   if (ctx->cfg.kernel != CMTF_KERNEL_OPT) return launch_v4<0>(ctx, a);
+  if (v4_tm(ctx)) {
+    ctx->kernel_which = 6;
+    CU(cudaFuncSetAttribute(hog4tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ctx->v2_smem));
+    hog4tm_kernel<<<ctx->v2_blocks, 256, ctx->v2_smem, ctx->stream>>>(a);
+    CU(cudaGetLastError());
+    return CMTF_OK;
+  }
   return v4_tc(ctx) ? launch_v4<2>(ctx, a) : launch_v4<1>(ctx, a);
 }
 
@@ -2066,6 +2089,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       return v && v[0] == '0';
     };
     ctx->env.v4_tc = !off("CMTF_V4_TC");
+    ctx->env.v4_tm = !off("CMTF_V4_TM");
     ctx->env.v3_tm = !off("CMTF_V3_TM");
     if (const char* v = std::getenv("CMTF_V2_SHAPE"))
       ctx->env.v2_shape = std::string(v) == "8x1" ? 1 : std::string(v) == "8x2" ? 2 : 0;

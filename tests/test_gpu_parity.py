@@ -555,7 +555,7 @@ def test_order4_kernel_rmse_within_1pct_of_oracle(kernel, order4_reference):
     epochs = 10
     for _ in range(epochs):
         api.run_epoch(st)
-    assert st.kernel_info()["kernel"] == "order4"
+    assert st.kernel_info()["kernel"] == ("order4tm" if kernel == "opt" else "order4")
     ref_train, ref_test = ref["seeds"]["0"][epochs - 1]
     gpu_train = api.epoch_stats(st, ref["lambda"]).train_rmse
     gpu_test = api.test_rmse(st, test)
@@ -564,13 +564,19 @@ def test_order4_kernel_rmse_within_1pct_of_oracle(kernel, order4_reference):
     assert abs(gpu_test - ref_test) <= 0.01 * ref_test, msg
 
 
-@pytest.mark.parametrize("kernel", ["opt", "naive"])
-def test_order4_single_entry_steps_match_oracle(kernel):
-    """One tensor entry per epoch (no concurrency): the hog4 sweep's row and
+@pytest.mark.parametrize("kernel", ["opt", "opt-mma.sync", "naive"])
+def test_order4_single_entry_steps_match_oracle(kernel, monkeypatch):
+    """One tensor entry per epoch (no concurrency): the order-4 sweep's row and
     core steps equal the oracle's serial step.  naive: fp32 CUDA-core sweep;
-    opt: the contractions and the core gradient on the tensor cores with
-    3xTF32 operands (fp32-level accuracy).  The updated parameters within
-    1e-4, and the parameter CHANGES within 1e-4 of their magnitude."""
+    opt: hog4tm, the contractions and the core gradient on tcgen05 with
+    split-fp16 operands; opt-mma.sync: hog4's mma.sync path with 3xTF32
+    operands (CMTF_V4_TM=0) -- both fp32-level accuracy.  The updated
+    parameters within 1e-4, and the parameter CHANGES within 1e-4 of their
+    magnitude."""
+    want = {"opt": "order4tm", "opt-mma.sync": "order4", "naive": "order4"}[kernel]
+    if kernel == "opt-mma.sync":
+        monkeypatch.setenv("CMTF_V4_TM", "0")
+        kernel = "opt"
     dims = [9, 8, 10, 8]
     idx = np.array([[1, 2, 3, 0]], dtype=np.uint32)
     b = api.DataBundle(api.SparseTensor(dims, idx, np.array([2.5])), [])
@@ -582,7 +588,7 @@ def test_order4_single_entry_steps_match_oracle(kernel):
     tr.model.copy_from(m0)
     tr.run_epoch()
     api.run_epoch(st)
-    assert st.kernel_info()["kernel"] == "order4"
+    assert st.kernel_info()["kernel"] == want
     m = st.model
     for a, ref, a0 in zip([m.core.reshape(-1)] + m.factors, [tr.model.core] + tr.model.factors,
                           [m0.core.reshape(-1)] + m0.factors):
@@ -604,7 +610,7 @@ def test_config4_rmse_within_1pct_of_reference():
     st = api.make_state(TrainConfig(ranks=[8] * 4, eta0=1e-3, mu=0.1, lambda_reg=0.01), b)
     for _ in range(10):
         api.run_epoch(st)
-    assert st.kernel_info()["kernel"] == "order4"
+    assert st.kernel_info()["kernel"] == "order4tm"
     tr = api.epoch_stats(st, 0.01).train_rmse
     te = api.test_rmse(st, test)
     assert abs(tr - ref["train"][-1]) <= 0.01 * ref["train"][-1], (tr, ref["train"][-1])
@@ -928,7 +934,9 @@ def _visit_cases():
         ("order3tm, blocked order", synth.config5_small(200_000), [10, 10, 10],
          {"env": {"CMTF_TM_BLOCKS": "8"}}),
         ("order3v2 naive", c2, [10, 10, 10], {"kernel": "naive"}),
-        ("order4", c4, [8, 8, 8, 8], {}),
+        ("order4tm", c4, [8, 8, 8, 8], {}),
+        ("order4 (mma.sync)", c4, [8, 8, 8, 8], {"env": {"CMTF_V4_TM": "0"}}),
+        ("order4 naive", c4, [8, 8, 8, 8], {"kernel": "naive"}),
         ("generic (CP core)", c1, [5, 5, 5], {"core_structure": "cp"}),
     ]
 
