@@ -395,6 +395,12 @@ def run_ours(args):
             "frac_at_measured_clock": ((nt * Ft / (ten_ms * 1e-3) / 1e12)
                                        / fp32_peak_tflops(sms, clk["sm_mhz"])
                                        if clk.get("sm_mhz") and not hbm_bound else None)})
+    if info["kernel"] in ("order3tm", "order4tm"):
+        roof["note"] = ("flops are the algorithmic 6*prod(J) per update of SURVEY 8(d), counted "
+                        "against the CUDA-core FP32 peak; the tcgen05 kernels run the "
+                        "contractions on the tensor cores (three fp16 MMAs per product, fp32 "
+                        "accumulate) and ~3J^2 (order 3) / ~5J^2 (order 4) FP32 FMAs per update, "
+                        "so the fraction is not capped by 1")
     # DRAM traffic per launch of the dominant kernel, from the committed ncu
     # --set full capture of the same command (profiles/ncu_r1_metrics.json)
     try:
