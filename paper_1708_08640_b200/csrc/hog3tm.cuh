@@ -51,6 +51,13 @@
 #ifndef CMTF_TM_MPF
 #define CMTF_TM_MPF 0  // matrix entries fetched one entry ahead: config 2 -0.9%, config 5 (rank 5) +13% -- off
 #endif
+#ifndef CMTF_TM_MPFL2
+#define CMTF_TM_MPFL2 0  // > 0: the rows (slot, coefficient) of a lane's next matrix entry are
+                         // prefetched into L2 this many iterations before the warp's matrix step
+                         // is due (the step itself fetches them synchronously).  Measured same-box
+                         // with 2: config 5 @1e9 +0.7%, config 3 +0.4%, config 2 +0.8% -- off: the
+                         // matrix phase's 13% of the warp's cycles is not its DRAM round trips
+#endif
 #ifndef CMTF_TM_FSTAGE
 #define CMTF_TM_FSTAGE 1  // hot-row merges with cp.async-staged global reads
 #endif
@@ -907,6 +914,18 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
     TMP(6);
     // ---- matrix entries due by this iteration (interleaved) ----
     const uint64_t mdue = mlo + msched.step();
+#if CMTF_TM_MPFL2 > 0 && !CMTF_TM_MPF
+    // the warp's next matrix step comes exactly CMTF_TM_MPFL2 iterations from
+    // now: pull the lines it will read (record mrn is in registers) into L2
+    if (msched.due_in(CMTF_TM_MPFL2) && mpos >= mdue && mpos < mhi) {
+      const MatDesc3& M = a.mats[mrn.w];
+      if (a.hot[M.mode].slot) prefetch_l2(a.hot[M.mode].slot + mrn.x);
+      if (M.hotV.slot) prefetch_l2(M.hotV.slot + mrn.y);
+      prefetch_l2(M.vreg + mrn.y);
+      prefetch_row_l2<JP>(a.U[M.mode] + (uint64_t)mrn.x * JP);
+      prefetch_row_l2<JP>(M.V + (uint64_t)mrn.y * JP);
+    }
+#endif
 #if CMTF_TM_MPF
     matrix_entries_until_pf<J, JP>(a, sm, mpos, mpf, mdue, mhi, lane);
 #else

@@ -723,6 +723,11 @@ struct MatSched {
     }
     return rel < cnt_l ? rel : cnt_l;
   }
+  // after step(): the next step that advances `rel` is exactly d iterations
+  // away (fewer than one matrix entry per iteration)
+  __device__ __forceinline__ bool due_in(uint32_t d) const {
+    return cnt_w < iters && acc + d * cnt_w >= iters && acc + (d - 1) * cnt_w < iters;
+  }
 };
 
 // Matrix entries of this lane up to `due`, in lockstep across the warp.
