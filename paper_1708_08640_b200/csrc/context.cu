@@ -27,6 +27,7 @@
 #include "hog4.cuh"
 #include "hog4tm.cuh"
 #include "hog3tm.cuh"
+#include "eval3tm.cuh"
 #include "stateless64.cuh"
 
 #include "host_rng.hpp"
@@ -194,6 +195,8 @@ struct cmtf_gpu_ctx {
 
   // scratch
   double* d_partial = nullptr;
+  double* d_partial2 = nullptr;  // reduce_partials' second level
+  uint64_t partial2_cap = 0;
   uint64_t partial_cap = 0;
   unsigned long long* d_first = nullptr;
 
@@ -280,6 +283,7 @@ struct cmtf_gpu_ctx {
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
+    bool eval_tm = true;   // CMTF_EVAL_TM=0: order-3 eval on eval3_kernel (CUDA cores) instead of eval3tm
   } env;
   int hog_threads_used = 0;
 
@@ -931,12 +935,48 @@ int ensure_partials(cmtf_gpu_ctx* ctx, uint64_t n) {
   return CMTF_OK;
 }
 
-// blocked_sum's pairwise combine over block partials (src/eval.cpp:46-48).
-double pairwise(std::vector<double>& p) {
-  if (p.empty()) return 0.0;
-  for (size_t width = 1; width < p.size(); width *= 2)
-    for (size_t i = 0; i + width < p.size(); i += 2 * width) p[i] += p[i + width];
-  return p[0];
+// blocked_sum's pairwise combine over block partials (src/eval.cpp:46-48) on
+// the device: the reference's tree -- element i takes element
+// i + width at every width = 1, 2, 4, ... -- evaluated chunk by chunk (a
+// 1024-aligned chunk's subtree is closed under the pairing, so the chunk
+// results combine by the same rule one level up).  Missing partners are
+// zeros (x + 0 = x), so the result is bit-identical to the host loop.
+__global__ void __launch_bounds__(512) pairwise_chunk_kernel(const double* in, uint64_t n,
+                                                              double* out) {
+  __shared__ double s[1024];
+  const uint64_t base = (uint64_t)blockIdx.x * 1024;
+  for (int i = threadIdx.x; i < 1024; i += 512) s[i] = base + i < n ? in[base + i] : 0.0;
+  __syncthreads();
+  for (int w = 1; w < 1024; w *= 2) {
+    const int i = threadIdx.x * 2 * w;
+    if (i + w < 1024) s[i] += s[i + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = s[0];
+}
+
+// Sum of d_partial[0, n) by the pairwise tree; only the result crosses PCIe.
+int reduce_partials(cmtf_gpu_ctx* ctx, uint64_t n, double* out) {
+  const uint64_t n1 = (n + 1023) / 1024;
+  if (n1 + 1 > ctx->partial2_cap) {
+    TRY(dalloc(ctx, &ctx->d_partial2, n1 + 1));
+    ctx->partial2_cap = n1 + 1;
+  }
+  const double* src = ctx->d_partial;
+  double* dst = ctx->d_partial2;
+  double* other = ctx->d_partial;  // level >= 2 results go back into the front of d_partial
+  uint64_t m = n;
+  do {
+    const uint64_t nb = (m + 1023) / 1024;
+    pairwise_chunk_kernel<<<(unsigned)nb, 512, 0, ctx->stream>>>(src, m, dst);
+    CU(cudaGetLastError());
+    src = dst;
+    std::swap(dst, other);
+    m = nb;
+  } while (m > 1);
+  CU(cudaMemcpyAsync(out, src, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return CMTF_OK;
 }
 
 bool fast3_supported(const cmtf_gpu_ctx* ctx, int* J) {
@@ -1001,6 +1041,18 @@ int launch_hog3(cmtf_gpu_ctx* ctx, int J, const Hog3Args& args, bool opt,
 template <int J>
 int launch_eval3_t(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
                    double* partial) {
+  if constexpr (J == 4 || J == 5 || J == 8 || J == 10) {
+    if (ctx->env.eval_tm) {  // the contraction on tcgen05 (eval3tm.cuh)
+      const uint64_t nblk = (nnz + kEvalBlock - 1) / kEvalBlock;
+      const uint64_t cap = (uint64_t)ctx->num_sms * CMTF_EVAL_TM_OCC;
+      const unsigned grid = (unsigned)(nblk < cap ? nblk : cap);
+      eval3tm_kernel<J><<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(rec), nnz,
+                                                       ctx->U[0], ctx->U[1], ctx->U[2], ctx->G,
+                                                       partial, nblk);
+      CU(cudaGetLastError());
+      return CMTF_OK;
+    }
+  }
   constexpr int J3P = round_up4(J);
   const size_t smem = sizeof(float) * (size_t)(J * J * J3P + 4 * round_up4(J) * 256);
   auto kern = eval3_kernel<J, J, J>;
@@ -1051,12 +1103,7 @@ int tensor_sse(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
         cs, ctx->G, rec, nnz, mode_tables(ctx), ctx->d_partial);
     CU(cudaGetLastError());
   }
-  std::vector<double> h(nb);
-  CU(cudaMemcpyAsync(h.data(), ctx->d_partial, nb * sizeof(double),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  *out = pairwise(h);
-  return CMTF_OK;
+  return reduce_partials(ctx, nb, out);
 }
 
 int matrix_sse(cmtf_gpu_ctx* ctx, const DevMatrix& m, double* out) {
@@ -1070,12 +1117,7 @@ int matrix_sse(cmtf_gpu_ctx* ctx, const DevMatrix& m, double* out) {
       m.rec, m.nnz, ctx->U[m.mode], m.V, ctx->J(m.mode), ctx->JP(m.mode),
       ctx->d_partial);
   CU(cudaGetLastError());
-  std::vector<double> h(nb);
-  CU(cudaMemcpyAsync(h.data(), ctx->d_partial, nb * sizeof(double),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  *out = pairwise(h);
-  return CMTF_OK;
+  return reduce_partials(ctx, nb, out);
 }
 
 int row_norms(cmtf_gpu_ctx* ctx, const float* F, uint32_t rows, uint32_t J,
@@ -2101,6 +2143,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       const char* w = std::getenv("CMTF_TM_STRIDED");
       ctx->env.tm_strided = w && w[0] == '1';
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
+      ctx->env.eval_tm = !off("CMTF_EVAL_TM");
       if (const char* h = std::getenv("CMTF_TM_SEQ")) ctx->env.tm_seq = atoi(h);
       if (const char* h = std::getenv("CMTF_TM_PFL2")) ctx->env.tm_pfl2 = atoi(h) ? 1 : 0;
       if (const char* b = std::getenv("CMTF_TM_BLOCKS"))
@@ -2199,6 +2242,7 @@ int cmtf_gpu_destroy(cmtf_gpu_ctx* ctx) {
   dfree(ctx->G);
   dfree(ctx->d_sched);
   dfree(ctx->d_partial);
+  dfree(ctx->d_partial2);
   dfree(ctx->d_first);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
