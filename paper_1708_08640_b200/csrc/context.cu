@@ -110,6 +110,9 @@ struct DevMatrix {
 
 }  // namespace
 
+constexpr int kUpChunks = 16;                 // upload copy/pack chunks (at most)
+constexpr uint64_t kUpChunkMin = 1ull << 20;  // entries per chunk (at least)
+
 struct cmtf_gpu_ctx {
   cmtf_gpu_config cfg{};
   std::vector<uint32_t> ranks;
@@ -261,7 +264,7 @@ struct cmtf_gpu_ctx {
   // timing
   cudaEvent_t ev[6] = {};
   cudaEvent_t uev[8] = {};
-  cudaEvent_t cev[4] = {};  // upload chunk copies
+  cudaEvent_t cev[16] = {};  // upload chunk copies (kUpChunks)
   double last_ms[4] = {0, 0, 0, 0};
   int32_t last_launches = 0;
   int kernel_which = 0;
@@ -283,6 +286,7 @@ struct cmtf_gpu_ctx {
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
+    int up_chunks = 16;    // CMTF_UP_CHUNKS=n: upload copy/pack chunks (1..16)
     bool eval_tm = true;   // CMTF_EVAL_TM=0: order-3 eval on eval3_kernel (CUDA cores) instead of eval3tm
   } env;
   int hog_threads_used = 0;
@@ -2144,6 +2148,8 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.tm_strided = w && w[0] == '1';
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
       ctx->env.eval_tm = !off("CMTF_EVAL_TM");
+      if (const char* v = std::getenv("CMTF_UP_CHUNKS"))
+        ctx->env.up_chunks = std::min(kUpChunks, std::max(1, std::atoi(v)));
       if (const char* h = std::getenv("CMTF_TM_SEQ")) ctx->env.tm_seq = atoi(h);
       if (const char* h = std::getenv("CMTF_TM_PFL2")) ctx->env.tm_pfl2 = atoi(h) ? 1 : 0;
       if (const char* b = std::getenv("CMTF_TM_BLOCKS"))
@@ -2412,8 +2418,11 @@ struct PhaseTimer {
   }
 };
 
+
 // The upload staging (up to ~45 bytes per entry: 45 GB at 1e9 entries) is
-// released after every upload instead of living with the context.
+// released after every upload instead of living with the context (keeping it
+// while memory is plentiful was measured: no gain beyond the noise of the
+// host-to-device copies, scripts/ab_upload.py).
 void release_staging(cmtf_gpu_ctx* ctx) {
   cudaStreamSynchronize(ctx->side);
   cudaStreamSynchronize(ctx->stream);
@@ -2646,8 +2655,11 @@ int cmtf_gpu_set_tensor(cmtf_gpu_ctx* ctx, const uint32_t* dims,
   // Host (pageable or pinned) or another device's memory: the copies run in
   // chunks on the side stream; each chunk is packed on the main stream as
   // soon as it lands (H2D overlaps validation and packing).
-  constexpr int kChunks = 4;
-  const uint64_t chunk = (nnz + kChunks - 1) / kChunks;
+  // the last chunk's pack + duplicate insert run after the copies end: many
+  // chunks keep that tail short (4 chunks: 40 ms at 9e8 entries), a floor on
+  // the chunk size keeps small uploads at one launch
+  const int kChunks = ctx->env.up_chunks;
+  const uint64_t chunk = std::max<uint64_t>((nnz + kChunks - 1) / kChunks, kUpChunkMin);
   for (int k = 0; k < kChunks; ++k) {
     const uint64_t c0 = k * chunk, c1 = std::min<uint64_t>(nnz, c0 + chunk);
     if (c0 >= c1) break;
@@ -2854,8 +2866,8 @@ int cmtf_gpu_add_matrix(cmtf_gpu_ctx* ctx, int32_t mode0, uint32_t rows,
     const bool direct = ctx->cfg.order_policy != 0;
     uint64_t pa = 1, pb = 0;
     if (shuffled) affine_params(nnz, ctx->cfg.seed + 7 + ctx->mats.size(), &pa, &pb);
-    constexpr int kChunks = 4;
-    const uint64_t chunk = (nnz + kChunks - 1) / kChunks;
+    const int kChunks = ctx->env.up_chunks;
+    const uint64_t chunk = std::max<uint64_t>((nnz + kChunks - 1) / kChunks, kUpChunkMin);
     CU(cudaEventRecord(ctx->ev_side_start, ctx->stream));  // count memset, staging reuse
     CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side_start, 0));
     for (int k = 0; k < kChunks; ++k) {
