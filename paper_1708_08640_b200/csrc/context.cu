@@ -286,6 +286,7 @@ struct cmtf_gpu_ctx {
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
+    bool rrec_late = true; // CMTF_RREC_LATE=0: hog3tm's rrec built before the blocked re-layout
     int up_chunks = 16;    // CMTF_UP_CHUNKS=n: upload copy/pack chunks (1..16)
     bool eval_tm = true;   // CMTF_EVAL_TM=0: order-3 eval on eval3_kernel (CUDA cores) instead of eval3tm
   } env;
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(256) part_tile_kernel(
       const uint32_t t = threadIdx.x + 256 * j;
       if (t < cnt) {
         r[j] = __ldcs(rec + p0 + t);
-        q[j] = __ldcs(rrec + p0 + t);
+        q[j] = rrec ? __ldcs(rrec + p0 + t) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
 #pragma unroll
@@ -818,7 +819,7 @@ __global__ void pack_matrix_kernel(const uint32_t* idx, const double* vals,
 int normalize_pos(cmtf_gpu_ctx* ctx);  // reshuffle machinery, below
 uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx);
 bool tables_beyond_l2(const cmtf_gpu_ctx* ctx);
-int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B);
+int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B, bool rrec_in = true);
 bool vt_wanted(const cmtf_gpu_ctx* ctx);
 int vt_table(cmtf_gpu_ctx* ctx, uint64_t epoch);
 bool tensor_shuffles(const cmtf_gpu_ctx* ctx);
@@ -1836,21 +1837,33 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
   if (mshuf) TRY(take_matrix_order(ctx));
   Hog3v2Args a{};
   if (!fill_sweep_args<3>(ctx, a, eta, t_lo, t_hi, m_lo, m_hi)) return CMTF_OK;
-  if (v3_tm(ctx) && !ctx->rrec_valid) {
-    // built from this epoch's record order (no gather of the next order is
-    // pending here; from now on the reshuffle keeps rrec aligned with rec);
-    // a blocked layout keeps its entry ids
+  const bool whole = t_lo == 0 && t_hi == ctx->nnz && !(m_lo && m_hi);
+  const bool relayout = !ctx->vt_on && whole && vt_wanted(ctx);
+  // rrec: the regulariser coefficients beside the records, built from this
+  // epoch's record order (no gather of the next order is pending here; from
+  // now on the reshuffle keeps rrec aligned with rec); a blocked layout keeps
+  // its entry ids in the fourth word.  When the blocked layout is about to be
+  // made from a fresh upload (ids in closed form), the coefficients are
+  // looked up AFTER the partition: two of the three lookups per record then
+  // fall into the stratum's row blocks (L2) instead of three 40 MB tables,
+  // and the partition's first pass does not read rrec at all.
+  const bool rrec_late = v3_tm(ctx) && !ctx->rrec_valid && relayout && ctx->pos_affine &&
+                         !ctx->pos_ids && ctx->env.rrec_late;
+  auto build_rrec = [&](int keep_w) -> int {
     TRY(ensure(ctx, &ctx->rrec, &ctx->rrec_cap, ctx->nnz));
     build_rrec_kernel<<<grid_for(ctx->nnz), 256, 0, ctx->stream>>>(
         reinterpret_cast<const uint4*>(ctx->rec), ctx->nnz, ctx->reg[0], ctx->reg[1],
-        ctx->reg[2], ctx->rrec, ctx->vt_on ? 1 : 0);
+        ctx->reg[2], ctx->rrec, keep_w);
     CU(cudaGetLastError());
     ctx->rrec_valid = true;
     ctx->last_launches += 1;
-  }
-  const bool whole = t_lo == 0 && t_hi == ctx->nnz && !(m_lo && m_hi);
-  if (!ctx->vt_on && whole && vt_wanted(ctx)) {
-    TRY(vt_setup(ctx, blocks_wanted(ctx)));
+    return CMTF_OK;
+  };
+  if (v3_tm(ctx) && !ctx->rrec_valid && !rrec_late) TRY(build_rrec(ctx->vt_on ? 1 : 0));
+  if (relayout) {
+    if (rrec_late) TRY(ensure(ctx, &ctx->rrec, &ctx->rrec_cap, ctx->nnz));
+    TRY(vt_setup(ctx, blocks_wanted(ctx), /*rrec_in=*/!rrec_late));
+    if (rrec_late) TRY(build_rrec(1));
     TRY(vt_table(ctx, (uint64_t)ctx->epoch));
   }
   a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;  // after a re-layout
@@ -2148,6 +2161,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.tm_strided = w && w[0] == '1';
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
       ctx->env.eval_tm = !off("CMTF_EVAL_TM");
+      ctx->env.rrec_late = !off("CMTF_RREC_LATE");
       if (const char* v = std::getenv("CMTF_UP_CHUNKS"))
         ctx->env.up_chunks = std::min(kUpChunks, std::max(1, std::atoi(v)));
       if (const char* h = std::getenv("CMTF_TM_SEQ")) ctx->env.tm_seq = atoi(h);
@@ -3297,7 +3311,7 @@ uint32_t blocks_wanted(const cmtf_gpu_ctx* ctx) {
 // rrec, ids in .w) out stratum-major -- a stable radix sort of the positions
 // by stratum keeps the random order inside a stratum -- and rebuild pos[]
 // from the ids.  The layout then stays until the next upload.
-int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B) {
+int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B, bool rrec_in_valid) {
   const uint64_t n = ctx->nnz;
   PhaseTimer pt("vt_setup", ctx);
   drain_side(ctx);
@@ -3344,7 +3358,8 @@ int vt_setup(cmtf_gpu_ctx* ctx, uint32_t B) {
   TRY(ensure(ctx, &ctx->rrec_alt, &ctx->rrec_alt_cap, n));
   const unsigned tg = (unsigned)std::min<uint64_t>((n + kTile - 1) / kTile, 148ull * 4);
   const uint4* rec_in = reinterpret_cast<const uint4*>(ctx->rec);
-  const uint4* rrec_in = reinterpret_cast<const uint4*>(ctx->rrec);
+  // rrec not built yet (closed-form ids): the first pass writes {0, 0, 0, id}
+  const uint4* rrec_in = rrec_in_valid ? reinterpret_cast<const uint4*>(ctx->rrec) : nullptr;
   uint4* rec_o = reinterpret_cast<uint4*>(ctx->rec_alt);
   uint4* rrec_o = reinterpret_cast<uint4*>(ctx->rrec_alt);
   if (S <= 64) {  // one pass; the result is in the alternate buffers
