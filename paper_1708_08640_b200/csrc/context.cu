@@ -1083,10 +1083,18 @@ int tensor_sse(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
   int J = 0;
   if (ctx->order == 4 && ctx->ranks[0] == 8 && ctx->ranks[1] == 8 && ctx->ranks[2] == 8 &&
       ctx->ranks[3] == 8 && !ctx->cfg.force_generic) {
-    const size_t smem = sizeof(float) * 8 * 8 * 8 * 8;
-    eval4_kernel<<<(unsigned)nb, 256, smem, ctx->stream>>>(rec, nnz, ctx->U[0], ctx->U[1],
-                                                           ctx->U[2], ctx->U[3], ctx->G,
-                                                           ctx->d_partial);
+    if (ctx->env.eval_tm) {  // the contraction on tcgen05 (eval3tm.cuh)
+      CU(cudaFuncSetAttribute(eval4tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kEval4tmSmem));
+      const uint64_t cap = (uint64_t)ctx->num_sms * CMTF_EVAL_TM_OCC;
+      eval4tm_kernel<<<(unsigned)std::min<uint64_t>(nb, cap), 128, kEval4tmSmem, ctx->stream>>>(
+          rec, nnz, ctx->U[0], ctx->U[1], ctx->U[2], ctx->U[3], ctx->G, ctx->d_partial, nb);
+    } else {
+      const size_t smem = sizeof(float) * 8 * 8 * 8 * 8;
+      eval4_kernel<<<(unsigned)nb, 256, smem, ctx->stream>>>(rec, nnz, ctx->U[0], ctx->U[1],
+                                                             ctx->U[2], ctx->U[3], ctx->G,
+                                                             ctx->d_partial);
+    }
     CU(cudaGetLastError());
   } else if (fast3_supported(ctx, &J)) {
     switch (J) {

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "hog3tm.cuh"
+#include "hog4tm.cuh"
 #include "umma.cuh"
 
 namespace cmtfb {
@@ -204,6 +205,182 @@ eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restr
   umma::fence_before();
   __syncthreads();
   if (w == 0) umma::tmem_free<TMC>(tmem_base);
+}
+
+// Order 4, J = 8 (BASELINE configs[3]): hog4tm's first sweep contraction per
+// tile of 128 entries,
+//   M1[e][(a,b)] = sum_cd q_e[cd] G[ab][cd],  q[(c,d)] = u3[c] u4[d]
+// (A = Q tile, 8 planes of [128 entries][8 fp16], K-major; B = G, K-major;
+// K = 64 in four steps, split-fp16 x3), then x_hat = sum_ab M1[ab] u1[a] u2[b]
+// in FP32: J^2 + J FMAs and J^2 packed-fp16 operand products per entry instead
+// of eval4_kernel's J^4 + ... CUDA-core FMAs.  Same block / partial scheme as
+// eval3tm_kernel; dynamic shared memory: G hi, G lo, Q hi, Q lo.
+constexpr int kEval4tmSmem = 2 * TM4Layout::G_TILE + 2 * TM4Layout::TILE;
+
+__global__ void __launch_bounds__(128, CMTF_EVAL_TM_OCC)
+eval4tm_kernel(const uint32_t* __restrict__ rec, uint64_t nnz, const float* __restrict__ U1,
+               const float* __restrict__ U2, const float* __restrict__ U3,
+               const float* __restrict__ U4, const float* __restrict__ G,
+               double* __restrict__ partial, uint64_t nblk) {
+  using L = TM4Layout;
+  constexpr int J = 8;
+  extern __shared__ __align__(1024) uint8_t smb4[];
+  uint8_t* Gh = smb4;
+  uint8_t* Gl = Gh + L::G_TILE;
+  uint8_t* Qh = Gl + L::G_TILE;
+  uint8_t* Ql = Qh + L::TILE;
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  __shared__ double acc_s[4];
+  const int e = threadIdx.x, w = e >> 5, lane = e & 31;
+
+  for (int q = e; q < 4096; q += 128) {  // G[(a,b)][(c,d)]: plane c, row (a,b)
+    const int ab = q >> 6, cd = q & 63;
+    __half h, l;
+    split_h(__ldg(G + q) * kS4g, h, l);
+    const int o = (cd >> 3) * L::G_PLANE + ab * 16 + (cd & 7) * 2;
+    *reinterpret_cast<__half*>(Gh + o) = h;
+    *reinterpret_cast<__half*>(Gl + o) = l;
+  }
+  if (e == 0) {
+    umma::mbar_init(&mbar, 1);
+    umma::fence_mbar_init();
+  }
+  if (w == 0) umma::tmem_alloc<64>(&tmem_base);
+  umma::fence_async_smem();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tm = tmem_base;
+  const uint32_t tm_lane = (uint32_t)(32 * w) << 16;
+  const uint32_t sQh = umma::smem_u32(Qh), sQl = umma::smem_u32(Ql);
+  const uint32_t sGh = umma::smem_u32(Gh), sGl = umma::smem_u32(Gl);
+  constexpr uint32_t ID = umma::idesc_f16(128, 64, false, false);
+  constexpr float kInv = 1.f / (kS4a * kS4b * kS4g);
+
+  auto load_row = [&](const float* U, uint32_t i, float* r) {
+    const float4 q0 = __ldg(reinterpret_cast<const float4*>(U + (uint64_t)i * 8));
+    const float4 q1 = __ldg(reinterpret_cast<const float4*>(U + (uint64_t)i * 8 + 4));
+    r[0] = q0.x; r[1] = q0.y; r[2] = q0.z; r[3] = q0.w;
+    r[4] = q1.x; r[5] = q1.y; r[6] = q1.z; r[7] = q1.w;
+  };
+  struct Rec5 { uint32_t i[4]; float x; };
+  auto load_rec = [&](uint64_t p) -> Rec5 {  // records are 5 words: i1..i4, bits(x)
+    Rec5 r;
+    const uint32_t* q = rec + 5 * p;
+    r.i[0] = __ldg(q); r.i[1] = __ldg(q + 1); r.i[2] = __ldg(q + 2); r.i[3] = __ldg(q + 3);
+    r.x = __uint_as_float(__ldg(q + 4));
+    return r;
+  };
+  const uint64_t nmine = blockIdx.x < nblk ? (nblk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t ntile = nmine * 8;
+  auto entry_of = [&](uint64_t s) -> uint64_t {
+    const uint64_t blk = blockIdx.x + (s >> 3) * (uint64_t)gridDim.x;
+    return blk * kEvalBlock + (s & 7) * 128 + e;
+  };
+  const Rec5 zero{{0u, 0u, 0u, 0u}, 0.f};
+  Rec5 rc = ntile > 0 && entry_of(0) < nnz ? load_rec(entry_of(0)) : zero;
+  Rec5 rc1 = ntile > 1 && entry_of(1) < nnz ? load_rec(entry_of(1)) : zero;
+  float u1[8], u2[8], u3[8], u4[8];
+  load_row(U1, rc.i[0], u1);
+  load_row(U2, rc.i[1], u2);
+  load_row(U3, rc.i[2], u3);
+  load_row(U4, rc.i[3], u4);
+
+  uint32_t par = 0;
+  double acc = 0.0;
+  for (uint64_t s = 0; s < ntile; ++s) {
+    const bool act = entry_of(s) < nnz;
+    const Rec5 rc2 = s + 2 < ntile && entry_of(s + 2) < nnz ? load_rec(entry_of(s + 2)) : zero;
+    {  // this entry's Q planes (fp16 hi / lo) by packed fp16 arithmetic
+      __half2 yh[4], yl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x0 = u4[2 * k] * kS4b, x1 = u4[2 * k + 1] * kS4b;
+        const float h0 = __uint_as_float(__float_as_uint(x0) & 0xffffe000u);
+        const float h1 = __uint_as_float(__float_as_uint(x1) & 0xffffe000u);
+        yh[k] = __floats2half2_rn(h0, h1);
+        yl[k] = __floats2half2_rn(x0 - h0, x1 - h1);
+      }
+#pragma unroll
+      for (int ic = 0; ic < J; ++ic) {
+        __half h, l;
+        split_h(u3[ic] * kS4a, h, l);
+        uint4 qh, ql;
+        split_outer8(__half2half2(h), __half2half2(l), yh, yl, qh, ql);
+        *reinterpret_cast<uint4*>(Qh + ic * L::PLANE + e * 16) = qh;
+        *reinterpret_cast<uint4*>(Ql + ic * L::PLANE + e * 16) = ql;
+      }
+    }
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    if (e == 0) {
+      umma::fence_after();
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t dAh = umma::desc(sQh + ks * 2 * L::PLANE, L::PLANE, 128);
+        const uint64_t dAl = umma::desc(sQl + ks * 2 * L::PLANE, L::PLANE, 128);
+        const uint64_t dBh = umma::desc(sGh + ks * 2 * L::G_PLANE, L::G_PLANE, 128);
+        const uint64_t dBl = umma::desc(sGl + ks * 2 * L::G_PLANE, L::G_PLANE, 128);
+        umma::mma_f16(tm, dAh, dBh, ID, ks > 0 ? 1u : 0u);
+        umma::mma_f16(tm, dAh, dBl, ID, 1u);
+        umma::mma_f16(tm, dAl, dBh, ID, 1u);
+      }
+      umma::commit(&mbar);
+    }
+    // next tile's rows while the MMAs run (this tile's u3, u4 are in the Q tile)
+    float n1[8], n2[8];
+    load_row(U3, rc1.i[2], u3);
+    load_row(U4, rc1.i[3], u4);
+    load_row(U1, rc1.i[0], n1);
+    load_row(U2, rc1.i[1], n2);
+    float w1[J];
+#pragma unroll
+    for (int k = 0; k < J; ++k) w1[k] = 0.f;
+    umma::mbar_wait(&mbar, par);
+    par ^= 1u;
+    umma::fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      float v[16];
+      umma::ld16(tm + tm_lane + c0, v);
+      umma::ld_wait();
+      umma::ld_fence_regs<16>(v);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int ia = (c0 + q) >> 3, ib = (c0 + q) & 7;
+        w1[ia] = fmaf(v[q], u2[ib], w1[ia]);
+      }
+    }
+    float xh = 0.f;
+#pragma unroll
+    for (int k = 0; k < J; ++k) xh = fmaf(w1[k], u1[k], xh);
+    xh *= kInv;
+    if (act) {
+      const double r = (double)rc.x - (double)xh;
+      acc += r * r;
+    }
+    if ((s & 7) == 7) {
+      const double ws = warp_sum_d(acc);
+      if (lane == 0) acc_s[w] = ws;
+      __syncthreads();
+      if (e == 0)
+        partial[blockIdx.x + (s >> 3) * (uint64_t)gridDim.x] =
+            (acc_s[0] + acc_s[1]) + (acc_s[2] + acc_s[3]);
+      acc = 0.0;
+    }
+    rc = rc1;
+    rc1 = rc2;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      u1[k] = n1[k];
+      u2[k] = n2[k];
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (w == 0) umma::tmem_free<64>(tmem_base);
 }
 
 }  // namespace cmtfb

@@ -1,6 +1,6 @@
 """epoch_stats / test_rmse time and value with the tcgen05 eval (default) and
 the CUDA-core eval3_kernel (CMTF_EVAL_TM=0) on one workload, same model:
-  python scripts/stats_ab.py config5 1e9 | config3 | config2"""
+  python scripts/stats_ab.py config5 1e9 | config4 [scale] | config3 | config2"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,12 +11,14 @@ if which == "config5":
     b, test = synth_gpu.generate(spec, device="cuda:0")
 elif which == "config3":
     b, test = synth_gpu.generate(synth_gpu.config3(1.0), device="cuda:0")
+elif which == "config4":
+    b, test = synth_gpu.generate(synth_gpu.config4(float(sys.argv[2]) if len(sys.argv) > 2 else 1.0), device="cuda:0")
 else:
     b, test, _ = synth.generate(synth.config2(1.0))
 out = {}
 for tm in ("1", "0"):
     os.environ["CMTF_EVAL_TM"] = tm
-    st = api.make_state(api.TrainConfig(ranks=[10, 10, 10], seed=0, eta0=1e-3, lambda_reg=0.01), b)
+    st = api.make_state(api.TrainConfig(ranks=([8] * 4 if which == "config4" else [10, 10, 10]), seed=0, eta0=1e-3, lambda_reg=0.01), b)
     api.run_epoch(st)
     ts = []
     for _ in range(4):
