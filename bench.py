@@ -462,9 +462,10 @@ def run_ours(args):
         h2d = bundle.tensor.indices.nbytes + bundle.tensor.values.nbytes + sum(
             m.indices.nbytes + m.values.nbytes for m in bundle.matrices)
         # the caller's host buffers live in pinned memory (as a data loader's would),
-        # on the GPU's own NUMA node (what `numactl --cpunodebind` gives a job: pinned
-        # pages land where the thread that first touches them runs; from the far
-        # socket the same copies ran at 18 instead of 46 GB/s on these boxes)
+        # first touched from the GPU-local CPUs (what `numactl --cpunodebind` gives a
+        # job on a multi-socket host; a no-op on this pool's single-node 16-vCPU VMs,
+        # whose upload rate still varied between 18 and 46 GB/s from run to run --
+        # `upload_gbs` says what this run got)
         from paper_1708_08640_b200.api import CoupledMatrix, DataBundle, SparseTensor
         aff0, numa = None, "unbound"
         try:
