@@ -288,6 +288,7 @@ struct cmtf_gpu_ctx {
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
     bool rrec_late = true; // CMTF_RREC_LATE=0: hog3tm's rrec built before the blocked re-layout
     int up_chunks = 16;    // CMTF_UP_CHUNKS=n: upload copy/pack chunks (1..16)
+    bool eval_stream3 = true; // CMTF_EVAL_STREAM3=0: eval3tm reads the unblocked mode's rows with plain loads
     bool eval_tm = true;   // CMTF_EVAL_TM=0: order-3 eval on eval3_kernel (CUDA cores) instead of eval3tm
   } env;
   int hog_threads_used = 0;
@@ -1053,7 +1054,8 @@ int launch_eval3_t(cmtf_gpu_ctx* ctx, const uint32_t* rec, uint64_t nnz,
       const unsigned grid = (unsigned)(nblk < cap ? nblk : cap);
       eval3tm_kernel<J><<<grid, 128, 0, ctx->stream>>>(reinterpret_cast<const uint4*>(rec), nnz,
                                                        ctx->U[0], ctx->U[1], ctx->U[2], ctx->G,
-                                                       partial, nblk);
+                                                       partial, nblk,
+                                                       rec == ctx->rec && ctx->vt_on && ctx->env.eval_stream3 ? 1 : 0);
       CU(cudaGetLastError());
       return CMTF_OK;
     }
@@ -2169,6 +2171,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
       ctx->env.tm_strided = w && w[0] == '1';
       ctx->env.tm_vorder = !off("CMTF_TM_VORDER");
       ctx->env.eval_tm = !off("CMTF_EVAL_TM");
+      ctx->env.eval_stream3 = !off("CMTF_EVAL_STREAM3");
       ctx->env.rrec_late = !off("CMTF_RREC_LATE");
       if (const char* v = std::getenv("CMTF_UP_CHUNKS"))
         ctx->env.up_chunks = std::min(kUpChunks, std::max(1, std::atoi(v)));

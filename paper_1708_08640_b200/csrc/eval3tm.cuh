@@ -41,7 +41,8 @@ template <int J>
 __global__ void __launch_bounds__(128, CMTF_EVAL_TM_OCC)
 eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restrict__ U1,
                const float* __restrict__ U2, const float* __restrict__ U3,
-               const float* __restrict__ G, double* __restrict__ partial, uint64_t nblk) {
+               const float* __restrict__ G, double* __restrict__ partial, uint64_t nblk,
+               int stream3) {
   using L = TMLayout<J>;
   constexpr int JP = L::JP, AB = L::AB, NT = L::NT;
   constexpr int TMC = EvalTMLayout<J>::TM_COLS;
@@ -90,10 +91,14 @@ eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restr
   uint8_t* myUh = tUh + e * 16;
   uint8_t* myUl = tUl + e * 16;
 
-  auto load_row = [&](const float* U, uint32_t i, float* r) {
+  // stream: evict-first loads.  Under the L2-blocked record layout (modes 1
+  // and 2 in row blocks) the mode-3 rows are the random ones: read
+  // evict-first, their lines do not push the active row blocks out of L2
+  auto load_row = [&](const float* U, uint32_t i, float* r, bool stream = false) {
 #pragma unroll
     for (int k = 0; k < JP; k += 4) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(U + (uint64_t)i * JP + k));
+      const float4* p = reinterpret_cast<const float4*>(U + (uint64_t)i * JP + k);
+      const float4 q = stream ? __ldcs(p) : __ldg(p);
       r[k] = q.x; r[k + 1] = q.y; r[k + 2] = q.z; r[k + 3] = q.w;
     }
   };
@@ -112,18 +117,18 @@ eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restr
     return h < nnz ? h : nnz;
   };
   const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-  uint4 rc = ntile > 0 && entry_of(0) < block_hi(0) ? __ldg(rec + entry_of(0)) : zero4;
-  uint4 rc1 = ntile > 1 && entry_of(1) < block_hi(1) ? __ldg(rec + entry_of(1)) : zero4;
+  uint4 rc = ntile > 0 && entry_of(0) < block_hi(0) ? __ldcs(rec + entry_of(0)) : zero4;
+  uint4 rc1 = ntile > 1 && entry_of(1) < block_hi(1) ? __ldcs(rec + entry_of(1)) : zero4;
   float u1[JP], u2[JP], u3[JP];
   load_row(U1, rc.x, u1);
   load_row(U2, rc.y, u2);
-  load_row(U3, rc.z, u3);
+  load_row(U3, rc.z, u3, stream3 != 0);
 
   uint32_t par = 0;
   double acc = 0.0;
   for (uint64_t s = 0; s < ntile; ++s) {
     const bool act = entry_of(s) < block_hi(s);
-    const uint4 rc2 = s + 2 < ntile && entry_of(s + 2) < block_hi(s + 2) ? __ldg(rec + entry_of(s + 2))
+    const uint4 rc2 = s + 2 < ntile && entry_of(s + 2) < block_hi(s + 2) ? __ldcs(rec + entry_of(s + 2))
                                                                           : zero4;
     // this entry's u3 as fp16 hi/lo rows of the A tile (K = 16, zero padded)
     {
@@ -152,7 +157,7 @@ eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restr
     }
     // next tile's rows while the MMAs run (this tile's u3 is in the A tile)
     float n1[JP], n2[JP];
-    load_row(U3, rc1.z, u3);
+    load_row(U3, rc1.z, u3, stream3 != 0);
     load_row(U1, rc1.x, n1);
     load_row(U2, rc1.y, n2);
     float w1[J];

@@ -170,6 +170,43 @@ def test_epoch_stats_and_test_rmse_match_oracle():
     assert abs(api.test_rmse(st, test) - t_ref) <= 1e-5 * t_ref
 
 
+@pytest.mark.parametrize("order,J,nnz", [(3, 4, 77), (3, 5, 128), (3, 8, 1023), (3, 10, 1025),
+                                          (3, 10, 20_011), (4, 8, 131), (4, 8, 9_001)])
+def test_tcgen05_eval_matches_oracle_on_ragged_sizes(order, J, nnz, monkeypatch):
+    """eval3tm / eval4tm (csrc/eval3tm.cuh; predict_entry src/tucker.cpp:96-127,
+    blocked_sum src/eval.cpp:14-65) against the f64 oracle at a trained model:
+    entry counts below one 128-entry tile, at tile and 1024-block edges and
+    past them, every supported rank; the CUDA-core eval kernel beside it."""
+    spec = synth.config1(literal=False)
+    spec.nnz, spec.seed = int(nnz / 0.9) + 1, 100 + nnz
+    spec.dims = [200, 150, 100] if order == 3 else [40, 30, 20, 16]
+    spec.ranks = [J] * order
+    spec.matrices[0].cols, spec.matrices[0].nnz = 20, 200
+    if order == 4:
+        spec.laws = ["uniform"] * 4
+    b, test, _ = synth.generate(spec)
+    ranks = [J] * order
+    out = {}
+    for tm in ("1", "0"):
+        monkeypatch.setenv("CMTF_EVAL_TM", tm)
+        st = api.make_state(TrainConfig(ranks=ranks, seed=1, eta0=0.005, lambda_reg=0.01), b)
+        if tm == "1":
+            api.run_epoch(st)
+            m = st.model
+        else:
+            st.model = m
+        s = api.epoch_stats(st, 0.01)
+        out[tm] = (s.train_rmse, s.objective, api.test_rmse(st, test))
+        st.close()
+    om = O.OracleModel(b, ranks).copy_from(m)
+    r_ref, o_ref = O.epoch_stats(b, om, 0.01)
+    t_ref = O.tensor_rmse(test, om)
+    for tm in ("1", "0"):
+        _within(out[tm][0], r_ref, 1e-5, f"train_rmse eval_tm={tm}")
+        _within(out[tm][1], o_ref, 1e-5, f"objective eval_tm={tm}")
+        _within(out[tm][2], t_ref, 1e-5, f"test_rmse eval_tm={tm}")
+
+
 def test_initial_model_matches_reference_law():
     # random_model draw law and stream (src/trainer.cpp:30-58,100)
     d = load_npz("epochs.npz")
