@@ -511,7 +511,7 @@ __global__ void remap_pos_kernel(uint32_t* pos, uint64_t count, uint64_t n, uint
 // Each epoch draws a random stratum sequence and a group-affine map per
 // stratum.  rrec[p].w carries the entry id of record p (pos[] is rebuilt
 // from it after the re-layout).
-constexpr int kMaxBlk = 32;
+constexpr int kMaxBlk = 64;
 
 // block of row i: floor(i * B / d), by a float estimate and an exact
 // correction (a 64-bit division is a ~100-instruction routine)
