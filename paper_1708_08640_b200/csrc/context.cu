@@ -285,6 +285,7 @@ struct cmtf_gpu_ctx {
     int tm_pfl2 = -1;      // CMTF_TM_PFL2=0/1: hog3tm L2 prefetch of the next entry's rows (-1 auto)
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
+    int tm_gather_ca = -1; // CMTF_TM_GATHER_CA=0/1: hog3tm row gathers through L1 (-1: with the blocked order)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
     bool rrec_late = true; // CMTF_RREC_LATE=0: hog3tm's rrec built before the blocked re-layout
     int up_chunks = 16;    // CMTF_UP_CHUNKS=n: upload copy/pack chunks (1..16)
@@ -1888,6 +1889,7 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     a.vtab = ctx->vt_on && whole ? ctx->d_vtab : nullptr;
     a.strided = ctx->env.tm_strided || (a.vtab && ctx->blk_B > 1);
     a.pf_l2 = ctx->env.tm_pfl2 > 0 ? 1 : 0;  // measured +10% epoch time on config 5: off
+    a.gather_ca = ctx->env.tm_gather_ca >= 0 ? ctx->env.tm_gather_ca : (a.vtab ? 1 : 0);
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);
@@ -2181,6 +2183,7 @@ int cmtf_gpu_create(const cmtf_gpu_config* cfg, cmtf_gpu_ctx** out) {
         ctx->env.tm_blocks = std::max(0, std::min(kMaxBlk, atoi(b)));
       if (const char* b = std::getenv("CMTF_TM_BULK")) ctx->env.tm_bulk = atoi(b) & 7;
       ctx->env.tm_galt = !off("CMTF_TM_GALT");
+      if (const char* h = std::getenv("CMTF_TM_GATHER_CA")) ctx->env.tm_gather_ca = atoi(h) ? 1 : 0;
     }
   }
   auto cleanup = [&](int rc) {

@@ -33,6 +33,9 @@ struct EvalTMLayout {
   static_assert(NT <= 128, "eval3tm: J^2 <= 128");
 };
 
+#ifndef CMTF_EVAL_TM_POLICY
+#define CMTF_EVAL_TM_POLICY 1  // streamed rows: explicit L2 evict-first policy (0: ld.global.cs)
+#endif
 #ifndef CMTF_EVAL_TM_OCC
 #define CMTF_EVAL_TM_OCC 3  // blocks per SM the register budget is set for
 #endif
@@ -94,11 +97,24 @@ eval3tm_kernel(const uint4* __restrict__ rec, uint64_t nnz, const float* __restr
   // stream: evict-first loads.  Under the L2-blocked record layout (modes 1
   // and 2 in row blocks) the mode-3 rows are the random ones: read
   // evict-first, their lines do not push the active row blocks out of L2
+  uint64_t pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
   auto load_row = [&](const float* U, uint32_t i, float* r, bool stream = false) {
 #pragma unroll
     for (int k = 0; k < JP; k += 4) {
       const float4* p = reinterpret_cast<const float4*>(U + (uint64_t)i * JP + k);
-      const float4 q = stream ? __ldcs(p) : __ldg(p);
+      float4 q;
+      if (stream) {
+#if CMTF_EVAL_TM_POLICY
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+                     : "l"(p), "l"(pol_first));
+#else
+        q = __ldcs(p);
+#endif
+      } else {
+        q = __ldg(p);
+      }
       r[k] = q.x; r[k + 1] = q.y; r[k + 2] = q.z; r[k + 3] = q.w;
     }
   };

@@ -444,22 +444,23 @@ __global__ void __launch_bounds__(256, 1) hog3tm_kernel(Hog3v2Args a) {
   // records two ahead, slots and coefficients one ahead; the next entry's
   // cold rows are copied (cp.async) straight into the operand tiles once the
   // sweep MMAs of the current tile are done
+  const bool gca = a.gather_ca != 0;
   auto issue_rows = [&](const uint4& r, const int* slx, bool act) {
     if (act) {
       if (slx[0] < 0) {
         const float* src = a.U[0] + (uint64_t)r.x * JP;
 #pragma unroll
-        for (int k = 0; k < JP; k += 4) cp_async16(myU1 + k, src + k);
+        for (int k = 0; k < JP; k += 4) cp_async16_sel(myU1 + k, src + k, gca);
       }
       if (slx[1] < 0) {
         const float* src = a.U[1] + (uint64_t)r.y * JP;
 #pragma unroll
-        for (int k = 0; k < JP; k += 4) cp_async16(land(myU2h, myU2l, k >> 2), src + k);
+        for (int k = 0; k < JP; k += 4) cp_async16_sel(land(myU2h, myU2l, k >> 2), src + k, gca);
       }
       if (slx[2] < 0) {
         const float* src = a.U[2] + (uint64_t)r.z * JP;
 #pragma unroll
-        for (int k = 0; k < JP; k += 4) cp_async16(land(myU3h, myU3l, k >> 2), src + k);
+        for (int k = 0; k < JP; k += 4) cp_async16_sel(land(myU3h, myU3l, k >> 2), src + k, gca);
       }
     }
     cp_async_commit();

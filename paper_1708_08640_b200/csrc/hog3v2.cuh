@@ -109,6 +109,7 @@ struct Hog3v2Args {
   // of an iteration before their cp.async gathers are issued (the gathers
   // land in the operand tiles, so they must wait for the sweep MMAs)
   int pf_l2;
+  int gather_ca;        // hog3tm: row gathers through L1 (cp_async16_sel)
 };
 
 // ---------------------------------------------------------------------
@@ -164,6 +165,18 @@ __device__ __forceinline__ float ld_strong(const float* p) {
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+// through L1 (.ca) when `ca`: the 16-byte chunks of one gathered row then
+// reach L2 as one request instead of three.  Worth -3.6% of the epoch where
+// the rows miss L2 (config 5 @1e9: 185.4 -> 178.7 ms) and +8% where they hit
+// (config 3), so the host sets it with the blocked order (tables beyond L2).
+// An L1 line outlives one iteration at most here (the block gathers ~100 KB
+// per iteration into an L1 of a few tens of KB beside its shared memory), the
+// staleness the one-entry-ahead gathers already have.
+__device__ __forceinline__ void cp_async16_sel(float* smem_dst, const float* gsrc, bool ca) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  if (ca) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+  else asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
