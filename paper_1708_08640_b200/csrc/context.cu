@@ -285,7 +285,7 @@ struct cmtf_gpu_ctx {
     int tm_pfl2 = -1;      // CMTF_TM_PFL2=0/1: hog3tm L2 prefetch of the next entry's rows (-1 auto)
     bool tm_vorder = true; // CMTF_TM_VORDER=0: hog3tm reshuffles its records physically
     int tm_bulk = -1;      // CMTF_TM_BULK=mask: modes whose cold-row steps are bulk reductions (-1 auto)
-    int tm_gather_ca = -1; // CMTF_TM_GATHER_CA=0/1: hog3tm row gathers through L1 (-1: with the blocked order)
+    int tm_gather_ca = -1; // CMTF_TM_GATHER_CA=0/1: order-3 row gathers through L1 (-1: when the tables exceed L2)
     bool tm_galt = true;   // CMTF_TM_GALT=0: both warpgroups convert every core refresh
     bool rrec_late = true; // CMTF_RREC_LATE=0: hog3tm's rrec built before the blocked re-layout
     int up_chunks = 16;    // CMTF_UP_CHUNKS=n: upload copy/pack chunks (1..16)
@@ -1878,6 +1878,8 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     TRY(vt_table(ctx, (uint64_t)ctx->epoch));
   }
   a.rec = reinterpret_cast<const uint4*>(ctx->rec) + t_lo;  // after a re-layout
+  // row gathers through L1 where the factor tables miss L2 (hog3tm, hog3v2: cp_async16_sel)
+  a.gather_ca = ctx->env.tm_gather_ca >= 0 ? ctx->env.tm_gather_ca : (tables_beyond_l2(ctx) ? 1 : 0);
   TRY(prefetch_orders(ctx, mshuf && t_lo == 0 && t_hi == ctx->nnz, mshuf));
   ctx->kernel_which = 3;
   const bool opt = ctx->cfg.kernel == CMTF_KERNEL_OPT;
@@ -1889,7 +1891,6 @@ int v2_sweep(cmtf_gpu_ctx* ctx, int J, float eta, uint64_t t_lo, uint64_t t_hi,
     a.vtab = ctx->vt_on && whole ? ctx->d_vtab : nullptr;
     a.strided = ctx->env.tm_strided || (a.vtab && ctx->blk_B > 1);
     a.pf_l2 = ctx->env.tm_pfl2 > 0 ? 1 : 0;  // measured +10% epoch time on config 5: off
-    a.gather_ca = ctx->env.tm_gather_ca >= 0 ? ctx->env.tm_gather_ca : (a.vtab ? 1 : 0);
     ctx->kernel_which = 5;
     switch (J) {
       case 4: return launch_v3tm<4>(ctx, a);

@@ -109,7 +109,7 @@ struct Hog3v2Args {
   // of an iteration before their cp.async gathers are issued (the gathers
   // land in the operand tiles, so they must wait for the sweep MMAs)
   int pf_l2;
-  int gather_ca;        // hog3tm: row gathers through L1 (cp_async16_sel)
+  int gather_ca;        // row gathers through L1 (cp_async16_sel)
 };
 
 // ---------------------------------------------------------------------
@@ -169,7 +169,8 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
 // through L1 (.ca) when `ca`: the 16-byte chunks of one gathered row then
 // reach L2 as one request instead of three.  Worth -3.6% of the epoch where
 // the rows miss L2 (config 5 @1e9: 185.4 -> 178.7 ms) and +8% where they hit
-// (config 3), so the host sets it with the blocked order (tables beyond L2).
+// (config 3), so the host sets it when the factor tables exceed L2 (naive
+// kernel on config 5 @1e9: 433.2 -> 403.4 ms).
 // An L1 line outlives one iteration at most here (the block gathers ~100 KB
 // per iteration into an L1 of a few tens of KB beside its shared memory), the
 // staleness the one-entry-ahead gathers already have.
@@ -850,7 +851,7 @@ hog3v2_kernel(Hog3v2Args a) {
         if (slx[j][n] < 0) {
           const float* src = a.U[n] + (uint64_t)ix[n] * JP;
 #pragma unroll
-          for (int k = 0; k < JP; k += 4) cp_async16(myst + n * JP + k, src + k);
+          for (int k = 0; k < JP; k += 4) cp_async16_sel(myst + n * JP + k, src + k, a.gather_ca != 0);
         }
     }
     cp_async_commit();
